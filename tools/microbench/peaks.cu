@@ -1,0 +1,213 @@
+// B3b microbenchmarks: the roofline denominators for the fp32 CUDA-core path.
+// Measures, on the box, per-SM-per-clock throughput of
+//   FFMA (3 register operands), FFMA (immediate operand), FFMA (constant-bank operand),
+//   FFMA2 (fma.rn.f32x2), LDS.128 (conflict-free), and the rho=1 SpMM inner loop
+//   (one LDS.128 of X + 2 FFMA2 per nonzero, metadata broadcast from smem).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o peaks peaks.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
+
+__constant__ float c_w[64];
+
+constexpr int ITERS = 4096;
+
+__global__ void k_ffma_reg(float* out, float w0, float w1, long long* clk) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  float x = w0 + threadIdx.x, y = w1 * (threadIdx.x + 1);
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) asm volatile("fma.rn.f32 %0, %1, %2, %0;" : "+f"(a[i]) : "f"(x), "f"(y));
+  }
+  long long t1 = clock64();
+  float s = 0; for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+__global__ void k_ffma_imm(float* out, float w0, long long* clk) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  float x = w0 + threadIdx.x;
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) asm volatile("fma.rn.f32 %0, %1, 0f3F9E0652, %0;" : "+f"(a[i]) : "f"(x));
+  }
+  long long t1 = clock64();
+  float s = 0; for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+// distinct immediates per FMA (as generated code would have)
+__global__ void k_ffma_imm_distinct(float* out, float w0, long long* clk) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  float x = w0 + threadIdx.x, x2 = w0 - threadIdx.x;
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+    asm volatile(
+      "fma.rn.f32 %0, %16, 0f3F9E0652, %0;\n\t"
+      "fma.rn.f32 %1, %17, 0f3E9E0653, %1;\n\t"
+      "fma.rn.f32 %2, %16, 0fBF1E0654, %2;\n\t"
+      "fma.rn.f32 %3, %17, 0f3D9E0655, %3;\n\t"
+      "fma.rn.f32 %4, %16, 0f3F1E0656, %4;\n\t"
+      "fma.rn.f32 %5, %17, 0fBE9E0657, %5;\n\t"
+      "fma.rn.f32 %6, %16, 0f3C9E0658, %6;\n\t"
+      "fma.rn.f32 %7, %17, 0f3F9E0659, %7;\n\t"
+      "fma.rn.f32 %8, %16, 0f3F9E065A, %8;\n\t"
+      "fma.rn.f32 %9, %17, 0f3E9E065B, %9;\n\t"
+      "fma.rn.f32 %10, %16, 0fBF1E065C, %10;\n\t"
+      "fma.rn.f32 %11, %17, 0f3D9E065D, %11;\n\t"
+      "fma.rn.f32 %12, %16, 0f3F1E065E, %12;\n\t"
+      "fma.rn.f32 %13, %17, 0fBE9E065F, %13;\n\t"
+      "fma.rn.f32 %14, %16, 0f3C9E0660, %14;\n\t"
+      "fma.rn.f32 %15, %17, 0f3F9E0661, %15;\n\t"
+      : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(a[4]), "+f"(a[5]), "+f"(a[6]), "+f"(a[7]),
+        "+f"(a[8]), "+f"(a[9]), "+f"(a[10]), "+f"(a[11]), "+f"(a[12]), "+f"(a[13]), "+f"(a[14]), "+f"(a[15])
+      : "f"(x), "f"(x2));
+  }
+  long long t1 = clock64();
+  float s = 0; for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+__global__ void k_ffma_const(float* out, float w0, long long* clk) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  float x = w0 + threadIdx.x;
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = fmaf(x, c_w[i], a[i]);
+    x += 1e-7f;
+  }
+  long long t1 = clock64();
+  float s = 0; for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+__global__ void k_ffma2(float* out, float w0, float w1, long long* clk) {
+  float2 a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = make_float2(threadIdx.x * 1e-3f + i, i);
+  float2 x = make_float2(w0 + threadIdx.x, w0), y = make_float2(w1, w1);
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = __ffma2_rn(x, y, a[i]);
+    asm volatile("" : "+f"(x.x), "+f"(x.y), "+f"(y.x));
+  }
+  long long t1 = clock64();
+  float s = 0; for (int i = 0; i < 8; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+__global__ void k_lds128(float* out, long long* clk) {
+  __shared__ float4 buf[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_float4(i, i + 1, i + 2, i + 3);
+  __syncthreads();
+  float4 acc = make_float4(0, 0, 0, 0);
+  int lane = threadIdx.x & 31;
+  int base = (threadIdx.x >> 5) * 32;
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 v = buf[((it * 8 + j) * 32 + base + lane) & 2047];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  long long t1 = clock64();
+  if (acc.x + acc.y + acc.z + acc.w == 12345.f) out[0] = acc.x;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+// rho = 1 inner loop: per nonzero, a broadcast (col, w) from smem, an LDS.128 of X[col][4*lane..], 2 FFMA2
+template <int ROWS>
+__global__ void k_rho1(float* out, long long* clk) {
+  __shared__ float4 xs[64 * 32];       // 64 columns x 128 floats
+  __shared__ int2 meta[1024];
+  for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) xs[i] = make_float4(i, 1, 2, 3);
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) meta[i] = make_int2((i * 37) & 63, __float_as_int(0.001f * i));
+  __syncthreads();
+  int lane = threadIdx.x & 31;
+  float2 acc[ROWS][2];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) { acc[r][0] = make_float2(0, 0); acc[r][1] = make_float2(0, 0); }
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+#pragma unroll 4
+      for (int j = 0; j < 8; ++j) {
+        int2 m = meta[(it * 8 + j + r * 64) & 1023];
+        float4 x = xs[m.x * 32 + lane];
+        float w = __int_as_float(m.y);
+        float2 ww = make_float2(w, w);
+        acc[r][0] = __ffma2_rn(ww, make_float2(x.x, x.y), acc[r][0]);
+        acc[r][1] = __ffma2_rn(ww, make_float2(x.z, x.w), acc[r][1]);
+      }
+    }
+  }
+  long long t1 = clock64();
+  float s = 0;
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) s += acc[r][0].x + acc[r][0].y + acc[r][1].x + acc[r][1].y;
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+int main() {
+  int dev = 0; CK(cudaSetDevice(dev));
+  cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
+  int clk_khz = 0; cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+  printf("device %s SMs %d L2 %d MB smem/block optin %zu KB regs/SM %d clock(attr) %d MHz\n",
+         p.name, p.multiProcessorCount, p.l2CacheSize >> 20, p.sharedMemPerBlockOptin >> 10,
+         p.regsPerMultiprocessor, clk_khz / 1000);
+  float* out; long long* clk; CK(cudaMalloc(&out, 64)); CK(cudaMalloc(&clk, 64));
+  float hw[64]; for (int i = 0; i < 64; ++i) hw[i] = 0.001f * (i + 1);
+  CK(cudaMemcpyToSymbol(c_w, hw, sizeof(hw)));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int SM = p.multiProcessorCount;
+  auto report = [&](const char* name, auto launch, double ops_per_thread, int blocks, int threads, double bytes_per_thread) {
+    for (int w = 0; w < 2; ++w) launch();
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    long long c; CK(cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost));
+    double tot = ops_per_thread * blocks * threads;
+    double rate = tot / (ms * 1e-3);
+    double sec_clk = c / (ms * 1e-3);  // approx clock (block 0's loop only)
+    double per_sm_clk = ops_per_thread * (double)threads * ((double)blocks / SM) / c;
+    printf("%-22s %8.3f ms  %9.2f Gop/s  per-SM/clk(block0 clock) %7.2f  eff.clock %6.0f MHz  %s%.1f GB/s\n",
+           name, ms, rate / 1e9, per_sm_clk, sec_clk / 1e6, bytes_per_thread > 0 ? "smem " : "",
+           bytes_per_thread > 0 ? bytes_per_thread * blocks * threads / (ms * 1e-3) / 1e9 : 0.0);
+  };
+  for (int occ : {1, 2, 4}) {
+    int blocks = SM * occ, threads = 256;
+    printf("--- %d blocks x %d threads\n", blocks, threads);
+    report("ffma_reg (fma/thr)", [&] { k_ffma_reg<<<blocks, threads>>>(out, 1.f, 0.5f, clk); }, 16.0 * ITERS, blocks, threads, 0);
+    report("ffma_imm", [&] { k_ffma_imm<<<blocks, threads>>>(out, 1.f, clk); }, 16.0 * ITERS, blocks, threads, 0);
+    report("ffma_imm_distinct", [&] { k_ffma_imm_distinct<<<blocks, threads>>>(out, 1.f, clk); }, 16.0 * ITERS, blocks, threads, 0);
+    report("ffma_const", [&] { k_ffma_const<<<blocks, threads>>>(out, 1.f, clk); }, 16.0 * ITERS, blocks, threads, 0);
+    report("ffma2 (fma/thr)", [&] { k_ffma2<<<blocks, threads>>>(out, 1.f, 0.5f, clk); }, 16.0 * ITERS, blocks, threads, 0);
+    report("lds128 (B/thr)", [&] { k_lds128<<<blocks, threads>>>(out, clk); }, 8.0 * ITERS * 16, blocks, threads, 8.0 * ITERS * 16);
+    report("rho1 R4 (fma/thr)", [&] { k_rho1<4><<<blocks, threads>>>(out, clk); }, 4.0 * 8 * 4 * (ITERS / 4), blocks, threads, 0);
+    report("rho1 R8 (fma/thr)", [&] { k_rho1<8><<<blocks, threads>>>(out, clk); }, 8.0 * 8 * 4 * (ITERS / 4), blocks, threads, 0);
+  }
+  return 0;
+}
