@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""bench.py — SparseDNN hot path (Y = act(W·X + b), sdnn_spmm) on 1..8 B200s.
+
+Workload (BASELINE.json configs[4], the multi-GPU scaling config the metric is quoted on "at
+1/2/4/8 B200"): W 4096×4096 fp32, 90 % uniform sparsity (nnz 1 677 722), X 4096×262144 N(0,1)
+sharded by contiguous column blocks across ranks (W replicated, no data-path collective), bias +
+ReLU fused.  One step = one sdnn_spmm over the rank's shard (the per-request execution stage;
+sdnn_prepare is the one-time preparation stage, timed separately as prep_ms).
+
+metric: effective GFLOP/s = 2·nnz·N / t (whole job, all ranks), t = max over ranks.
+X per rank ≥ 512 MiB > 126 MB L2, so every step streams X from HBM (no flush needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import sdnn_synth as synth  # noqa: E402
+
+WORKLOAD = "c5"
+METRIC = "SpMM effective GFLOP/s (2·nnz·N) and HBM GB/s vs roofline at 1/2/4/8 B200"
+KERNEL = "spmm_tma_kernel"
+
+
+# ----------------------------------------------------------------------------- sharding / reductions
+def shard_range(N: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous column block of rank r: [r·N/g, (r+1)·N/g) with the remainder spread over the
+    first ranks, rounded so every shard but the last starts at a multiple of 4 (TMA alignment)."""
+    base = (N // world) // 4 * 4
+    starts = [r * base for r in range(world)] + [N]
+    return starts[rank], starts[rank + 1]
+
+
+def max_over_ranks(x: float, dist=None) -> float:
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return x
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def plan_hash(info: dict, perm: np.ndarray) -> str:
+    h = hashlib.sha256()
+    h.update(json.dumps({k: v for k, v in sorted(info.items()) if k != "device"}).encode())
+    h.update(np.ascontiguousarray(perm).tobytes())
+    return h.hexdigest()[:16]
+
+
+def check_same_across_ranks(s: str, dist=None) -> bool:
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return True
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, s)
+    return all(o == out[0] for o in out)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while the timed region runs."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4,
+               "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int, period: float = 0.05):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.sm_max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.sm_max = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.sm_max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(workload_key: str):
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(workload_key)
+    except Exception:
+        return None
+
+
+def fill_x(p, c0: int, c1: int, out: np.ndarray, threads: int = 16):
+    """X[:, c0:c1] into `out` (K × (c1-c0)), generated block-parallel (block-seeded, shard-invariant)."""
+    from concurrent.futures import ThreadPoolExecutor
+    B = synth.X_BLOCK
+    blocks = range(c0 // B, (c1 - 1) // B + 1)
+
+    def one(b):
+        blk = p.x_block(b)
+        s0, s1 = max(c0, b * B), min(c1, b * B + blk.shape[1])
+        out[:, s0 - c0:s1 - c0] = blk[:, s0 - b * B:s1 - b * B]
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, blocks))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(p, target_s: float = 12.0, max_cols: int = 16384):
+    """Time the oracle (as it stands, OpenMP over rows, all host cores) on a bounded column sample of
+    the workload sized to ≈ target_s seconds; returns (GFLOP/s, threads, sample description, seconds)."""
+    import oracle
+    oracle.build()
+    cols = 32
+    X = p.x_cols(0, cols)
+    t0 = time.perf_counter()
+    _, _, used = oracle.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, threads=host_cores())
+    dt = time.perf_counter() - t0
+    cols = int(min(max_cols, max(32, cols * target_s / max(dt, 1e-3))) // 32 * 32)
+    X = p.x_cols(0, cols)
+    t0 = time.perf_counter()
+    _, _, used = oracle.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, threads=host_cores())
+    dt = time.perf_counter() - t0
+    gflops = 2.0 * p.nnz * cols / dt / 1e9
+    return gflops, used, f"{WORKLOAD} W (all {p.nnz} nonzeros) on X[:, 0:{cols}] ({cols} of {p.N} columns)", dt
+
+
+# ----------------------------------------------------------------------------- reference arm (oracle)
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    p = synth.config_problem(WORKLOAD, N=args.n_total)
+    per_step = []
+    sample = None
+    cores = None
+    for i in range(args.warmup + args.steps):
+        g, cores, sample, dt = oracle_sample(p, target_s=args.ref_step_s, max_cols=4096)
+        if i >= args.warmup:
+            per_step.append((g, dt))
+    value = statistics.median([g for g, _ in per_step])
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * statistics.median([d for _, d in per_step]), 3),
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64-accumulate/f32-io",
+            "data": "synthetic (seeded; BASELINE configs[4] shapes)",
+            "config": {"workload": f"{WORKLOAD}: W 4096x4096 fp32 90% uniform, X 4096x{args.n_total}, bias+ReLU",
+                       "impl": "CPU oracle (oracle/spmm_oracle.c, fp64 CSR triple loop, OpenMP over rows)"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- product arm
+def run_product(args, rank: int, world: int, local_rank: int, dist):
+    import torch
+
+    import paper_2101_07948_b200 as sdnn
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p = synth.config_problem(WORKLOAD, N=args.n_total)
+    if args.scaling == "weak":
+        c0, c1 = 0, args.n_total
+    else:
+        c0, c1 = shard_range(args.n_total, rank, world)
+    Nr = c1 - c0
+
+    # ---- preparation stage (once): Algorithm 1 + packing + upload
+    t0 = time.perf_counter()
+    h = sdnn.Handle.from_problem(p)
+    prep_ms = 1e3 * (time.perf_counter() - t0)
+    info = h.info()
+    same = check_same_across_ranks(plan_hash(info, h.permutation()), dist)
+
+    # ---- inputs: rank's X shard generated on host (pinned), copied to HBM once
+    Xh = torch.empty((p.K, Nr), dtype=torch.float32, pin_memory=True)
+    fill_x(p, c0, c1, Xh.numpy())
+    X = Xh.to(dev, non_blocking=False)
+    bias = torch.from_numpy(p.bias).to(dev)
+    Y = torch.empty((p.M, Nr), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        h.spmm(X, bias, act=1, out=Y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps between barrier+sync, CUDA events on the launching stream
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        if dist is not None and dist.is_initialized():
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None and dist.is_initialized():
+            dist.barrier()
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_rank, dist)
+
+    # ---- parity spot check on this rank's shard (oracle on 64 sampled columns; rank 0 reports)
+    parity = None
+    if not args.no_parity:
+        import oracle
+        cols = np.unique(np.concatenate([np.arange(0, 16), np.arange(Nr - 16, Nr),
+                                         np.random.default_rng(rank).choice(Nr, 32, replace=False)]))
+        ct = torch.from_numpy(cols).to(dev)
+        Ys = Y[:, ct].cpu().numpy()
+        Xs = np.ascontiguousarray(Xh.numpy()[:, cols])
+        Yo, S, _ = oracle.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, Xs, p.bias, act=1, want_scale=True)
+        err = np.abs(Ys.astype(np.float64) - Yo) / np.where(S > 0, S, 1.0)
+        parity = max_over_ranks(float(err.max()), dist)
+
+    # ---- optional Y all-gather over NVLink (NCCL), reported separately
+    ag_ms = None
+    if args.allgather and world > 1:
+        Yall = torch.empty((world, p.M, Nr), dtype=torch.float32, device=dev)
+        for _ in range(2):
+            dist.all_gather_into_tensor(Yall, Y)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(3):
+            dist.all_gather_into_tensor(Yall, Y)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ag_ms = max_over_ranks(a0.elapsed_time(a1) / 3, dist)
+        del Yall
+
+    # ---- e2e through the public host-buffer API (H2D of X + bias, D2H of Y inside the timed region)
+    Yh = torch.empty((p.M, Nr), dtype=torch.float32, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    for _ in range(1):
+        h.spmm_host_ptr(Xh.data_ptr(), Nr, p.bias.ctypes.data, 1, Yh.data_ptr())
+    if dist is not None and dist.is_initialized():
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        h.spmm_host_ptr(Xh.data_ptr(), Nr, p.bias.ctypes.data, 1, Yh.data_ptr())
+    e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t0) / e2e_steps, dist)
+    e2e_ok = bool(torch.equal(Yh[:, :8].to(dev), Y[:, :8]))
+
+    # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        g, cores, sample, dt = oracle_sample(p, target_s=args.cpu_s)
+        cpu = {"value": round(g, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
+               "seconds": round(dt, 2)}
+
+    if rank != 0:
+        return 0
+    N_job = Nr * world if args.scaling == "weak" else args.n_total
+    flops_job = 2.0 * p.nnz * N_job
+    value = flops_job / (ms * 1e-3) / 1e9
+    flops_launch = 2.0 * p.nnz * Nr
+    achieved_tf = flops_launch / (ms_rank * 1e-3) / 1e12
+    peaks = measured_peaks()
+    sm_mhz_max = float(peaks.get("sm_max_mhz") or (clk.sm_max or 1965))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak_tf = nsm * 128 * 2 * sm_mhz_max * 1e6 / 1e12
+    alg_bytes = p.nnz * 8 + (p.K + p.M) * Nr * 4
+    hbm_gbs = alg_bytes / (ms_rank * 1e-3) / 1e9
+    hbm_peak = float(peaks.get("hbm_gbs") or 6650.0)
+    trf = ncu_traffic(f"{WORKLOAD}_g{world}_{args.scaling}")
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1) X, N(0,0.05) W, N(0,0.1) b)",
+        "config": {"workload": f"{WORKLOAD}: W {p.M}x{p.K} fp32 90% uniform (nnz {p.nnz}), X {p.K}x{args.n_total} "
+                               f"sharded by columns, bias+ReLU",
+                   "M": p.M, "K": p.K, "nnz": p.nnz, "N_total": N_job, "N_per_gpu": Nr,
+                   "parallelism": f"column-sharded x{world}, W replicated, no data-path collective",
+                   "l2": "inputs larger than L2 (X shard %.0f MiB > 126 MB L2); no flush" % (p.K * Nr * 4 / 2**20),
+                   "kernel": f"{KERNEL}<R_w={info['panel_rows']},V={'8' if info['num_row_blocks'] * ((Nr + 255) // 256) >= 296 else '4'}>",
+                   "panel_rows": info["panel_rows"], "cta_panels": info["cta_panels"], "k_chunk": info["k_chunk"],
+                   "permuted": bool(info["permuted"]), "prep_ms": round(prep_ms, 1), "plan_hash_identical": same},
+        "roofline": {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(fp32_peak_tf, 2),
+                     "unit": "TFLOP/s", "frac": round(achieved_tf / fp32_peak_tf, 4),
+                     "traffic": None if trf is None else trf.get("dram_bytes_per_launch"),
+                     "peak_source": f"fp32 FFMA: {nsm} SMs x 128 lanes x 2 flop x {sm_mhz_max:.0f} MHz "
+                                    "(B200_PROFILING unit counts, MEASURED_PEAKS sm_max_mhz; 128 FMA/clk/SM "
+                                    "re-measured in profiles/r01_microbench.log)",
+                     "hbm": {"achieved_gbs": round(hbm_gbs, 1), "peak_gbs": hbm_peak,
+                             "frac": round(hbm_gbs / hbm_peak, 4), "alg_bytes_per_launch": alg_bytes},
+                     "lds_ceiling_frac": 0.25},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(flops_job / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(p.K * Nr * 4 + p.M * 4), "d2h_bytes_per_step": int(p.M * Nr * 4),
+                "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps, "api": "sdnn_spmm_host (pinned host buffers)",
+                "matches_device_result": e2e_ok},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "parity_max_err_over_scale": parity,
+        "allgather_ms": None if ag_ms is None else round(ag_ms, 3),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["product", "reference"], default="product")
+    ap.add_argument("--n-total", type=int, default=synth.CONFIGS[WORKLOAD][2])
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
+    ap.add_argument("--allgather", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-s", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=8.0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_product(args, rank, world, local_rank, dist)
+    finally:
+        if dist is not None and dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

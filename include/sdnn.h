@@ -1,0 +1,160 @@
+/*
+ * sdnn.h — C ABI of libsdnn: the SparseDNN hot path (arXiv 2101.07948) on NVIDIA B200 (sm_100a).
+ *
+ *   Y = act(W·X + b)      W: M×K fp32 unstructured-sparse weight (CSR), X: K×N fp32 dense activation,
+ *                         b: fp32[M] bias (optional), act ∈ {NONE, RELU}, Y: M×N fp32.
+ *
+ * The operation is the paper's SpMM, "sparse matrix -- dense matrix multiplication" (PAPER.md P:62,
+ * §2.2), computed by a microkernel that broadcasts each nonzero of the sparse operand and multiplies it
+ * with the dense row slice (P:135 fig:spmm, §3.2.2), with the following elementwise layer fused
+ * (§3.1).  Work is split into a one-time preparation stage and a per-request execution stage
+ * (§2.1, §3): sdnn_prepare performs the weight permutation of Algorithm 1 (§3.1.2)
+ * and re-stores the matrix in its own execution-ordered format; sdnn_spmm runs the multiply.
+ *
+ * Conventions
+ *   - Every entry point returns sdnn_status; no C++ exception crosses the boundary.
+ *   - "host" pointers are ordinary CPU memory; "device" pointers are CUDA global memory on the
+ *     handle's device.  Matrices are row-major and contiguous: X is K×N (row stride N floats),
+ *     Y is M×N (row stride N floats).  Indices are int32; sizes of N are int64.
+ *   - A failing call leaves outputs untouched where possible and sets a thread-local message
+ *     readable with sdnn_last_error_message().
+ *   - Numerics: fp32 FMA accumulation on CUDA cores in a fixed order (bitwise reproducible for the
+ *     same handle and inputs); accuracy contract |Y − Y_exact| ≤ 1e-4 · (Σ|w||x| + |b|) per element
+ *     (BASELINE.json north_star, reading C9).
+ */
+#ifndef SDNN_H_
+#define SDNN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDNN_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SDNN_API __attribute__((visibility("default")))
+#else
+#define SDNN_API
+#endif
+
+typedef enum {
+  SDNN_OK = 0,
+  SDNN_ERR_INVALID_ARGUMENT = 1, /* NULL where not allowed, negative size, unknown act, aliasing  */
+  SDNN_ERR_INVALID_CSR = 2,      /* CSR invariants violated (message names the first bad row)      */
+  SDNN_ERR_UNSUPPORTED = 3,      /* valid input this build cannot run (e.g. device is not sm_100)  */
+  SDNN_ERR_OUT_OF_MEMORY = 4,    /* host or device allocation failed                              */
+  SDNN_ERR_CUDA = 5,             /* a CUDA runtime/driver call or kernel launch failed            */
+  SDNN_ERR_DEVICE_MISMATCH = 6,  /* current device differs from the handle's device               */
+  SDNN_ERR_INTERNAL = 7
+} sdnn_status;
+
+typedef enum { SDNN_ACT_NONE = 0, SDNN_ACT_RELU = 1 } sdnn_act;
+
+/* Preparation options.  Pass NULL for defaults.  struct_size must be sizeof(sdnn_perm_opts). */
+typedef struct {
+  uint32_t struct_size;
+  int32_t permute;          /* 1 (default): Algorithm 1 greedy row reorder; 0: identity   */
+  int32_t panel_rows_max;   /* rows per warp panel: 0 = auto, else 4 or 8                            */
+  int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
+  int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
+                               multiple of 8                                                        */
+  uint32_t flags;           /* reserved, must be 0                                                   */
+} sdnn_perm_opts;
+
+/* Read-only description of a prepared handle (or a host plan). */
+typedef struct {
+  uint32_t struct_size;     /* in: sizeof(sdnn_info)                                                 */
+  int32_t M, K;
+  int64_t nnz;
+  int32_t device;           /* CUDA ordinal, −1 for a host-only plan                                  */
+  int32_t permuted;         /* 1 if Algorithm 1 was applied                                           */
+  int32_t panel_rows;       /* R_w: rows per warp panel                                               */
+  int32_t cta_panels;       /* W_c: panels per CTA                                                    */
+  int32_t num_panels;       /* P = num_row_blocks · W_c (trailing panels may be empty)               */
+  int32_t num_row_blocks;   /* ⌈M / (R_w·W_c)⌉                                                        */
+  int32_t k_chunk;          /* KC                                                                     */
+  int32_t num_chunks;       /* ⌈K / KC⌉                                                               */
+  int64_t meta_bytes;       /* device bytes of the execution-ordered stream                           */
+  int32_t max_block_bytes;  /* largest (row block, chunk) metadata block, bytes                       */
+  int32_t reserved0;
+  int64_t max_panel_nnz;
+} sdnn_info;
+
+typedef struct sdnn_handle_s* sdnn_handle; /* opaque; owns its device memory; immutable after prepare */
+typedef struct sdnn_plan_s* sdnn_plan;     /* opaque host-only plan (no device needed)               */
+
+/* ------------------------------------------------------------------ preparation (once per weight)
+ * sdnn_prepare: validate the CSR (row_ptr[0] = 0, nondecreasing, row_ptr[M] = nnz < 2^31,
+ * 0 ≤ col < K, strictly increasing columns per row; explicit zero values are kept as structural
+ * nonzeros, reading C6), apply Algorithm 1 (opts->permute), pack the permuted rows into
+ * warp panels and the execution-ordered per-(row block, K chunk) metadata stream, and
+ * upload it to the CURRENT CUDA device.  All three arrays are HOST pointers, read during the call
+ * only.  nnz = 0 is allowed (Y = act(b)).  Synchronous; deterministic (same input → bit-identical
+ * device arrays).  Errors: INVALID_ARGUMENT (NULL out, M < 1, K < 1, NULL arrays with nnz > 0,
+ * bad opts), INVALID_CSR, UNSUPPORTED (device is not compute capability 10.0), OUT_OF_MEMORY, CUDA. */
+SDNN_API sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M,
+                         int32_t K, const sdnn_perm_opts* perm_opts, sdnn_handle* out);
+
+/* Release a handle.  NULL is a no-op.  The caller must ensure no sdnn_spmm on it is in flight. */
+SDNN_API sdnn_status sdnn_destroy(sdnn_handle h);
+
+/* ------------------------------------------------------------------ execution (per request)
+ * sdnn_spmm: Y = act(W·X + b) on DEVICE buffers of the handle's device.
+ *   X     device, K×N row-major fp32 (exactly the handle's K rows; caller guarantees ≥ K·N floats)
+ *   N     ≥ 0 columns; N = 0 returns SDNN_OK without work
+ *   bias  device fp32[M] in ORIGINAL row order, or NULL for no bias
+ *   act   SDNN_ACT_NONE or SDNN_ACT_RELU
+ *   Y     device, M×N row-major fp32, written in ORIGINAL row order (the permutation is invisible);
+ *         must not overlap X or bias
+ *   stream cudaStream_t (NULL = legacy default stream).  The call enqueues and returns without a
+ *         host synchronisation; device faults surface at the caller's next sync.
+ * Fast path: X and Y 16-byte aligned and N % 4 == 0 (TMA tiles); otherwise a slower correct path.
+ * Errors: INVALID_ARGUMENT (NULL handle/X/Y, N < 0, bad act, Y overlapping X or bias),
+ * DEVICE_MISMATCH (current device ≠ handle device), CUDA (launch failure). */
+SDNN_API sdnn_status sdnn_spmm(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
+                      void* stream);
+
+/* sdnn_spmm_host: the same operation on HOST buffers (X host K×N, bias host fp32[M] or NULL, Y host
+ * M×N).  Columns are processed in blocks of `block_cols` (0 = auto), with host→device copy, kernel
+ * and device→host copy of successive blocks overlapped on internal streams; pinned (page-locked)
+ * host buffers give full PCIe/C2C bandwidth.  Synchronous: returns after Y is complete in host
+ * memory.  Uses the current device (must be the handle's).  Errors as sdnn_spmm plus OUT_OF_MEMORY. */
+SDNN_API sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const float* bias_host, int32_t act,
+                           float* Y_host, int64_t block_cols);
+
+/* ------------------------------------------------------------------ introspection
+ * sdnn_get_permutation: out_perm (HOST, M entries) receives order[i] = original row at permuted
+ * position i (Algorithm 1 output, SPEC S:295 convention).  sdnn_get_info fills *info. */
+SDNN_API sdnn_status sdnn_get_permutation(sdnn_handle h, int32_t* out_perm);
+SDNN_API sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info);
+
+/* ------------------------------------------------------------------ host-only planning (no GPU)
+ * sdnn_permutation: Algorithm 1 alone, on host CSR, inverted-index implementation;
+ * order[M] (HOST) receives the permutation; ties → lowest original row (readings C2, C3).
+ * Validates the CSR like sdnn_prepare. */
+SDNN_API sdnn_status sdnn_permutation(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K,
+                             int32_t* order);
+
+/* sdnn_plan_create: everything sdnn_prepare does except the upload, on host.  sdnn_plan_export
+ * copies the plan's arrays into caller HOST buffers sized from sdnn_plan_get_info:
+ *   row_orig  int32[num_panels·panel_rows]  original row of each panel slot, −1 for empty slots
+ *   blk_off   int64[num_row_blocks·num_chunks + 1] byte offset of each metadata block in `meta`
+ *   meta      uint8[meta_bytes]  execution-ordered blocks; see DESIGN.md "Execution-ordered format"
+ * Any export pointer may be NULL to skip it.  Used by the packing-invariant tests. */
+SDNN_API sdnn_status sdnn_plan_create(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M,
+                             int32_t K, const sdnn_perm_opts* perm_opts, sdnn_plan* out);
+SDNN_API sdnn_status sdnn_plan_get_info(sdnn_plan p, sdnn_info* info);
+SDNN_API sdnn_status sdnn_plan_export(sdnn_plan p, int32_t* row_orig, int64_t* blk_off, uint8_t* meta);
+SDNN_API sdnn_status sdnn_plan_destroy(sdnn_plan p);
+
+/* ------------------------------------------------------------------ errors / version */
+SDNN_API const char* sdnn_status_string(sdnn_status s);
+SDNN_API const char* sdnn_last_error_message(void); /* thread-local; "" if none */
+SDNN_API int32_t sdnn_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDNN_H_ */

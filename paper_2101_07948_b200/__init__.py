@@ -1,0 +1,219 @@
+"""paper_2101_07948_b200 — thin Python binding of libsdnn (include/sdnn.h).
+
+Argument marshalling only: every step of the hot path (Algorithm 1, packing, the SpMM kernel, the
+fused epilogue) runs inside libsdnn.so.  PyTorch supplies device memory and streams.  There is no
+CPU fallback: if the in-tree library is missing this module raises on import; build it with
+`python -m paper_2101_07948_b200.build` or `__graft_entry__.build()`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsdnn.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libsdnn.so not built at {LIB_PATH}; run `python -m paper_2101_07948_b200.build`")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+ACT_NONE, ACT_RELU = 0, 1
+STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR", 3: "SDNN_ERR_UNSUPPORTED",
+          4: "SDNN_ERR_OUT_OF_MEMORY", 5: "SDNN_ERR_CUDA", 6: "SDNN_ERR_DEVICE_MISMATCH", 7: "SDNN_ERR_INTERNAL"}
+
+# exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
+EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_host", "sdnn_get_permutation", "sdnn_get_info",
+           "sdnn_permutation", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_destroy",
+           "sdnn_status_string", "sdnn_last_error_message", "sdnn_abi_version"]
+
+
+class SdnnError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.sdnn_last_error_message().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PermOpts(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("permute", ctypes.c_int32), ("panel_rows_max", ctypes.c_int32),
+                ("cta_panels", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("M", ctypes.c_int32), ("K", ctypes.c_int32),
+                ("nnz", ctypes.c_int64), ("device", ctypes.c_int32), ("permuted", ctypes.c_int32),
+                ("panel_rows", ctypes.c_int32), ("cta_panels", ctypes.c_int32), ("num_panels", ctypes.c_int32),
+                ("num_row_blocks", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
+                ("meta_bytes", ctypes.c_int64), ("max_block_bytes", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("max_panel_nnz", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f not in ("struct_size", "reserved0")}
+
+
+_vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+_lib.sdnn_prepare.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts), ctypes.POINTER(_vp)]
+_lib.sdnn_destroy.argtypes = [_vp]
+_lib.sdnn_spmm.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _vp]
+_lib.sdnn_spmm_host.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64]
+_lib.sdnn_get_permutation.argtypes = [_vp, _vp]
+_lib.sdnn_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
+_lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
+_lib.sdnn_plan_create.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts), ctypes.POINTER(_vp)]
+_lib.sdnn_plan_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
+_lib.sdnn_plan_export.argtypes = [_vp, _vp, _vp, _vp]
+_lib.sdnn_plan_destroy.argtypes = [_vp]
+_lib.sdnn_status_string.restype = ctypes.c_char_p
+_lib.sdnn_last_error_message.restype = ctypes.c_char_p
+_lib.sdnn_abi_version.restype = ctypes.c_int32
+for _f in EXPORTS:
+    if _f not in ("sdnn_status_string", "sdnn_last_error_message", "sdnn_abi_version"):
+        getattr(_lib, _f).restype = ctypes.c_int
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise SdnnError(st, where)
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _csr(row_ptr, col_idx, vals):
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    v = None if vals is None else np.ascontiguousarray(vals, dtype=np.float32)
+    return rp, ci, v
+
+
+def _opts(permute=True, panel_rows=0, cta_panels=0, k_chunk=0):
+    return PermOpts(ctypes.sizeof(PermOpts), int(bool(permute)), int(panel_rows), int(cta_panels), int(k_chunk), 0)
+
+
+def _act(act) -> int:
+    if isinstance(act, str):
+        return {"none": ACT_NONE, "relu": ACT_RELU}[act.lower()]
+    return int(act)
+
+
+def permutation(row_ptr, col_idx, M: int, K: int) -> np.ndarray:
+    """Algorithm 1 on host via libsdnn (no GPU needed)."""
+    rp, ci, _ = _csr(row_ptr, col_idx, None)
+    order = np.empty(M, dtype=np.int32)
+    _check(_lib.sdnn_permutation(_np_ptr(rp), _np_ptr(ci), M, K, _np_ptr(order)), "sdnn_permutation")
+    return order
+
+
+class Plan:
+    """Host-only plan (sdnn_plan_*): the prepared execution-ordered format without a device."""
+
+    def __init__(self, row_ptr, col_idx, vals, M: int, K: int, **opts):
+        rp, ci, v = _csr(row_ptr, col_idx, vals)
+        h = _vp()
+        o = _opts(**opts)
+        _check(_lib.sdnn_plan_create(_np_ptr(rp), _np_ptr(ci), _np_ptr(v), M, K, ctypes.byref(o), ctypes.byref(h)),
+               "sdnn_plan_create")
+        self._h = h
+
+    def info(self) -> dict:
+        i = Info()
+        i.struct_size = ctypes.sizeof(Info)
+        _check(_lib.sdnn_plan_get_info(self._h, ctypes.byref(i)), "sdnn_plan_get_info")
+        return i.as_dict()
+
+    def export(self):
+        i = self.info()
+        row_orig = np.empty(i["num_panels"] * i["panel_rows"], np.int32)
+        blk_off = np.empty(i["num_row_blocks"] * i["num_chunks"] + 1, np.int64)
+        meta = np.empty(i["meta_bytes"], np.uint8)
+        _check(_lib.sdnn_plan_export(self._h, _np_ptr(row_orig), _np_ptr(blk_off), _np_ptr(meta)), "sdnn_plan_export")
+        return row_orig, blk_off, meta
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sdnn_plan_destroy(self._h)
+            self._h = None
+
+
+class Handle:
+    """sdnn_prepare on the current CUDA device; .spmm runs the kernel on torch CUDA tensors."""
+
+    def __init__(self, row_ptr, col_idx, vals, M: int, K: int, **opts):
+        rp, ci, v = _csr(row_ptr, col_idx, vals)
+        self.M, self.K = int(M), int(K)
+        h = _vp()
+        o = _opts(**opts)
+        _check(_lib.sdnn_prepare(_np_ptr(rp), _np_ptr(ci), _np_ptr(v), M, K, ctypes.byref(o), ctypes.byref(h)),
+               "sdnn_prepare")
+        self._h = h
+
+    @classmethod
+    def from_problem(cls, p, **opts):
+        return cls(p.row_ptr, p.col_idx, p.vals, p.M, p.K, **opts)
+
+    def info(self) -> dict:
+        i = Info()
+        i.struct_size = ctypes.sizeof(Info)
+        _check(_lib.sdnn_get_info(self._h, ctypes.byref(i)), "sdnn_get_info")
+        return i.as_dict()
+
+    def permutation(self) -> np.ndarray:
+        out = np.empty(self.M, np.int32)
+        _check(_lib.sdnn_get_permutation(self._h, _np_ptr(out)), "sdnn_get_permutation")
+        return out
+
+    def spmm(self, X, bias=None, act="relu", out=None, stream=None):
+        """Y = act(W·X + b) for a CUDA float32 K×N tensor X (row-major contiguous)."""
+        import torch
+        if X.dim() != 2 or X.shape[0] != self.K or X.dtype != torch.float32 or not X.is_cuda:
+            raise ValueError(f"X must be a CUDA float32 tensor of shape ({self.K}, N)")
+        if not X.is_contiguous():
+            raise ValueError("X must be contiguous (row-major K×N)")
+        N = X.shape[1]
+        if out is None:
+            out = torch.empty((self.M, N), dtype=torch.float32, device=X.device)
+        elif out.shape != (self.M, N) or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float32 (M, N) tensor")
+        if bias is not None and (bias.numel() != self.M or bias.dtype != torch.float32 or not bias.is_cuda
+                                 or not bias.is_contiguous()):
+            raise ValueError("bias must be a contiguous CUDA float32 tensor of M elements")
+        s = torch.cuda.current_stream(X.device) if stream is None else stream
+        _check(_lib.sdnn_spmm(self._h, X.data_ptr(), N, None if bias is None else bias.data_ptr(), _act(act),
+                              out.data_ptr(), s.cuda_stream), "sdnn_spmm")
+        return out
+
+    def spmm_host(self, X: np.ndarray, bias: np.ndarray | None = None, act="relu", out: np.ndarray | None = None,
+                  block_cols: int = 0):
+        """The same operation on host arrays (sdnn_spmm_host); synchronous."""
+        if X.dtype != np.float32 or X.ndim != 2 or X.shape[0] != self.K or not X.flags.c_contiguous:
+            raise ValueError("X must be a C-contiguous float32 (K, N) array")
+        N = X.shape[1]
+        if out is None:
+            out = np.empty((self.M, N), np.float32)
+        if out.dtype != np.float32 or out.shape != (self.M, N) or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32 (M, N) array")
+        if bias is not None:
+            bias = np.ascontiguousarray(bias, dtype=np.float32)
+        _check(_lib.sdnn_spmm_host(self._h, X.ctypes.data, N, _np_ptr(bias), _act(act), out.ctypes.data,
+                                   int(block_cols)), "sdnn_spmm_host")
+        return out
+
+    def spmm_host_ptr(self, x_ptr: int, N: int, bias_ptr, act, y_ptr: int, block_cols: int = 0):
+        """sdnn_spmm_host on raw host pointers (e.g. pinned torch CPU tensors)."""
+        _check(_lib.sdnn_spmm_host(self._h, x_ptr, N, bias_ptr, _act(act), y_ptr, int(block_cols)), "sdnn_spmm_host")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.sdnn_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def abi_version() -> int:
+    return _lib.sdnn_abi_version()

@@ -1,0 +1,48 @@
+// sdnn_internal.h — shared by the product sources of libsdnn only (never by oracle/).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sdnn.h"
+
+namespace sdnn {
+
+// Thread-local error detail behind sdnn_last_error_message().
+void set_error(const std::string& msg);
+sdnn_status fail(sdnn_status s, const std::string& msg);
+
+// Host-side result of preparation ("execution-ordered format"):
+//   row_orig[num_panels * panel_rows]  original row per panel slot (−1: empty slot)
+//   blk_off[num_row_blocks * num_chunks + 1]  byte offsets of the (row block, chunk) blocks in meta
+//   meta: per block, a header of R_cta = cta_panels·panel_rows uint32 words
+//         (start_entry << 16 | count) padded to 16 B, then 8-byte entries {uint32 col_local, float w}
+//         with every row segment starting at an even entry (16-byte aligned pairs).
+struct Plan {
+  int32_t M = 0, K = 0;
+  int64_t nnz = 0;
+  int32_t permuted = 0;
+  int32_t panel_rows = 0, cta_panels = 0, num_panels = 0, num_row_blocks = 0;
+  int32_t k_chunk = 0, num_chunks = 0;
+  int32_t max_block_bytes = 0;
+  int64_t max_panel_nnz = 0;
+  int64_t meta_size_uploaded = 0;
+  std::vector<int32_t> perm;      // order[i] = original row at permuted position i
+  std::vector<int32_t> row_orig;
+  std::vector<int64_t> blk_off;
+  std::vector<uint8_t> meta;
+};
+
+sdnn_status validate_csr(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K);
+// Algorithm 1 with an inverted index; order must hold M entries.
+void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K, int32_t* order);
+sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
+                       const sdnn_perm_opts* opts, Plan& plan);
+
+// Shared-memory budget used for the X/metadata stage ring (bytes) and the fixed CTA layout.
+constexpr int kSmemBudget = 220 * 1024;
+constexpr int kMaxTN = 256;  // widest N tile (V = 8 floats per lane)
+
+inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace sdnn

@@ -1,0 +1,558 @@
+// sdnn_spmm.cu — device side of libsdnn for B200 (sm_100a): upload of the prepared plan
+// (sdnn_prepare), the SpMM kernels and their launch (sdnn_spmm, sdnn_spmm_host).
+//
+// Kernel: one CTA owns a row block of W_c warp panels (R_w permuted rows each)
+// and one N tile of TN = 32·V columns.  A producer warp streams the reduction dimension in chunks of
+// KC rows ("split-K" tiling along the reduction dimension): per chunk one TMA tile
+// load of X[k0:k0+KC, n0:n0+TN] plus one bulk copy of the chunk's execution-ordered metadata block
+// into a ring of shared-memory stages, completed on an mbarrier.  Each consumer warp then,
+// for every nonzero of its rows in the chunk, broadcasts the weight and FMAs it with the X row slice
+// read from shared memory into statically indexed accumulator registers (the SpMM microkernel of
+// P:135 fig:spmm / P:139 §3.2.2), in ascending column order.  The fused epilogue adds the bias,
+// applies ReLU (§3.1) and stores each row to its ORIGINAL position (inverse of the Algorithm 1
+// permutation).  No tensor cores (unstructured sparsity is not a dense contraction; north_star).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sdnn_internal.h"
+
+namespace sdnn {
+void plan_fill_info(const Plan& p, int32_t device, sdnn_info* info);
+}
+using namespace sdnn;
+
+struct sdnn_handle_s {
+  Plan plan;            // host copy (meta cleared after upload to save memory)
+  int32_t device = -1;
+  uint8_t* d_meta = nullptr;
+  int64_t* d_blk_off = nullptr;
+  int32_t* d_row_orig = nullptr;
+};
+
+// ------------------------------------------------------------------------------------------------
+// PTX helpers (mbarrier, TMA, bulk copy)
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct KParams {
+  const uint8_t* meta;
+  const int64_t* blk_off;
+  const int32_t* row_orig;
+  const float* X;  // fallback kernel only
+  const float* bias;
+  float* Y;
+  int64_t N;
+  int32_t K, nch, kc, wc, nrb, stages;
+  int32_t x_stage_bytes, m_stage_bytes, hdr_bytes;
+  int32_t act;
+};
+
+// Consume one chunk: for each of the warp's RW rows, every (col, w) entry of the chunk:
+// acc[r] += w · X_stage[col][lane·4 .. +4] (and +128 for V = 8), ascending column order.
+template <int RW, int V>
+__device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const float* __restrict__ xs,
+                                              const uint8_t* __restrict__ ms, int warp, int lane, int hdr_bytes) {
+  constexpr int TN = 32 * V;
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + warp * RW;
+  const float4* ent = reinterpret_cast<const float4*>(ms + hdr_bytes);
+  const float* xl = xs + lane * 4;
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const uint32_t h = hdr[r];
+    const int cnt = int(h & 0xffffu);
+    const float4* e = ent + (h >> 16) / 2;
+    for (int i = 0; i < cnt; i += 2) {
+      const float4 ee = e[i >> 1];
+      {
+        const float* xp = xl + __float_as_int(ee.x) * TN;
+        const float2 w2 = make_float2(ee.y, ee.y);
+        const float4 x0 = *reinterpret_cast<const float4*>(xp);
+        acc[r][0] = __ffma2_rn(w2, make_float2(x0.x, x0.y), acc[r][0]);
+        acc[r][1] = __ffma2_rn(w2, make_float2(x0.z, x0.w), acc[r][1]);
+        if constexpr (V == 8) {
+          const float4 x1 = *reinterpret_cast<const float4*>(xp + 128);
+          acc[r][2] = __ffma2_rn(w2, make_float2(x1.x, x1.y), acc[r][2]);
+          acc[r][3] = __ffma2_rn(w2, make_float2(x1.z, x1.w), acc[r][3]);
+        }
+      }
+      if (i + 1 < cnt) {
+        const float* xp = xl + __float_as_int(ee.z) * TN;
+        const float2 w2 = make_float2(ee.w, ee.w);
+        const float4 x0 = *reinterpret_cast<const float4*>(xp);
+        acc[r][0] = __ffma2_rn(w2, make_float2(x0.x, x0.y), acc[r][0]);
+        acc[r][1] = __ffma2_rn(w2, make_float2(x0.z, x0.w), acc[r][1]);
+        if constexpr (V == 8) {
+          const float4 x1 = *reinterpret_cast<const float4*>(xp + 128);
+          acc[r][2] = __ffma2_rn(w2, make_float2(x1.x, x1.y), acc[r][2]);
+          acc[r][3] = __ffma2_rn(w2, make_float2(x1.z, x1.w), acc[r][3]);
+        }
+      }
+    }
+  }
+}
+
+// Fused epilogue: y = acc + b[orig]; ReLU; store to Y[orig][n0 + ...] (inverse permutation).
+template <int RW, int V, bool VEC>
+__device__ __forceinline__ void epilogue(const float2 (&acc)[RW][V / 2], const KParams& p, int panel, int lane,
+                                         int64_t n0) {
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int32_t orow = p.row_orig[panel * RW + r];
+    if (orow < 0) continue;
+    const float b = p.bias ? p.bias[orow] : 0.f;
+    float* yrow = p.Y + int64_t(orow) * p.N;
+#pragma unroll
+    for (int h = 0; h < V / 4; ++h) {
+      const int64_t n = n0 + h * 128 + lane * 4;
+      float v[4] = {acc[r][2 * h].x + b, acc[r][2 * h].y + b, acc[r][2 * h + 1].x + b, acc[r][2 * h + 1].y + b};
+      if (p.act == SDNN_ACT_RELU) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = v[q] > 0.f ? v[q] : 0.f;
+      }
+      if (VEC) {
+        if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (n + q < p.N) yrow[n + q] = v[q];
+      }
+    }
+  }
+}
+
+// Fast path: TMA producer warp + W_c consumer warps, mbarrier stage ring.
+template <int RW, int V>
+__global__ void __launch_bounds__(17 * 32, 1) spmm_tma_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int TN = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = blockIdx.x % p.nrb;
+  const int64_t tile = blockIdx.x / p.nrb;
+  const int64_t n0 = tile * TN;
+  const int S = p.stages;
+  uint8_t* xstage = smem;
+  uint8_t* mstage = smem + size_t(S) * p.x_stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(mstage + size_t(S) * p.m_stage_bytes);
+  uint64_t* empty = full + S;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], p.wc);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == p.wc) {  // producer
+    if (lane == 0) {
+      const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
+      for (int j = 0; j < p.nch; ++j) {
+        const int s = j % S;
+        if (j >= S) mbar_wait(&empty[s], ((j / S) - 1) & 1);
+        const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
+        mbar_expect_tx(&full[s], uint32_t(p.x_stage_bytes) + mbytes);
+        tma_load_2d(xstage + size_t(s) * p.x_stage_bytes, &tmap, int32_t(n0), j * p.kc, &full[s]);
+        bulk_load(mstage + size_t(s) * p.m_stage_bytes, p.meta + off[j], mbytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  float2 acc[RW][V / 2];
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) acc[r][q] = make_float2(0.f, 0.f);
+
+  for (int j = 0; j < p.nch; ++j) {
+    const int s = j % S;
+    mbar_wait(&full[s], (j / S) & 1);
+    consume_chunk<RW, V>(acc, reinterpret_cast<const float*>(xstage + size_t(s) * p.x_stage_bytes),
+                         mstage + size_t(s) * p.m_stage_bytes, warp, lane, p.hdr_bytes);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  (void)TN;
+  epilogue<RW, V, true>(acc, p, rb * p.wc + warp, lane, n0);
+}
+
+// Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
+// threads using bounds-checked loads (zero fill) and a block barrier instead of TMA/mbarriers.
+template <int RW, int V>
+__global__ void __launch_bounds__(16 * 32, 1) spmm_generic_kernel(const KParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int TN = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = blockIdx.x % p.nrb;
+  const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
+  float* xs = reinterpret_cast<float*>(smem);
+  uint8_t* ms = smem + p.x_stage_bytes;
+  const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
+  const int nthr = blockDim.x;
+
+  float2 acc[RW][V / 2];
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) acc[r][q] = make_float2(0.f, 0.f);
+
+  for (int j = 0; j < p.nch; ++j) {
+    __syncthreads();
+    const int k0 = j * p.kc;
+    for (int idx = threadIdx.x; idx < p.kc * TN; idx += nthr) {
+      const int kk = idx / TN, nn = idx % TN;
+      const int64_t k = k0 + kk, n = n0 + nn;
+      xs[idx] = (k < p.K && n < p.N) ? p.X[k * p.N + n] : 0.f;
+    }
+    const int32_t mbytes = int32_t(off[j + 1] - off[j]);
+    const uint4* src = reinterpret_cast<const uint4*>(p.meta + off[j]);
+    for (int idx = threadIdx.x; idx < mbytes / 16; idx += nthr) reinterpret_cast<uint4*>(ms)[idx] = src[idx];
+    __syncthreads();
+    consume_chunk<RW, V>(acc, xs, ms, warp, lane, p.hdr_bytes);
+  }
+  epilogue<RW, V, false>(acc, p, rb * p.wc + warp, lane, n0);
+}
+
+// ------------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------------
+#define SDNN_CUDA_TRY(call)                                                                            \
+  do {                                                                                                 \
+    cudaError_t e_ = (call);                                                                           \
+    if (e_ != cudaSuccess) return fail(SDNN_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(f);
+  });
+  return fn;
+}
+
+template <int RW, int V>
+static cudaError_t set_smem_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(spmm_tma_kernel<RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBudget + 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(spmm_generic_kernel<RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kSmemBudget + 1024);
+}
+
+static sdnn_status launch(const sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
+                          cudaStream_t stream) {
+  const Plan& pl = h->plan;
+  const int rw = pl.panel_rows, wc = pl.cta_panels;
+  // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
+  int V = 8;
+  if (int64_t(pl.num_row_blocks) * ((N + 255) / 256) < 2 * 148) V = 4;
+  const int TN = 32 * V;
+  const int64_t ntiles = (N + TN - 1) / TN;
+  const int64_t nblocks = ntiles * pl.num_row_blocks;
+  if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "N too large for one launch");
+
+  KParams p{};
+  p.meta = h->d_meta;
+  p.blk_off = h->d_blk_off;
+  p.row_orig = h->d_row_orig;
+  p.X = X;
+  p.bias = bias;
+  p.Y = Y;
+  p.N = N;
+  p.K = pl.K;
+  p.nch = pl.num_chunks;
+  p.kc = pl.k_chunk;
+  p.wc = wc;
+  p.nrb = pl.num_row_blocks;
+  p.x_stage_bytes = int32_t(align_up(int64_t(pl.k_chunk) * TN * 4, 128));
+  p.m_stage_bytes = int32_t(align_up(pl.max_block_bytes, 128));
+  p.hdr_bytes = int32_t(align_up(int64_t(rw) * wc * 4, 16));
+  p.act = act;
+
+  const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+  if (fast) {
+    int S = int(kSmemBudget / (p.x_stage_bytes + p.m_stage_bytes));
+    S = std::min(S, std::min(pl.num_chunks, 4));
+    if (S < 1) return fail(SDNN_ERR_INTERNAL, "stage does not fit shared memory");
+    p.stages = S;
+    const size_t smem = size_t(S) * (p.x_stage_bytes + p.m_stage_bytes) + size_t(2 * S) * 8;
+    PFN_encodeTiled enc = get_encode_fn();
+    if (!enc) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap tmap;
+    const cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(pl.K)};
+    const cuuint64_t strides[1] = {cuuint64_t(N) * 4};
+    const cuuint32_t box[2] = {cuuint32_t(TN), cuuint32_t(pl.k_chunk)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
+    const dim3 grid{unsigned(nblocks)}, block{unsigned((wc + 1) * 32)};
+    if (rw == 8 && V == 8) spmm_tma_kernel<8, 8><<<grid, block, smem, stream>>>(tmap, p);
+    else if (rw == 8 && V == 4) spmm_tma_kernel<8, 4><<<grid, block, smem, stream>>>(tmap, p);
+    else if (rw == 4 && V == 8) spmm_tma_kernel<4, 8><<<grid, block, smem, stream>>>(tmap, p);
+    else spmm_tma_kernel<4, 4><<<grid, block, smem, stream>>>(tmap, p);
+  } else {
+    p.stages = 1;
+    const size_t smem = size_t(p.x_stage_bytes) + p.m_stage_bytes;
+    const dim3 grid{unsigned(nblocks)}, block{unsigned(wc * 32)};
+    if (rw == 8 && V == 8) spmm_generic_kernel<8, 8><<<grid, block, smem, stream>>>(p);
+    else if (rw == 8 && V == 4) spmm_generic_kernel<8, 4><<<grid, block, smem, stream>>>(p);
+    else if (rw == 4 && V == 8) spmm_generic_kernel<4, 8><<<grid, block, smem, stream>>>(p);
+    else spmm_generic_kernel<4, 4><<<grid, block, smem, stream>>>(p);
+  }
+  SDNN_CUDA_TRY(cudaGetLastError());
+  return SDNN_OK;
+}
+
+static bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+  if (!a || !b || !an || !bn) return false;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return a0 < b0 + bn && b0 < a0 + an;
+}
+
+static sdnn_status check_device(const sdnn_handle_s* h) {
+  int dev = -1;
+  SDNN_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != h->device)
+    return fail(SDNN_ERR_DEVICE_MISMATCH, "current device " + std::to_string(dev) + " != handle device " +
+                                              std::to_string(h->device));
+  return SDNN_OK;
+}
+
+extern "C" {
+
+sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
+                         const sdnn_perm_opts* perm_opts, sdnn_handle* out) {
+  if (!out) return fail(SDNN_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  int dev = -1;
+  SDNN_CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  SDNN_CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(SDNN_ERR_UNSUPPORTED, "libsdnn is built for sm_100a (B200); device is sm_" +
+                                          std::to_string(prop.major) + std::to_string(prop.minor));
+  sdnn_handle_s* h = new (std::nothrow) sdnn_handle_s;
+  if (!h) return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
+  sdnn_status st = build_plan(csr_ptr, col_idx, vals, M, K, perm_opts, h->plan);
+  if (st != SDNN_OK) {
+    delete h;
+    return st;
+  }
+  h->device = dev;
+  static std::once_flag attr_once[64];
+  cudaError_t ae = cudaSuccess;
+  std::call_once(attr_once[dev & 63], [&] {
+    ae = set_smem_attrs<8, 8>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<8, 4>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<4, 8>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<4, 4>();
+  });
+  auto cleanup = [&](sdnn_status s, const std::string& m) {
+    cudaFree(h->d_meta);
+    cudaFree(h->d_blk_off);
+    cudaFree(h->d_row_orig);
+    delete h;
+    return fail(s, m);
+  };
+  if (ae != cudaSuccess) return cleanup(SDNN_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ae));
+  Plan& pl = h->plan;
+  const size_t mbytes = std::max<size_t>(pl.meta.size(), 16);
+  cudaError_t e = cudaMalloc(&h->d_meta, mbytes);
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_blk_off, pl.blk_off.size() * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_row_orig, pl.row_orig.size() * 4);
+  if (e != cudaSuccess)
+    return cleanup(e == cudaErrorMemoryAllocation ? SDNN_ERR_OUT_OF_MEMORY : SDNN_ERR_CUDA,
+                   std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  if (!pl.meta.empty()) e = cudaMemcpy(h->d_meta, pl.meta.data(), pl.meta.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_blk_off, pl.blk_off.data(), pl.blk_off.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(h->d_row_orig, pl.row_orig.data(), pl.row_orig.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cleanup(SDNN_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+  pl.meta_size_uploaded = int64_t(pl.meta.size());
+  std::vector<uint8_t>().swap(pl.meta);
+  *out = h;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_destroy(sdnn_handle h) {
+  if (!h) return SDNN_OK;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != h->device) cudaSetDevice(h->device);
+  cudaFree(h->d_meta);
+  cudaFree(h->d_blk_off);
+  cudaFree(h->d_row_orig);
+  if (cur != h->device && cur >= 0) cudaSetDevice(cur);
+  delete h;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_spmm(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
+                      void* stream) {
+  if (!h) return fail(SDNN_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (N < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "N < 0");
+  if (act != SDNN_ACT_NONE && act != SDNN_ACT_RELU) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown act");
+  if (N == 0) return SDNN_OK;
+  if (!X || !Y) return fail(SDNN_ERR_INVALID_ARGUMENT, "X or Y is NULL");
+  const size_t ybytes = size_t(h->plan.M) * size_t(N) * 4;
+  if (overlaps(Y, ybytes, X, size_t(h->plan.K) * size_t(N) * 4) || overlaps(Y, ybytes, bias, size_t(h->plan.M) * 4))
+    return fail(SDNN_ERR_INVALID_ARGUMENT, "Y overlaps X or bias");
+  sdnn_status st = check_device(h);
+  if (st != SDNN_OK) return st;
+  return launch(h, X, N, bias, act, Y, static_cast<cudaStream_t>(stream));
+}
+
+sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const float* bias_host, int32_t act,
+                           float* Y_host, int64_t block_cols) {
+  if (!h) return fail(SDNN_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (N < 0 || block_cols < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "N < 0 or block_cols < 0");
+  if (act != SDNN_ACT_NONE && act != SDNN_ACT_RELU) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown act");
+  if (N == 0) return SDNN_OK;
+  if (!X_host || !Y_host) return fail(SDNN_ERR_INVALID_ARGUMENT, "X or Y is NULL");
+  sdnn_status st = check_device(h);
+  if (st != SDNN_OK) return st;
+  const int64_t M = h->plan.M, K = h->plan.K;
+  int64_t nc = block_cols;
+  if (nc == 0) {  // ~128 MiB of X+Y per block, multiple of 256 columns
+    nc = std::max<int64_t>(256, (int64_t(128) << 20) / ((M + K) * 4) / 256 * 256);
+  }
+  nc = std::min(nc, N);
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[3][2] = {};
+  float* xd[2] = {nullptr, nullptr};
+  float* yd[2] = {nullptr, nullptr};
+  float* bd = nullptr;
+  sdnn_status rs = SDNN_OK;
+  std::string msg;
+  auto ck = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rs == SDNN_OK) {
+      rs = e == cudaErrorMemoryAllocation ? SDNN_ERR_OUT_OF_MEMORY : SDNN_ERR_CUDA;
+      msg = std::string(what) + ": " + cudaGetErrorString(e);
+    }
+    return rs == SDNN_OK;
+  };
+  for (int i = 0; i < 3 && rs == SDNN_OK; ++i) {
+    ck(cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int b = 0; b < 2 && rs == SDNN_OK; ++b) ck(cudaEventCreateWithFlags(&ev[i][b], cudaEventDisableTiming), "cudaEventCreate");
+  }
+  for (int b = 0; b < 2 && rs == SDNN_OK; ++b) {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&xd[b]), size_t(K * nc * 4), s[1]), "cudaMallocAsync");
+    if (rs == SDNN_OK) ck(cudaMallocAsync(reinterpret_cast<void**>(&yd[b]), size_t(M * nc * 4), s[1]), "cudaMallocAsync");
+  }
+  if (rs == SDNN_OK && bias_host) {
+    if (ck(cudaMallocAsync(reinterpret_cast<void**>(&bd), size_t(M * 4), s[1]), "cudaMallocAsync"))
+      ck(cudaMemcpyAsync(bd, bias_host, size_t(M * 4), cudaMemcpyHostToDevice, s[1]), "cudaMemcpyAsync(bias)");
+  }
+  if (rs == SDNN_OK) {
+    // s[0]: H2D copies, s[1]: kernels, s[2]: D2H copies.  ev[0][b]: X block in buffer b ready;
+    // ev[1][b]: kernel on buffer b done; ev[2][b]: Y buffer b drained to host.
+    ck(cudaEventRecord(ev[1][0], s[1]), "cudaEventRecord");
+    ck(cudaEventRecord(ev[1][1], s[1]), "cudaEventRecord");
+    ck(cudaEventRecord(ev[2][0], s[1]), "cudaEventRecord");
+    ck(cudaEventRecord(ev[2][1], s[1]), "cudaEventRecord");
+    int i = 0;
+    for (int64_t c0 = 0; c0 < N && rs == SDNN_OK; c0 += nc, ++i) {
+      const int b = i & 1;
+      const int64_t w = std::min(nc, N - c0);
+      ck(cudaStreamWaitEvent(s[0], ev[1][b], 0), "cudaStreamWaitEvent");
+      ck(cudaMemcpy2DAsync(xd[b], size_t(w * 4), X_host + c0, size_t(N * 4), size_t(w * 4), size_t(K),
+                           cudaMemcpyHostToDevice, s[0]), "cudaMemcpy2DAsync(X)");
+      ck(cudaEventRecord(ev[0][b], s[0]), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(s[1], ev[0][b], 0), "cudaStreamWaitEvent");
+      ck(cudaStreamWaitEvent(s[1], ev[2][b], 0), "cudaStreamWaitEvent");
+      if (rs == SDNN_OK) {
+        sdnn_status ls = launch(h, xd[b], w, bd, act, yd[b], s[1]);
+        if (ls != SDNN_OK) { rs = ls; msg = sdnn_last_error_message(); }
+      }
+      ck(cudaEventRecord(ev[1][b], s[1]), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(s[2], ev[1][b], 0), "cudaStreamWaitEvent");
+      ck(cudaMemcpy2DAsync(Y_host + c0, size_t(N * 4), yd[b], size_t(w * 4), size_t(w * 4), size_t(M),
+                           cudaMemcpyDeviceToHost, s[2]), "cudaMemcpy2DAsync(Y)");
+      ck(cudaEventRecord(ev[2][b], s[2]), "cudaEventRecord");
+    }
+  }
+  // drain everything before freeing
+  for (int i = 0; i < 3; ++i)
+    if (s[i]) ck(cudaStreamSynchronize(s[i]), "cudaStreamSynchronize");
+  for (int b = 0; b < 2; ++b) {
+    if (xd[b]) cudaFreeAsync(xd[b], s[1]);
+    if (yd[b]) cudaFreeAsync(yd[b], s[1]);
+  }
+  if (bd) cudaFreeAsync(bd, s[1]);
+  if (s[1]) cudaStreamSynchronize(s[1]);
+  for (int i = 0; i < 3; ++i) {
+    for (int b = 0; b < 2; ++b)
+      if (ev[i][b]) cudaEventDestroy(ev[i][b]);
+    if (s[i]) cudaStreamDestroy(s[i]);
+  }
+  if (rs != SDNN_OK) return fail(rs, msg);
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_get_permutation(sdnn_handle h, int32_t* out_perm) {
+  if (!h || !out_perm) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle or out_perm");
+  std::memcpy(out_perm, h->plan.perm.data(), h->plan.perm.size() * 4);
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info) {
+  if (!h || !info) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle or info");
+  if (info->struct_size != sizeof(sdnn_info)) return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_info.struct_size mismatch");
+  plan_fill_info(h->plan, h->device, info);
+  info->meta_bytes = h->plan.meta_size_uploaded;
+  return SDNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+"""GPU parity: libsdnn (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star; reading C9): |Y_gpu − Y_oracle| ≤ 1e-4 · S per element,
+S = Σ|w||x| + |b| from the oracle; exact equality where S = 0.  Invariants that hold bitwise (fixed
+per-row accumulation order) are checked bitwise."""
+import numpy as np
+import pytest
+
+import sdnn_synth as synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def sdnn():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2101_07948_b200 as m
+    return m
+
+
+def run_gpu(sdnn, p, X, bias=None, act=1, handle=None, **opts):
+    h = handle or sdnn.Handle.from_problem(p, **opts)
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    bd = None if bias is None else torch.from_numpy(bias).cuda()
+    Y = h.spmm(Xd, bd, act=act)
+    torch.cuda.synchronize()
+    return Y.cpu().numpy(), h
+
+
+def assert_parity(Y, Yo, S, what=""):
+    err = np.abs(Y.astype(np.float64) - Yo.astype(np.float64))
+    zero = S == 0
+    assert np.all(Y[zero] == Yo[zero]), f"{what}: nonzero output where S = 0"
+    ratio = np.where(zero, 0.0, err / np.where(zero, 1.0, S))
+    worst = float(ratio.max()) if ratio.size else 0.0
+    assert worst <= TOL, f"{what}: max |err|/S = {worst:.3e} > {TOL}"
+    return worst
+
+
+def check(sdnn, oracle_mod, p, X=None, act=None, bias="p", **opts):
+    X = p.x() if X is None else X
+    b = p.bias if isinstance(bias, str) else bias
+    act = p.act if act is None else act
+    Y, h = run_gpu(sdnn, p, X, b, act, **opts)
+    Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, b, act=act, want_scale=True)[:2]
+    return assert_parity(Y, Yo, S, p.name), Y, h
+
+
+# ------------------------------------------------------------------ worked examples (P1)
+def test_worked_example(sdnn, oracle_mod):
+    W = np.array([[0, 2], [3, 0]], np.float32)
+    rp, ci, v = np.array([0, 1, 2], np.int32), np.array([1, 0], np.int32), np.array([2, 3], np.float32)
+    h = sdnn.Handle(rp, ci, v, 2, 2)
+    Y = h.spmm(torch.ones(2, 2, device="cuda"), None, act=0).cpu().numpy()
+    np.testing.assert_array_equal(Y, [[2, 2], [3, 3]])
+
+
+# ------------------------------------------------------------------ BASELINE configs c1-c4 (full size)
+@pytest.mark.parametrize("key", [k for k in synth.CONFIGS if k != "c5"])
+def test_config_parity(sdnn, oracle_mod, key):
+    p = synth.config_problem(key)
+    worst, _, _ = check(sdnn, oracle_mod, p)
+    print(f"{key}: max err/S = {worst:.2e}")
+
+
+def test_c2_no_act(sdnn, oracle_mod):
+    p = synth.config_problem("c2_3072x768", act=0)
+    check(sdnn, oracle_mod, p)
+
+
+# ------------------------------------------------------------------ desk grid
+@pytest.mark.parametrize("g", list(synth.desk_grid()), ids=lambda g: f"{g['name']}_s{g['seed']}")
+def test_desk_grid(sdnn, oracle_mod, g):
+    p = synth.make_problem(g["name"], g["M"], g["K"], g["N"], g["sparsity"], seed=g["seed"])
+    check(sdnn, oracle_mod, p)
+
+
+# ------------------------------------------------------------------ c5 at full size, launch config of bench.py
+def test_c5_full_size_sampled_columns(sdnn, oracle_mod):
+    p = synth.config_problem("c5")
+    h = sdnn.Handle.from_problem(p)
+    X = torch.empty((p.K, p.N), dtype=torch.float32, device="cuda")
+    for b in range((p.N + synth.X_BLOCK - 1) // synth.X_BLOCK):
+        blk = torch.from_numpy(p.x_block(b))
+        X[:, b * synth.X_BLOCK:b * synth.X_BLOCK + blk.shape[1]].copy_(blk)
+    bias = torch.from_numpy(p.bias).cuda()
+    Y = h.spmm(X, bias, act=1)
+    cols = np.concatenate([np.arange(0, 64), np.arange(131072 - 32, 131072 + 32), np.arange(p.N - 64, p.N),
+                           np.random.default_rng(0).choice(p.N, 64, replace=False)])
+    cols_t = torch.from_numpy(cols).cuda()
+    Ys = Y[:, cols_t].cpu().numpy()
+    Xs = X[:, cols_t].cpu().numpy()
+    Yo, S, _ = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, Xs, p.bias, act=1, want_scale=True)
+    assert_parity(Ys, Yo, S, "c5 sampled")
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 127, 129, 300, 1000])
+def test_ragged_n(sdnn, oracle_mod, N):
+    p = synth.make_problem("ragged", 200, 150, N, 0.9, mask="lognormal", seed=N)
+    check(sdnn, oracle_mod, p)
+
+
+def test_unaligned_pointers(sdnn, oracle_mod):
+    p = synth.make_problem("unal", 100, 90, 64, 0.8, seed=1)
+    X = p.x()
+    h = sdnn.Handle.from_problem(p)
+    Xbuf = torch.zeros(p.K * p.N + 1, device="cuda")
+    Xbuf[1:].copy_(torch.from_numpy(X).reshape(-1))
+    Ybuf = torch.zeros(p.M * p.N + 1, device="cuda")
+    Xv = Xbuf[1:].view(p.K, p.N)
+    Yv = Ybuf[1:].view(p.M, p.N)
+    h.spmm(Xv, torch.from_numpy(p.bias).cuda(), act=1, out=Yv)
+    Yo, S = oracle_mod.spmm(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1)
+    assert_parity(Yv.cpu().numpy(), Yo, S, "unaligned")
+
+
+@pytest.mark.parametrize("M,K,N,dens", [(1, 1, 4, 1.0), (1, 500, 8, 0.3), (500, 1, 8, 0.5), (37, 65, 12, 1.0),
+                                        (129, 257, 20, 0.0), (64, 64, 64, 1.0), (2100, 70, 40, 0.05)])
+def test_degenerate_shapes(sdnn, oracle_mod, M, K, N, dens):
+    rng = np.random.default_rng(M + K + N)
+    mask = rng.random((M, K)) < dens
+    rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum(mask.sum(1))
+    ci = np.nonzero(mask)[1].astype(np.int32)
+    v = (0.05 * rng.standard_normal(ci.size)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(M)).astype(np.float32)
+    p = synth.Problem("deg", M, K, N, 0, "x", rp, ci, v, b, 1, 0)
+    X = rng.standard_normal((K, N)).astype(np.float32)
+    for act in (0, 1):
+        check(sdnn, oracle_mod, p, X=X, act=act)
+    check(sdnn, oracle_mod, p, X=X, act=1, bias=None)
+
+
+def test_empty_weight(sdnn, oracle_mod):
+    M, K, N = 70, 40, 24
+    p = synth.Problem("empty", M, K, N, 1.0, "x", np.zeros(M + 1, np.int32), np.zeros(0, np.int32),
+                      np.zeros(0, np.float32), np.linspace(-1, 1, M).astype(np.float32), 1, 0)
+    X = np.random.default_rng(0).standard_normal((K, N)).astype(np.float32)
+    _, Y, _ = check(sdnn, oracle_mod, p, X=X)
+    np.testing.assert_array_equal(Y, np.repeat(np.maximum(p.bias, 0)[:, None], N, 1))
+
+
+def test_n_zero_is_noop(sdnn):
+    p = synth.config_problem("c1")
+    h = sdnn.Handle.from_problem(p)
+    out = torch.full((p.M, 0), 1.0, device="cuda")
+    h.spmm(torch.empty((p.K, 0), device="cuda"), None, out=out)
+
+
+# ------------------------------------------------------------------ invariants (bitwise)
+def test_permute_on_off_and_tilings_bitwise(sdnn):
+    p = synth.config_problem("c2_768x3072")
+    X = p.x()
+    ref, _ = run_gpu(sdnn, p, X, p.bias, 1)
+    for opts in [dict(permute=False), dict(panel_rows=8), dict(cta_panels=1), dict(k_chunk=8),
+                 dict(k_chunk=128, panel_rows=4, cta_panels=2)]:
+        Y, _ = run_gpu(sdnn, p, X, p.bias, 1, **opts)
+        np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
+
+
+def test_column_shards_bitwise(sdnn):
+    p = synth.config_problem("c3_512x512")
+    X = p.x()
+    h = sdnn.Handle.from_problem(p)
+    ref, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    for a, b in [(0, 4), (4, 1000), (1000, 1001), (1001, p.N)]:
+        Y, _ = run_gpu(sdnn, p, np.ascontiguousarray(X[:, a:b]), p.bias, 1, handle=h)
+        np.testing.assert_array_equal(Y, ref[:, a:b])
+
+
+def test_repeat_bitwise_and_linearity(sdnn):
+    p = synth.config_problem("c3_1024x512", act=0)
+    X = p.x()
+    h = sdnn.Handle.from_problem(p)
+    Y1, _ = run_gpu(sdnn, p, X, None, 0, handle=h)
+    Y2, _ = run_gpu(sdnn, p, X, None, 0, handle=h)
+    np.testing.assert_array_equal(Y1, Y2)
+    Y3, _ = run_gpu(sdnn, p, 2 * X, None, 0, handle=h)
+    np.testing.assert_array_equal(Y3, 2 * Y1)
+
+
+def test_host_entry_point_matches_device(sdnn):
+    p = synth.config_problem("c3_256x128")
+    X = p.x()
+    h = sdnn.Handle.from_problem(p)
+    ref, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    for bc in (0, 512, 1000, 4):
+        Y = h.spmm_host(X, p.bias, act=1, block_cols=bc)
+        np.testing.assert_array_equal(Y, ref)
+
+
+def test_cuda_graph_capture(sdnn):
+    p = synth.config_problem("c3_512x512")
+    h = sdnn.Handle.from_problem(p)
+    X = torch.from_numpy(p.x()).cuda()
+    b = torch.from_numpy(p.bias).cuda()
+    Y = torch.empty((p.M, p.N), device="cuda")
+    ref = h.spmm(X, b, act=1).clone()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        h.spmm(X, b, act=1, out=Y)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(Y, ref)
+
+
+def test_get_permutation_and_info(sdnn, oracle_mod):
+    p = synth.config_problem("c2_768x768")
+    h = sdnn.Handle.from_problem(p)
+    np.testing.assert_array_equal(h.permutation(), oracle_mod.alg1(p.row_ptr, p.col_idx, p.M, p.K))
+    info = h.info()
+    assert info["device"] == torch.cuda.current_device() and info["nnz"] == p.nnz and info["meta_bytes"] > 0
+
+
+def test_errors(sdnn):
+    p = synth.config_problem("c1")
+    h = sdnn.Handle.from_problem(p)
+    X = torch.zeros((p.K, 8), device="cuda")
+    with pytest.raises(sdnn.SdnnError):
+        h.spmm(X, None, act=5)
+    st = sdnn._lib.sdnn_spmm(h._h, X.data_ptr(), -1, None, 1, X.data_ptr(), None)
+    assert st == 1
+    st = sdnn._lib.sdnn_spmm(h._h, X.data_ptr(), 8, None, 1, X.data_ptr(), None)  # Y aliases X
+    assert st == 1

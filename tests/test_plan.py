@@ -1,0 +1,108 @@
+"""Host-side preparation checks (no GPU): the C++ inverted-index Algorithm 1 against the oracle
+ and the packing invariants of the execution-ordered format."""
+import numpy as np
+import pytest
+
+import paper_2101_07948_b200 as sdnn
+import sdnn_synth as synth
+
+
+def decode(p, plan):
+    """Decode the exported plan back into (orig_row, col, val) triples, checking the layout."""
+    info = plan.info()
+    row_orig, blk_off, meta = plan.export()
+    rw, wc, kc, nch, nrb = (info[k] for k in ("panel_rows", "cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
+    rcta = rw * wc
+    hdr_bytes = (rcta * 4 + 15) // 16 * 16
+    assert blk_off[0] == 0 and blk_off[-1] == meta.size and np.all(np.diff(blk_off) > 0)
+    assert np.all(blk_off % 16 == 0)
+    assert np.diff(blk_off).max() <= info["max_block_bytes"]
+    triples = []
+    last_col = {}
+    for b in range(nrb):
+        for j in range(nch):
+            blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]]
+            hdr = blk[:rcta * 4].view(np.uint32)
+            ent = blk[hdr_bytes:]
+            for s in range(rcta):
+                start, cnt = int(hdr[s] >> 16), int(hdr[s] & 0xFFFF)
+                assert start % 2 == 0
+                orow = int(row_orig[b * rcta + s])
+                if orow < 0:
+                    assert cnt == 0
+                    continue
+                for i in range(cnt):
+                    e = ent[(start + i) * 8:(start + i) * 8 + 8]
+                    cl = int(e[:4].view(np.uint32)[0])
+                    w = e[4:].view(np.float32)[0]
+                    assert 0 <= cl < kc
+                    col = j * kc + cl
+                    assert col > last_col.get(orow, -1)  # ascending column order per row
+                    last_col[orow] = col
+                    triples.append((orow, col, w))
+    return info, row_orig, triples
+
+
+def csr_triples(p):
+    r = np.repeat(np.arange(p.M), np.diff(p.row_ptr))
+    return sorted(zip(r.tolist(), p.col_idx.tolist(), p.vals.tolist()))
+
+
+@pytest.mark.parametrize("key", ["c1", "c2_768x768", "c3_128x64", "c4_512x2048_s95"])
+def test_c_alg1_equals_oracle_on_configs(oracle_mod, key):
+    p = synth.config_problem(key, N=4)
+    np.testing.assert_array_equal(sdnn.permutation(p.row_ptr, p.col_idx, p.M, p.K),
+                                  oracle_mod.alg1(p.row_ptr, p.col_idx, p.M, p.K))
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_c_alg1_equals_bruteforce_random(oracle_mod, seed):
+    rng = np.random.default_rng(seed)
+    M, K = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+    mask = rng.random((M, K)) < rng.uniform(0, 0.7)
+    if seed % 5 == 0:
+        mask[M // 2:] = mask[:M - M // 2]
+    rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum(mask.sum(1))
+    ci = np.nonzero(mask)[1].astype(np.int32)
+    order = sdnn.permutation(rp, ci, M, K).tolist()
+    assert order == oracle_mod.alg1_bruteforce([set(np.flatnonzero(mask[i]).tolist()) for i in range(M)])
+
+
+@pytest.mark.parametrize("key,opts", [
+    ("c1", {}), ("c1", dict(permute=False)), ("c2_768x3072", {}), ("c3_128x64", dict(panel_rows=8, cta_panels=3)),
+    ("c4_512x2048_s80", dict(k_chunk=8)), ("c3_256x128", dict(k_chunk=96, cta_panels=1)),
+])
+def test_packing_invariants(oracle_mod, key, opts):
+    p = synth.config_problem(key, N=4)
+    plan = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, **opts)
+    info, row_orig, triples = decode(p, plan)
+    # every nonzero appears exactly once with its original row, column and value
+    assert sorted(triples) == csr_triples(p)
+    # panels tile the permuted rows: row_orig = perm followed by empty slots
+    perm = sdnn.permutation(p.row_ptr, p.col_idx, p.M, p.K) if opts.get("permute", True) else np.arange(p.M)
+    np.testing.assert_array_equal(row_orig[:p.M], perm)
+    assert np.all(row_orig[p.M:] == -1)
+    assert info["num_row_blocks"] * info["panel_rows"] * info["cta_panels"] >= p.M
+    cnt = np.diff(p.row_ptr)
+    assert info["max_panel_nnz"] >= cnt.max()
+
+
+def test_degenerate_shapes():
+    for M, K, dens in [(1, 1, 1.0), (1, 300, 0.5), (300, 1, 0.5), (5, 7, 0.0), (33, 65, 1.0)]:
+        rng = np.random.default_rng(M * K)
+        mask = rng.random((M, K)) < dens
+        rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum(mask.sum(1))
+        ci = np.nonzero(mask)[1].astype(np.int32)
+        v = rng.standard_normal(ci.size).astype(np.float32)
+        p = synth.Problem("d", M, K, 1, 0, "x", rp, ci, v, None, 0, 0)
+        plan = sdnn.Plan(rp, ci, v, M, K)
+        _, _, triples = decode(p, plan)
+        assert sorted(triples) == csr_triples(p)
+
+
+def test_plan_deterministic():
+    p = synth.config_problem("c2_768x768", N=4)
+    a = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).export()
+    b = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).export()
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
