@@ -157,7 +157,7 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
     X = p.x()
     ref, _ = run_gpu(sdnn, p, X, p.bias, 1)
     for opts in [dict(permute=False), dict(panel_rows=8), dict(cta_panels=1), dict(k_chunk=8),
-                 dict(k_chunk=128, panel_rows=4, cta_panels=2)]:
+                 dict(k_chunk=96, panel_rows=4, cta_panels=2)]:
         Y, _ = run_gpu(sdnn, p, X, p.bias, 1, **opts)
         np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
 
