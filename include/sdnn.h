@@ -56,7 +56,10 @@ typedef enum { SDNN_ACT_NONE = 0, SDNN_ACT_RELU = 1 } sdnn_act;
 typedef struct {
   uint32_t struct_size;
   int32_t permute;          /* 1 (default): Algorithm 1 greedy row reorder; 0: identity   */
-  int32_t panel_rows_max;   /* rows per warp panel: 0 = auto, else 4 or 8                            */
+  int32_t kernel;           /* 0 = auto (cost model), 1 = row kernel (each nonzero reads its X row
+                               slice from shared memory), 2 = group kernel (16-row groups: one X
+                               load feeds every nonzero of the group in that column)               */
+  int32_t panel_rows_max;   /* row kernel: rows per warp panel, 0 = auto, else 4 or 8 (group: 16)   */
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
                                multiple of 8                                                        */
@@ -70,6 +73,8 @@ typedef struct {
   int64_t nnz;
   int32_t device;           /* CUDA ordinal, −1 for a host-only plan                                  */
   int32_t permuted;         /* 1 if Algorithm 1 was applied                                           */
+  int32_t kernel;           /* 1 = row kernel, 2 = group kernel                                       */
+  int32_t group_entries_per_nnz_x1000; /* group format: union entries per nonzero · 1000            */
   int32_t panel_rows;       /* R_w: rows per warp panel                                               */
   int32_t cta_panels;       /* W_c: panels per CTA                                                    */
   int32_t num_panels;       /* P = num_row_blocks · W_c (trailing panels may be empty)               */

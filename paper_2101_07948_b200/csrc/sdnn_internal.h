@@ -22,6 +22,8 @@ struct Plan {
   int32_t M = 0, K = 0;
   int64_t nnz = 0;
   int32_t permuted = 0;
+  int32_t kernel = 1;          // 1 = row kernel, 2 = group kernel
+  int64_t group_entries = 0;   // union entries of the group format
   int32_t panel_rows = 0, cta_panels = 0, num_panels = 0, num_row_blocks = 0;
   int32_t k_chunk = 0, num_chunks = 0;
   int32_t max_block_bytes = 0;
@@ -42,6 +44,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
 // Shared-memory budget used for the X/metadata stage ring (bytes) and the fixed CTA layout.
 constexpr int kSmemBudget = 220 * 1024;
 constexpr int kMaxTN = 256;  // widest N tile (V = 8 floats per lane)
+constexpr int kMaxGroupWarps = 11;  // group kernel: consumer warps per CTA (register budget)
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 

@@ -82,32 +82,124 @@ void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32
   }
 }
 
-// Bytes of the (row block, chunk) metadata block for a given KC, over all blocks; returns max.
-static int64_t max_block_bytes_for(const int32_t* csr_ptr, const int32_t* col_idx, const std::vector<int32_t>& perm,
-                                   int32_t M, int32_t K, int32_t rcta, int32_t kc) {
-  const int32_t nch = (K + kc - 1) / kc;
-  const int64_t hdr = align_up(int64_t(rcta) * 4, 16);
-  std::vector<int64_t> ent(nch);
-  int64_t mx = hdr;
-  for (int32_t b0 = 0; b0 < M; b0 += rcta) {
-    std::fill(ent.begin(), ent.end(), 0);
-    for (int32_t s = 0; s < rcta && b0 + s < M; ++s) {
-      const int32_t r = perm[b0 + s];
-      int32_t cur = -1, c_in = 0;
-      for (int32_t p = csr_ptr[r]; p < csr_ptr[r + 1]; ++p) {
-        const int32_t j = col_idx[p] / kc;
-        if (j != cur) {
-          if (cur >= 0) ent[cur] += align_up(c_in, 2);
-          cur = j;
-          c_in = 0;
-        }
-        ++c_in;
-      }
-      if (cur >= 0) ent[cur] += align_up(c_in, 2);
+// ------------------------------------------------------------------------------------------------
+// Execution-ordered format: one metadata block per (row block, K chunk), in the order the
+// kernel consumes them.  Two layouts:
+//  row kernel   header: R_cta uint32 words (start_entry << 16 | count), padded to 16 B; then 8-byte
+//               entries {uint32 col_local, float w}, each row segment starting at an even entry.
+//  group kernel header: W_c × 16 B {head_off_words, n_entries, w_off_words, 0}; per warp the
+//               entry heads (uint32: col_local | mask_bank0 << 16 | mask_bank1 << 24) padded to
+//               16 B; then per warp the weights, in entry order, bank-0 rows then bank-1 rows.
+// Emitter: walks blocks in order; with `out` == nullptr it only computes the block sizes.
+// ------------------------------------------------------------------------------------------------
+struct Geometry {
+  int32_t kernel, rw, wc, kc, nch, nrb;
+};
+
+static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals,
+                        const std::vector<int32_t>& row_orig, const Geometry& g, std::vector<int64_t>& sizes,
+                        uint8_t* out, const std::vector<int64_t>* offs, int64_t* entries_total) {
+  const int32_t rcta = g.rw * g.wc;
+  sizes.assign(size_t(g.nrb) * g.nch, 0);
+  std::vector<int32_t> cur(rcta);
+  int64_t ent_total = 0;
+  // group scratch
+  std::vector<uint16_t> mask(g.kc);
+  std::vector<float> wv(size_t(g.kc) * 16);
+  for (int32_t b = 0; b < g.nrb; ++b) {
+    for (int32_t s = 0; s < rcta; ++s) {
+      const int32_t orow = row_orig[size_t(b) * rcta + s];
+      cur[s] = orow >= 0 ? csr_ptr[orow] : 0;
     }
-    for (int32_t j = 0; j < nch; ++j) mx = std::max(mx, hdr + ent[j] * 8);
+    for (int32_t j = 0; j < g.nch; ++j) {
+      const int32_t lo = j * g.kc, hi = lo + g.kc;
+      uint8_t* blk = out ? out + (*offs)[size_t(b) * g.nch + j] : nullptr;
+      int64_t bytes = 0;
+      if (g.kernel == 1) {
+        const int64_t hdr = align_up(int64_t(rcta) * 4, 16);
+        int32_t e = 0;
+        for (int32_t s = 0; s < rcta; ++s) {
+          const int32_t orow = row_orig[size_t(b) * rcta + s];
+          int32_t c = 0;
+          if (orow >= 0) {
+            int32_t& p = cur[s];
+            while (p < csr_ptr[orow + 1] && col_idx[p] < hi) {
+              if (blk) {
+                const uint32_t cl = uint32_t(col_idx[p] - lo);
+                std::memcpy(blk + hdr + size_t(e + c) * 8, &cl, 4);
+                std::memcpy(blk + hdr + size_t(e + c) * 8 + 4, &vals[p], 4);
+              }
+              ++c;
+              ++p;
+            }
+          }
+          if (blk) reinterpret_cast<uint32_t*>(blk)[s] = (uint32_t(e) << 16) | uint32_t(c);
+          e += int32_t(align_up(c, 2));
+        }
+        ent_total += e;
+        bytes = align_up(hdr + int64_t(e) * 8, 16);
+      } else {
+        // group kernel: per warp (16-row group) the union of its rows' columns in this chunk
+        const int64_t hdr = int64_t(g.wc) * 16;
+        int64_t head_words = 0, w_words = 0;
+        std::vector<std::vector<uint32_t>> wh(g.wc);
+        std::vector<std::vector<float>> ww(g.wc);
+        for (int32_t w = 0; w < g.wc; ++w) {
+          std::fill(mask.begin(), mask.end(), 0);
+          for (int32_t r = 0; r < 16; ++r) {
+            const int32_t s = w * 16 + r;
+            const int32_t orow = row_orig[size_t(b) * rcta + s];
+            if (orow < 0) continue;
+            int32_t& p = cur[s];
+            while (p < csr_ptr[orow + 1] && col_idx[p] < hi) {
+              const int32_t cl = col_idx[p] - lo;
+              mask[cl] |= uint16_t(1u << r);
+              wv[size_t(cl) * 16 + r] = vals ? vals[p] : 0.f;
+              ++p;
+            }
+          }
+          for (int32_t cl = 0; cl < g.kc; ++cl) {
+            if (!mask[cl]) continue;
+            const uint32_t m = mask[cl];
+            wh[w].push_back(uint32_t(cl) | ((m & 0xffu) << 16) | ((m >> 8) << 24));
+            for (int32_t r = 0; r < 16; ++r)
+              if (m >> r & 1u) ww[w].push_back(wv[size_t(cl) * 16 + r]);
+          }
+          head_words += align_up(int64_t(wh[w].size()), 4);
+          w_words += int64_t(ww[w].size());
+          ent_total += int64_t(wh[w].size());
+        }
+        bytes = align_up(hdr + head_words * 4 + w_words * 4, 16);
+        if (blk) {
+          uint32_t* h32 = reinterpret_cast<uint32_t*>(blk);
+          int64_t hpos = hdr / 4, wpos = hdr / 4 + head_words;
+          for (int32_t w = 0; w < g.wc; ++w) {
+            h32[w * 4 + 0] = uint32_t(hpos);
+            h32[w * 4 + 1] = uint32_t(wh[w].size());
+            h32[w * 4 + 2] = uint32_t(wpos);
+            h32[w * 4 + 3] = 0;
+            std::memcpy(h32 + hpos, wh[w].data(), wh[w].size() * 4);
+            hpos += align_up(int64_t(wh[w].size()), 4);
+            std::memcpy(h32 + wpos, ww[w].data(), ww[w].size() * 4);
+            wpos += int64_t(ww[w].size());
+          }
+        }
+      }
+      sizes[size_t(b) * g.nch + j] = bytes;
+    }
   }
-  return align_up(mx, 16);
+  if (entries_total) *entries_total = ent_total;
+}
+
+static int64_t max_of(const std::vector<int64_t>& v) {
+  int64_t m = 0;
+  for (int64_t x : v) m = std::max(m, x);
+  return m;
+}
+
+// X stage bytes at the widest N tile + metadata stage; S stages must fit the smem budget.
+static int32_t stages_for(int32_t kc, int64_t max_block) {
+  return int32_t(kSmemBudget / (int64_t(kc) * kMaxTN * 4 + align_up(max_block, 128)));
 }
 
 sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
@@ -121,9 +213,13 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     o = *opts;
     if (o.flags != 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.flags must be 0");
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
-    if (o.panel_rows_max != 0 && o.panel_rows_max != 4 && o.panel_rows_max != 8)
-      return fail(SDNN_ERR_INVALID_ARGUMENT, "panel_rows_max must be 0, 4 or 8");
+    if (o.kernel < 0 || o.kernel > 2) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0, 1 or 2");
+    if (o.panel_rows_max != 0 && o.panel_rows_max != 4 && o.panel_rows_max != 8 &&
+        !(o.panel_rows_max == 16 && o.kernel == 2))
+      return fail(SDNN_ERR_INVALID_ARGUMENT, "panel_rows_max must be 0, 4 or 8 (16 with the group kernel)");
     if (o.cta_panels < 0 || o.cta_panels > 16) return fail(SDNN_ERR_INVALID_ARGUMENT, "cta_panels must be 0..16");
+    if (o.kernel == 2 && o.cta_panels > kMaxGroupWarps)
+      return fail(SDNN_ERR_INVALID_ARGUMENT, "cta_panels must be <= 11 with the group kernel");
     if (o.k_chunk != 0 && (o.k_chunk < 8 || o.k_chunk > 128 || o.k_chunk % 8))
       return fail(SDNN_ERR_INVALID_ARGUMENT, "k_chunk must be 0 or a multiple of 8 in [8, 128]");
   }
@@ -144,109 +240,99 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     else
       for (int32_t i = 0; i < M; ++i) plan.perm[i] = i;
 
-    // Launch geometry: R_w rows per warp panel, W_c panels per CTA.
-    const int32_t rw = o.panel_rows_max ? o.panel_rows_max : (M >= 2048 ? 8 : 4);
-    int32_t wc = o.cta_panels;
-    if (!wc) {
-      wc = 16;
-      while (wc > 4 && (M + rw * wc - 1) / (rw * wc) < 32) wc /= 2;
-    }
-    const int32_t rcta = rw * wc;
-    plan.panel_rows = rw;
-    plan.cta_panels = wc;
-    plan.num_row_blocks = (M + rcta - 1) / rcta;
-    plan.num_panels = plan.num_row_blocks * wc;
-
+    // Candidate geometries: the row kernel (R_w rows per warp) and the group kernel (16 rows per
+    // warp).  Launch geometry: W_c warps per CTA, enough row blocks to fill
+    // the machine for the typical N.
+    auto make_geo = [&](int32_t kernel) {
+      Geometry g{};
+      g.kernel = kernel;
+      g.rw = kernel == 2 ? 16 : (o.panel_rows_max ? o.panel_rows_max : (M >= 2048 ? 8 : 4));
+      int32_t wc = o.cta_panels;
+      if (!wc) {
+        wc = kernel == 2 ? kMaxGroupWarps : 16;
+        while (wc > 4 && (M + g.rw * wc - 1) / (g.rw * wc) < (kernel == 2 ? 16 : 32)) wc = kernel == 2 ? wc - 1 : wc / 2;
+      }
+      g.wc = wc;
+      g.nrb = (M + g.rw * wc - 1) / (g.rw * wc);
+      return g;
+    };
+    auto row_orig_for = [&](const Geometry& g) {
+      std::vector<int32_t> ro(size_t(g.nrb) * g.wc * g.rw, -1);
+      for (int32_t p = 0; p < M; ++p) ro[p] = plan.perm[p];
+      return ro;
+    };
     // K chunk (split-K tiling along the reduction dimension): the largest KC whose stage
     // (X tile at the widest N tile + metadata block) fits three times in the shared-memory budget.
-    int32_t kc = o.k_chunk, stages = 0;
-    int64_t mb = 0;
-    const int32_t cands[] = {64, 32, 16, 8};
-    if (kc) {
-      mb = max_block_bytes_for(csr_ptr, col_idx, plan.perm, M, K, rcta, kc);
-      stages = int32_t(kSmemBudget / (int64_t(kc) * kMaxTN * 4 + align_up(mb, 128)));
-      if (stages < 2) return fail(SDNN_ERR_UNSUPPORTED, "k_chunk too large for the shared-memory budget");
-    } else {
+    auto choose_kc = [&](Geometry& g, const std::vector<int32_t>& ro, int64_t* entries) -> bool {
+      std::vector<int64_t> sizes;
+      const int32_t cands[] = {64, 32, 16, 8};
       for (int32_t c : cands) {
-        const int64_t m = max_block_bytes_for(csr_ptr, col_idx, plan.perm, M, K, rcta, c);
-        const int32_t s = int32_t(kSmemBudget / (int64_t(c) * kMaxTN * 4 + align_up(m, 128)));
-        if (s >= 3 || (c == 8 && s >= 2)) { kc = c; mb = m; stages = s; break; }
+        if (o.k_chunk && c != o.k_chunk) continue;
+        g.kc = c;
+        g.nch = (K + c - 1) / c;
+        emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries);
+        const int32_t s = stages_for(c, max_of(sizes));
+        if (s >= 3 || (s >= 2 && (o.k_chunk || c == 8))) return true;
       }
-      if (!kc) return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
-    }
-    (void)stages;
-    plan.k_chunk = kc;
-    plan.num_chunks = (K + kc - 1) / kc;
-    plan.max_block_bytes = int32_t(mb);
+      if (o.k_chunk) {  // explicit KC not in the candidate list
+        g.kc = o.k_chunk;
+        g.nch = (K + g.kc - 1) / g.kc;
+        emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries);
+        return stages_for(g.kc, max_of(sizes)) >= 2;
+      }
+      return false;
+    };
 
-    // row_orig
-    plan.row_orig.assign(size_t(plan.num_panels) * rw, -1);
-    for (int32_t p = 0; p < M; ++p) plan.row_orig[p] = plan.perm[p];
+    Geometry g{};
+    std::vector<int32_t> ro;
+    int64_t entries = 0;
+    if (o.kernel == 1 || o.kernel == 2) {
+      g = make_geo(o.kernel);
+      ro = row_orig_for(g);
+      if (!choose_kc(g, ro, &entries))
+        return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
+    } else {
+      // Cost model (shared-memory wavefronts per warp, V = 8 floats per lane): row kernel
+      // 8 per nonzero + 0.5 (entry pairs); group kernel 8 per union entry + 0.25 (heads) + 1 per
+      // nonzero (weights).  Pick the group kernel when it saves >= 10 %.
+      Geometry gr = make_geo(1), gg = make_geo(2);
+      std::vector<int32_t> ror = row_orig_for(gr), rog = row_orig_for(gg);
+      int64_t er = 0, eg = 0;
+      const bool okr = choose_kc(gr, ror, &er);
+      const bool okg = choose_kc(gg, rog, &eg);
+      const double cost_r = 8.5 * double(nnz), cost_g = 8.25 * double(eg) + double(nnz);
+      if (okg && (!okr || cost_g < 0.9 * cost_r)) {
+        g = gg; ro.swap(rog); entries = eg;
+      } else if (okr) {
+        g = gr; ro.swap(ror); entries = er;
+      } else {
+        return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
+      }
+    }
+    plan.kernel = g.kernel;
+    plan.panel_rows = g.rw;
+    plan.cta_panels = g.wc;
+    plan.num_row_blocks = g.nrb;
+    plan.num_panels = g.nrb * g.wc;
+    plan.k_chunk = g.kc;
+    plan.num_chunks = g.nch;
+    plan.row_orig.swap(ro);
     for (int32_t pn = 0; pn < plan.num_panels; ++pn) {
       int64_t s = 0;
-      for (int32_t r = 0; r < rw; ++r) {
-        const int32_t orow = plan.row_orig[size_t(pn) * rw + r];
+      for (int32_t r = 0; r < g.rw; ++r) {
+        const int32_t orow = plan.row_orig[size_t(pn) * g.rw + r];
         if (orow >= 0) s += csr_ptr[orow + 1] - csr_ptr[orow];
       }
       plan.max_panel_nnz = std::max(plan.max_panel_nnz, s);
     }
-
-    // Execution-ordered metadata: blocks ordered [row block][chunk], rows in slot order,
-    // each row's entries in ascending column order (the order the kernel accumulates them).
-    const int32_t nch = plan.num_chunks;
-    const int64_t hdr = align_up(int64_t(rcta) * 4, 16);
-    plan.blk_off.assign(size_t(plan.num_row_blocks) * nch + 1, 0);
-    // first pass: sizes
-    std::vector<int32_t> rowpos(rcta);
-    std::vector<std::vector<int32_t>> seg_cnt(rcta, std::vector<int32_t>(nch));
-    int64_t total = 0;
-    std::vector<int64_t> sizes(size_t(plan.num_row_blocks) * nch);
-    for (int32_t b = 0; b < plan.num_row_blocks; ++b) {
-      std::vector<int64_t> ent(nch, 0);
-      for (int32_t s = 0; s < rcta; ++s) {
-        const int32_t orow = plan.row_orig[size_t(b) * rcta + s];
-        if (orow < 0) continue;
-        std::vector<int32_t> c_in(nch, 0);
-        for (int32_t p = csr_ptr[orow]; p < csr_ptr[orow + 1]; ++p) c_in[col_idx[p] / kc]++;
-        for (int32_t j = 0; j < nch; ++j) ent[j] += align_up(c_in[j], 2);
-      }
-      for (int32_t j = 0; j < nch; ++j) {
-        sizes[size_t(b) * nch + j] = align_up(hdr + ent[j] * 8, 16);
-        total += sizes[size_t(b) * nch + j];
-      }
-    }
+    std::vector<int64_t> sizes;
+    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, nullptr, nullptr, &entries);
+    plan.group_entries = g.kernel == 2 ? entries : 0;
+    plan.max_block_bytes = int32_t(max_of(sizes));
+    plan.blk_off.assign(sizes.size() + 1, 0);
     for (size_t i = 0; i < sizes.size(); ++i) plan.blk_off[i + 1] = plan.blk_off[i] + sizes[i];
-    plan.meta.assign(size_t(total), 0);
-    // second pass: fill
-    for (int32_t b = 0; b < plan.num_row_blocks; ++b) {
-      for (int32_t s = 0; s < rcta; ++s) {
-        const int32_t orow = plan.row_orig[size_t(b) * rcta + s];
-        rowpos[s] = orow >= 0 ? csr_ptr[orow] : 0;
-      }
-      for (int32_t j = 0; j < nch; ++j) {
-        uint8_t* blk = plan.meta.data() + plan.blk_off[size_t(b) * nch + j];
-        uint32_t* h = reinterpret_cast<uint32_t*>(blk);
-        uint8_t* ent = blk + hdr;
-        int32_t e = 0;
-        const int32_t lim = (j + 1) * kc;
-        for (int32_t s = 0; s < rcta; ++s) {
-          const int32_t orow = plan.row_orig[size_t(b) * rcta + s];
-          int32_t c = 0;
-          if (orow >= 0) {
-            int32_t& p = rowpos[s];
-            while (p < csr_ptr[orow + 1] && col_idx[p] < lim) {
-              const uint32_t cl = uint32_t(col_idx[p] - j * kc);
-              std::memcpy(ent + size_t(e + c) * 8, &cl, 4);
-              std::memcpy(ent + size_t(e + c) * 8 + 4, &vals[p], 4);
-              ++c;
-              ++p;
-            }
-          }
-          h[s] = (uint32_t(e) << 16) | uint32_t(c);
-          e += int32_t(align_up(c, 2));
-        }
-      }
-    }
+    plan.meta.assign(size_t(plan.blk_off.back()), 0);
+    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, plan.meta.data(), &plan.blk_off, nullptr);
   } catch (const std::bad_alloc&) {
     return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed during planning");
   }
@@ -267,6 +353,8 @@ static void fill_info(const Plan& p, int32_t device, sdnn_info* info) {
   info->nnz = p.nnz;
   info->device = device;
   info->permuted = p.permuted;
+  info->kernel = p.kernel;
+  info->group_entries_per_nnz_x1000 = p.nnz ? int32_t(1000 * p.group_entries / p.nnz) : 0;
   info->panel_rows = p.panel_rows;
   info->cta_panels = p.cta_panels;
   info->num_panels = p.num_panels;

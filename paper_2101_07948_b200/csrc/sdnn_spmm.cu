@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "sdnn_internal.h"
+#include "group_dispatch.inc"
 
 namespace sdnn {
 void plan_fill_info(const Plan& p, int32_t device, sdnn_info* info);
@@ -131,6 +132,50 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
   }
 }
 
+// Group kernel, one chunk: the warp owns a 16-row group (two banks of 8 rows).  For every column of
+// the group's union in this chunk: one X row slice load (V floats per lane) feeds the FMAs of every
+// nonzero of the group in that column, dispatched on the bank's 8-bit mask to a specialised case
+// whose accumulator registers are named statically (group_dispatch.inc; "statically encoding
+// the accumulation position in the vector register name").  Columns ascend, so every row still
+// accumulates in ascending column order (bitwise identical to the row kernel).
+template <int V>
+__device__ __forceinline__ void group_entry(float2 (&acc)[16][V / 2], uint32_t h, const float* __restrict__ xl,
+                                         const float*& wp) {
+  constexpr int TN = 32 * V;
+  const float* xp = xl + (h & 0xffffu) * TN;
+  float2 xq[V / 2];
+  {
+    const float4 a = *reinterpret_cast<const float4*>(xp);
+    xq[0] = make_float2(a.x, a.y);
+    xq[1] = make_float2(a.z, a.w);
+    if constexpr (V == 8) {
+      const float4 b = *reinterpret_cast<const float4*>(xp + 128);
+      xq[2] = make_float2(b.x, b.y);
+      xq[3] = make_float2(b.z, b.w);
+    }
+  }
+  const uint32_t m0 = (h >> 16) & 0xffu, m1 = h >> 24;
+  if (m0) { SDNN_DISPATCH_BANK0(m0) }
+  if (m1) { SDNN_DISPATCH_BANK1(m1) }
+}
+
+template <int V>
+__device__ __forceinline__ void consume_group(float2 (&acc)[16][V / 2], const float* __restrict__ xs,
+                                              const uint8_t* __restrict__ ms, int warp, int lane) {
+  const uint4 hd = reinterpret_cast<const uint4*>(ms)[warp];
+  const uint32_t* heads = reinterpret_cast<const uint32_t*>(ms) + hd.x;
+  const int n = int(hd.y);
+  const float* wp = reinterpret_cast<const float*>(ms) + hd.z;
+  const float* xl = xs + lane * 4;
+  uint4 h4 = make_uint4(0, 0, 0, 0);
+  for (int e = 0; e < n; ++e) {
+    const int t = e & 3;
+    if (t == 0) h4 = *reinterpret_cast<const uint4*>(heads + e);
+    const uint32_t h = t == 0 ? h4.x : t == 1 ? h4.y : t == 2 ? h4.z : h4.w;
+    group_entry<V>(acc, h, xl, wp);
+  }
+}
+
 // Fused epilogue: y = acc + b[orig]; ReLU; store to Y[orig][n0 + ...] (inverse permutation).
 template <int RW, int V, bool VEC>
 __device__ __forceinline__ void epilogue(const float2 (&acc)[RW][V / 2], const KParams& p, int panel, int lane,
@@ -161,8 +206,10 @@ __device__ __forceinline__ void epilogue(const float2 (&acc)[RW][V / 2], const K
 }
 
 // Fast path: TMA producer warp + W_c consumer warps, mbarrier stage ring.
-template <int RW, int V>
-__global__ void __launch_bounds__(17 * 32, 1) spmm_tma_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+// KIND 1 = row kernel (RW rows per warp), KIND 2 = group kernel (RW = 16).
+template <int KIND, int RW, int V>
+__global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 32, 1)
+    spmm_tma_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -207,8 +254,11 @@ __global__ void __launch_bounds__(17 * 32, 1) spmm_tma_kernel(const __grid_const
   for (int j = 0; j < p.nch; ++j) {
     const int s = j % S;
     mbar_wait(&full[s], (j / S) & 1);
-    consume_chunk<RW, V>(acc, reinterpret_cast<const float*>(xstage + size_t(s) * p.x_stage_bytes),
-                         mstage + size_t(s) * p.m_stage_bytes, warp, lane, p.hdr_bytes);
+    const float* xs = reinterpret_cast<const float*>(xstage + size_t(s) * p.x_stage_bytes);
+    if constexpr (KIND == 2)
+      consume_group<V>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane);
+    else
+      consume_chunk<RW, V>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane, p.hdr_bytes);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -218,8 +268,8 @@ __global__ void __launch_bounds__(17 * 32, 1) spmm_tma_kernel(const __grid_const
 
 // Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
 // threads using bounds-checked loads (zero fill) and a block barrier instead of TMA/mbarriers.
-template <int RW, int V>
-__global__ void __launch_bounds__(16 * 32, 1) spmm_generic_kernel(const KParams p) {
+template <int KIND, int RW, int V>
+__global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) spmm_generic_kernel(const KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -248,7 +298,10 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_generic_kernel(const KParams 
     const uint4* src = reinterpret_cast<const uint4*>(p.meta + off[j]);
     for (int idx = threadIdx.x; idx < mbytes / 16; idx += nthr) reinterpret_cast<uint4*>(ms)[idx] = src[idx];
     __syncthreads();
-    consume_chunk<RW, V>(acc, xs, ms, warp, lane, p.hdr_bytes);
+    if constexpr (KIND == 2)
+      consume_group<V>(acc, xs, ms, warp, lane);
+    else
+      consume_chunk<RW, V>(acc, xs, ms, warp, lane, p.hdr_bytes);
   }
   epilogue<RW, V, false>(acc, p, rb * p.wc + warp, lane, n0);
 }
@@ -279,12 +332,12 @@ static PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
-template <int RW, int V>
+template <int KIND, int RW, int V>
 static cudaError_t set_smem_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(spmm_tma_kernel<RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(spmm_tma_kernel<KIND, RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBudget + 1024);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(spmm_generic_kernel<RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(spmm_generic_kernel<KIND, RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kSmemBudget + 1024);
 }
 
@@ -338,18 +391,22 @@ static sdnn_status launch(const sdnn_handle_s* h, const float* X, int64_t N, con
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
     const dim3 grid{unsigned(nblocks)}, block{unsigned((wc + 1) * 32)};
-    if (rw == 8 && V == 8) spmm_tma_kernel<8, 8><<<grid, block, smem, stream>>>(tmap, p);
-    else if (rw == 8 && V == 4) spmm_tma_kernel<8, 4><<<grid, block, smem, stream>>>(tmap, p);
-    else if (rw == 4 && V == 8) spmm_tma_kernel<4, 8><<<grid, block, smem, stream>>>(tmap, p);
-    else spmm_tma_kernel<4, 4><<<grid, block, smem, stream>>>(tmap, p);
+    if (pl.kernel == 2 && V == 8) spmm_tma_kernel<2, 16, 8><<<grid, block, smem, stream>>>(tmap, p);
+    else if (pl.kernel == 2) spmm_tma_kernel<2, 16, 4><<<grid, block, smem, stream>>>(tmap, p);
+    else if (rw == 8 && V == 8) spmm_tma_kernel<1, 8, 8><<<grid, block, smem, stream>>>(tmap, p);
+    else if (rw == 8 && V == 4) spmm_tma_kernel<1, 8, 4><<<grid, block, smem, stream>>>(tmap, p);
+    else if (rw == 4 && V == 8) spmm_tma_kernel<1, 4, 8><<<grid, block, smem, stream>>>(tmap, p);
+    else spmm_tma_kernel<1, 4, 4><<<grid, block, smem, stream>>>(tmap, p);
   } else {
     p.stages = 1;
     const size_t smem = size_t(p.x_stage_bytes) + p.m_stage_bytes;
     const dim3 grid{unsigned(nblocks)}, block{unsigned(wc * 32)};
-    if (rw == 8 && V == 8) spmm_generic_kernel<8, 8><<<grid, block, smem, stream>>>(p);
-    else if (rw == 8 && V == 4) spmm_generic_kernel<8, 4><<<grid, block, smem, stream>>>(p);
-    else if (rw == 4 && V == 8) spmm_generic_kernel<4, 8><<<grid, block, smem, stream>>>(p);
-    else spmm_generic_kernel<4, 4><<<grid, block, smem, stream>>>(p);
+    if (pl.kernel == 2 && V == 8) spmm_generic_kernel<2, 16, 8><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 2) spmm_generic_kernel<2, 16, 4><<<grid, block, smem, stream>>>(p);
+    else if (rw == 8 && V == 8) spmm_generic_kernel<1, 8, 8><<<grid, block, smem, stream>>>(p);
+    else if (rw == 8 && V == 4) spmm_generic_kernel<1, 8, 4><<<grid, block, smem, stream>>>(p);
+    else if (rw == 4 && V == 8) spmm_generic_kernel<1, 4, 8><<<grid, block, smem, stream>>>(p);
+    else spmm_generic_kernel<1, 4, 4><<<grid, block, smem, stream>>>(p);
   }
   SDNN_CUDA_TRY(cudaGetLastError());
   return SDNN_OK;
@@ -394,10 +451,12 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
   static std::once_flag attr_once[64];
   cudaError_t ae = cudaSuccess;
   std::call_once(attr_once[dev & 63], [&] {
-    ae = set_smem_attrs<8, 8>();
-    if (ae == cudaSuccess) ae = set_smem_attrs<8, 4>();
-    if (ae == cudaSuccess) ae = set_smem_attrs<4, 8>();
-    if (ae == cudaSuccess) ae = set_smem_attrs<4, 4>();
+    ae = set_smem_attrs<1, 8, 8>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<1, 8, 4>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<1, 4, 8>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<1, 4, 4>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4>();
   });
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     cudaFree(h->d_meta);

@@ -60,11 +60,12 @@ def test_worked_example(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ BASELINE configs c1-c4 (full size)
+@pytest.mark.parametrize("kernel", ["auto", "row", "group"])
 @pytest.mark.parametrize("key", [k for k in synth.CONFIGS if k != "c5"])
-def test_config_parity(sdnn, oracle_mod, key):
+def test_config_parity(sdnn, oracle_mod, key, kernel):
     p = synth.config_problem(key)
-    worst, _, _ = check(sdnn, oracle_mod, p)
-    print(f"{key}: max err/S = {worst:.2e}")
+    worst, _, h = check(sdnn, oracle_mod, p, kernel=kernel)
+    print(f"{key} {kernel}->{h.info()['kernel']}: max err/S = {worst:.2e}")
 
 
 def test_c2_no_act(sdnn, oracle_mod):
@@ -73,16 +74,18 @@ def test_c2_no_act(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ desk grid
+@pytest.mark.parametrize("kernel", ["row", "group"])
 @pytest.mark.parametrize("g", list(synth.desk_grid()), ids=lambda g: f"{g['name']}_s{g['seed']}")
-def test_desk_grid(sdnn, oracle_mod, g):
+def test_desk_grid(sdnn, oracle_mod, g, kernel):
     p = synth.make_problem(g["name"], g["M"], g["K"], g["N"], g["sparsity"], seed=g["seed"])
-    check(sdnn, oracle_mod, p)
+    check(sdnn, oracle_mod, p, kernel=kernel)
 
 
 # ------------------------------------------------------------------ c5 at full size, launch config of bench.py
-def test_c5_full_size_sampled_columns(sdnn, oracle_mod):
+@pytest.mark.parametrize("kernel", ["auto", "row"])
+def test_c5_full_size_sampled_columns(sdnn, oracle_mod, kernel):
     p = synth.config_problem("c5")
-    h = sdnn.Handle.from_problem(p)
+    h = sdnn.Handle.from_problem(p, kernel=kernel)
     X = torch.empty((p.K, p.N), dtype=torch.float32, device="cuda")
     for b in range((p.N + synth.X_BLOCK - 1) // synth.X_BLOCK):
         blk = torch.from_numpy(p.x_block(b))
@@ -99,16 +102,18 @@ def test_c5_full_size_sampled_columns(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("kernel", ["row", "group"])
 @pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 127, 129, 300, 1000])
-def test_ragged_n(sdnn, oracle_mod, N):
+def test_ragged_n(sdnn, oracle_mod, N, kernel):
     p = synth.make_problem("ragged", 200, 150, N, 0.9, mask="lognormal", seed=N)
-    check(sdnn, oracle_mod, p)
+    check(sdnn, oracle_mod, p, kernel=kernel)
 
 
-def test_unaligned_pointers(sdnn, oracle_mod):
+@pytest.mark.parametrize("kernel", ["row", "group"])
+def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     p = synth.make_problem("unal", 100, 90, 64, 0.8, seed=1)
     X = p.x()
-    h = sdnn.Handle.from_problem(p)
+    h = sdnn.Handle.from_problem(p, kernel=kernel)
     Xbuf = torch.zeros(p.K * p.N + 1, device="cuda")
     Xbuf[1:].copy_(torch.from_numpy(X).reshape(-1))
     Ybuf = torch.zeros(p.M * p.N + 1, device="cuda")
@@ -119,9 +124,10 @@ def test_unaligned_pointers(sdnn, oracle_mod):
     assert_parity(Yv.cpu().numpy(), Yo, S, "unaligned")
 
 
+@pytest.mark.parametrize("kernel", ["row", "group"])
 @pytest.mark.parametrize("M,K,N,dens", [(1, 1, 4, 1.0), (1, 500, 8, 0.3), (500, 1, 8, 0.5), (37, 65, 12, 1.0),
                                         (129, 257, 20, 0.0), (64, 64, 64, 1.0), (2100, 70, 40, 0.05)])
-def test_degenerate_shapes(sdnn, oracle_mod, M, K, N, dens):
+def test_degenerate_shapes(sdnn, oracle_mod, M, K, N, dens, kernel):
     rng = np.random.default_rng(M + K + N)
     mask = rng.random((M, K)) < dens
     rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum(mask.sum(1))
@@ -131,8 +137,8 @@ def test_degenerate_shapes(sdnn, oracle_mod, M, K, N, dens):
     p = synth.Problem("deg", M, K, N, 0, "x", rp, ci, v, b, 1, 0)
     X = rng.standard_normal((K, N)).astype(np.float32)
     for act in (0, 1):
-        check(sdnn, oracle_mod, p, X=X, act=act)
-    check(sdnn, oracle_mod, p, X=X, act=1, bias=None)
+        check(sdnn, oracle_mod, p, X=X, act=act, kernel=kernel)
+    check(sdnn, oracle_mod, p, X=X, act=1, bias=None, kernel=kernel)
 
 
 def test_empty_weight(sdnn, oracle_mod):
@@ -157,7 +163,8 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
     X = p.x()
     ref, _ = run_gpu(sdnn, p, X, p.bias, 1)
     for opts in [dict(permute=False), dict(panel_rows=8), dict(cta_panels=1), dict(k_chunk=8),
-                 dict(k_chunk=96, panel_rows=4, cta_panels=2)]:
+                 dict(k_chunk=96, panel_rows=4, cta_panels=2), dict(kernel="group"), dict(kernel="row"),
+                 dict(kernel="group", permute=False), dict(kernel="group", cta_panels=3, k_chunk=16)]:
         Y, _ = run_gpu(sdnn, p, X, p.bias, 1, **opts)
         np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
 

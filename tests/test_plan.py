@@ -10,6 +10,8 @@ import sdnn_synth as synth
 def decode(p, plan):
     """Decode the exported plan back into (orig_row, col, val) triples, checking the layout."""
     info = plan.info()
+    if info["kernel"] == 2:
+        return decode_group(p, plan)
     row_orig, blk_off, meta = plan.export()
     rw, wc, kc, nch, nrb = (info[k] for k in ("panel_rows", "cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
     rcta = rw * wc
@@ -43,6 +45,40 @@ def decode(p, plan):
     return info, row_orig, triples
 
 
+def decode_group(p, plan):
+    info = plan.info()
+    row_orig, blk_off, meta = plan.export()
+    wc, kc, nch, nrb = (info[k] for k in ("cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
+    assert info["panel_rows"] == 16
+    assert blk_off[0] == 0 and blk_off[-1] == meta.size and np.all(blk_off % 16 == 0)
+    triples, last_col, entries = [], {}, 0
+    for b in range(nrb):
+        for j in range(nch):
+            blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]].view(np.uint32)
+            for w in range(wc):
+                hoff, n, woff = int(blk[4 * w]), int(blk[4 * w + 1]), int(blk[4 * w + 2])
+                assert hoff % 4 == 0
+                wts = blk[woff:].view(np.float32)
+                wi, prev = 0, -1
+                for e in range(n):
+                    h = int(blk[hoff + e])
+                    cl, mask = h & 0xFFFF, (h >> 16) & 0xFF | ((h >> 24) << 8)
+                    assert 0 <= cl < kc and cl > prev and mask != 0  # union columns ascend, no empty entry
+                    prev = cl
+                    entries += 1
+                    for r in range(16):
+                        if mask >> r & 1:
+                            orow = int(row_orig[(b * wc + w) * 16 + r])
+                            assert orow >= 0
+                            col = j * kc + cl
+                            assert col > last_col.get(orow, -1)
+                            last_col[orow] = col
+                            triples.append((orow, col, wts[wi]))
+                            wi += 1
+    assert abs(entries * 1000 // max(p.nnz, 1) - info["group_entries_per_nnz_x1000"]) <= 1
+    return info, row_orig, triples
+
+
 def csr_triples(p):
     r = np.repeat(np.arange(p.M), np.diff(p.row_ptr))
     return sorted(zip(r.tolist(), p.col_idx.tolist(), p.vals.tolist()))
@@ -71,6 +107,8 @@ def test_c_alg1_equals_bruteforce_random(oracle_mod, seed):
 @pytest.mark.parametrize("key,opts", [
     ("c1", {}), ("c1", dict(permute=False)), ("c2_768x3072", {}), ("c3_128x64", dict(panel_rows=8, cta_panels=3)),
     ("c4_512x2048_s80", dict(k_chunk=8)), ("c3_256x128", dict(k_chunk=96, cta_panels=1)),
+    ("c1", dict(kernel="group")), ("c2_768x3072", dict(kernel="group")), ("c3_128x64", dict(kernel="group", cta_panels=3)),
+    ("c4_2048x512_s95", dict(kernel="group", k_chunk=16)), ("c2_768x768", dict(kernel="group", permute=False)),
 ])
 def test_packing_invariants(oracle_mod, key, opts):
     p = synth.config_problem(key, N=4)
@@ -87,6 +125,17 @@ def test_packing_invariants(oracle_mod, key, opts):
     assert info["max_panel_nnz"] >= cnt.max()
 
 
+def test_auto_kernel_choice_and_alg1_benefit():
+    """The cost model picks the group kernel where 16-row unions are small, and Algorithm 1 shrinks
+    the unions on structured masks (the paper's reason for the permutation)."""
+    for key in ("c2_768x768", "c4_2048x512_s80"):
+        p = synth.config_problem(key, N=4)
+        a = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="group").info()
+        b = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="group", permute=False).info()
+        assert a["group_entries_per_nnz_x1000"] < b["group_entries_per_nnz_x1000"], key
+        assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).info()["kernel"] == 2
+
+
 def test_degenerate_shapes():
     for M, K, dens in [(1, 1, 1.0), (1, 300, 0.5), (300, 1, 0.5), (5, 7, 0.0), (33, 65, 1.0)]:
         rng = np.random.default_rng(M * K)
@@ -95,9 +144,10 @@ def test_degenerate_shapes():
         ci = np.nonzero(mask)[1].astype(np.int32)
         v = rng.standard_normal(ci.size).astype(np.float32)
         p = synth.Problem("d", M, K, 1, 0, "x", rp, ci, v, None, 0, 0)
-        plan = sdnn.Plan(rp, ci, v, M, K)
-        _, _, triples = decode(p, plan)
-        assert sorted(triples) == csr_triples(p)
+        for kernel in ("row", "group"):
+            plan = sdnn.Plan(rp, ci, v, M, K, kernel=kernel)
+            _, _, triples = decode(p, plan)
+            assert sorted(triples) == csr_triples(p)
 
 
 def test_plan_deterministic():
