@@ -89,7 +89,7 @@ void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32
 //               entries {uint32 col_local, float w}, each row segment starting at an even entry.
 //  group kernel header: W_c × 16 B {head_off_words, n_entries, w_off_words, 0}; per warp the
 //               entry heads (uint32: col_local | mask_bank0 << 16 | mask_bank1 << 24) padded to
-//               16 B; then per warp the weights, in entry order, bank-0 rows then bank-1 rows.
+//               16 B; then per warp the weights, in entry order, rows in descending order.
 // Emitter: walks blocks in order; with `out` == nullptr it only computes the block sizes.
 // ------------------------------------------------------------------------------------------------
 struct Geometry {
@@ -162,7 +162,7 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
             if (!mask[cl]) continue;
             const uint32_t m = mask[cl];
             wh[w].push_back(uint32_t(cl) | ((m & 0xffu) << 16) | ((m >> 8) << 24));
-            for (int32_t r = 0; r < 16; ++r)
+            for (int32_t r = 15; r >= 0; --r)  // descending rows: the kernel walks bits MSB first
               if (m >> r & 1u) ww[w].push_back(wv[size_t(cl) * 16 + r]);
           }
           head_words += align_up(int64_t(wh[w].size()), 4);

@@ -22,7 +22,7 @@
 #include <vector>
 
 #include "sdnn_internal.h"
-#include "group_dispatch.inc"
+#include "group_entry.inc"
 
 namespace sdnn {
 void plan_fill_info(const Plan& p, int32_t device, sdnn_info* info);
@@ -132,53 +132,42 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
   }
 }
 
-// Group kernel, one chunk: the warp owns a 16-row group (two banks of 8 rows).  For every column of
-// the group's union in this chunk: one X row slice load (V floats per lane) feeds the FMAs of every
-// nonzero of the group in that column, dispatched on the bank's 8-bit mask to a specialised case
-// whose accumulator registers are named statically (group_dispatch.inc; "statically encoding
-// the accumulation position in the vector register name").  Columns ascend, so every row still
+// Group kernel, one chunk: the warp owns a 16-row group.  For every column of the group's union in
+// this chunk one X row slice load (V floats per lane) feeds the FMAs of every nonzero of the group
+// in that column; each nonzero jumps through a 16-entry branch table to a snippet that names its
+// row's accumulators statically (group_entry.inc, generated; "statically encoding the
+// accumulation position in the vector register name").  Columns ascend, so every row still
 // accumulates in ascending column order (bitwise identical to the row kernel).
 template <int V>
-__device__ __forceinline__ void group_entry(float2 (&acc)[16][V / 2], uint32_t h, const float* __restrict__ xl,
-                                         const float*& wp) {
-  constexpr int TN = 32 * V;
-  const float* xp = xl + (h & 0xffffu) * TN;
-  float2 xq[V / 2];
-  {
-    const float4 a = *reinterpret_cast<const float4*>(xp);
-    xq[0] = make_float2(a.x, a.y);
-    xq[1] = make_float2(a.z, a.w);
-    if constexpr (V == 8) {
-      const float4 b = *reinterpret_cast<const float4*>(xp + 128);
-      xq[2] = make_float2(b.x, b.y);
-      xq[3] = make_float2(b.z, b.w);
-    }
-  }
-  const uint32_t m0 = (h >> 16) & 0xffu, m1 = h >> 24;
-  if (m0) { SDNN_DISPATCH_BANK0(m0) }
-  if (m1) { SDNN_DISPATCH_BANK1(m1) }
-}
-
-template <int V>
-__device__ __forceinline__ void consume_group(float2 (&acc)[16][V / 2], const float* __restrict__ xs,
+__device__ __forceinline__ void consume_group(uint64_t (&acc)[16][V / 2], const float* __restrict__ xs,
                                               const uint8_t* __restrict__ ms, int warp, int lane) {
   const uint4 hd = reinterpret_cast<const uint4*>(ms)[warp];
   const uint32_t* heads = reinterpret_cast<const uint32_t*>(ms) + hd.x;
   const int n = int(hd.y);
-  const float* wp = reinterpret_cast<const float*>(ms) + hd.z;
-  const float* xl = xs + lane * 4;
+  uint32_t wp = smem_u32(ms) + hd.z * 4u;
+  const uint32_t xl = smem_u32(xs) + uint32_t(lane) * 16u;
   uint4 h4 = make_uint4(0, 0, 0, 0);
   for (int e = 0; e < n; ++e) {
     const int t = e & 3;
     if (t == 0) h4 = *reinterpret_cast<const uint4*>(heads + e);
     const uint32_t h = t == 0 ? h4.x : t == 1 ? h4.y : t == 2 ? h4.z : h4.w;
-    group_entry<V>(acc, h, xl, wp);
+    if constexpr (V == 8) group_entry_v8(acc, h, xl, wp);
+    else group_entry_v4(acc, h, xl, wp);
   }
 }
 
 // Fused epilogue: y = acc + b[orig]; ReLU; store to Y[orig][n0 + ...] (inverse permutation).
-template <int RW, int V, bool VEC>
-__device__ __forceinline__ void epilogue(const float2 (&acc)[RW][V / 2], const KParams& p, int panel, int lane,
+__device__ __forceinline__ float2 as_f2(float2 v) { return v; }
+__device__ __forceinline__ float2 as_f2(uint64_t v) {
+  return make_float2(__uint_as_float(uint32_t(v)), __uint_as_float(uint32_t(v >> 32)));
+}
+// accumulator register type: float2 (row kernel, CUDA C++ FFMA2) or its bit pattern (group kernel PTX)
+template <int KIND> struct AccSel { using type = float2; };
+template <> struct AccSel<2> { using type = uint64_t; };
+template <int KIND> using AccT = typename AccSel<KIND>::type;
+
+template <int RW, int V, bool VEC, typename A>
+__device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParams& p, int panel, int lane,
                                          int64_t n0) {
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
@@ -189,7 +178,8 @@ __device__ __forceinline__ void epilogue(const float2 (&acc)[RW][V / 2], const K
 #pragma unroll
     for (int h = 0; h < V / 4; ++h) {
       const int64_t n = n0 + h * 128 + lane * 4;
-      float v[4] = {acc[r][2 * h].x + b, acc[r][2 * h].y + b, acc[r][2 * h + 1].x + b, acc[r][2 * h + 1].y + b};
+      const float2 a0 = as_f2(acc[r][2 * h]), a1 = as_f2(acc[r][2 * h + 1]);
+      float v[4] = {a0.x + b, a0.y + b, a1.x + b, a1.y + b};
       if (p.act == SDNN_ACT_RELU) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) v[q] = v[q] > 0.f ? v[q] : 0.f;
@@ -245,11 +235,11 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
     return;
   }
 
-  float2 acc[RW][V / 2];
+  AccT<KIND> acc[RW][V / 2];
 #pragma unroll
   for (int r = 0; r < RW; ++r)
 #pragma unroll
-    for (int q = 0; q < V / 2; ++q) acc[r][q] = make_float2(0.f, 0.f);
+    for (int q = 0; q < V / 2; ++q) acc[r][q] = AccT<KIND>{};
 
   for (int j = 0; j < p.nch; ++j) {
     const int s = j % S;
@@ -280,11 +270,11 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) 
   const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
   const int nthr = blockDim.x;
 
-  float2 acc[RW][V / 2];
+  AccT<KIND> acc[RW][V / 2];
 #pragma unroll
   for (int r = 0; r < RW; ++r)
 #pragma unroll
-    for (int q = 0; q < V / 2; ++q) acc[r][q] = make_float2(0.f, 0.f);
+    for (int q = 0; q < V / 2; ++q) acc[r][q] = AccT<KIND>{};
 
   for (int j = 0; j < p.nch; ++j) {
     __syncthreads();

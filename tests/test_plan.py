@@ -66,7 +66,7 @@ def decode_group(p, plan):
                     assert 0 <= cl < kc and cl > prev and mask != 0  # union columns ascend, no empty entry
                     prev = cl
                     entries += 1
-                    for r in range(16):
+                    for r in range(15, -1, -1):  # weights stored in descending row order
                         if mask >> r & 1:
                             orow = int(row_orig[(b * wc + w) * 16 + r])
                             assert orow >= 0
