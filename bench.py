@@ -222,7 +222,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
 
     # ---- preparation stage (once): Algorithm 1 + packing + upload
     t0 = time.perf_counter()
-    h = sdnn.Handle.from_problem(p, kernel=args.kernel)
+    h = sdnn.Handle.from_problem(p, kernel=args.kernel, group_sb=args.group_sb)
     prep_ms = 1e3 * (time.perf_counter() - t0)
     info = h.info()
     same = check_same_across_ranks(plan_hash(info, h.permutation()), dist)
@@ -334,7 +334,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
                    "l2": "inputs larger than L2 (X shard %.0f MiB > 126 MB L2); no flush" % (p.K * Nr * 4 / 2**20),
                    "kernel": f"{KERNEL}<{'group' if info['kernel'] == 2 else 'row'},R_w={info['panel_rows']},"
                              f"V={'8' if info['num_row_blocks'] * ((Nr + 255) // 256) >= 296 else '4'}>",
-                   "group_entries_per_nnz": info["group_entries_per_nnz_x1000"] / 1000,
+                   "group_entries_per_nnz": info["group_entries_per_nnz_x1000"] / 1000, "group_sb": info["group_sb"],
                    "panel_rows": info["panel_rows"], "cta_panels": info["cta_panels"], "k_chunk": info["k_chunk"],
                    "permuted": bool(info["permuted"]), "prep_ms": round(prep_ms, 1), "plan_hash_identical": same},
         "roofline": {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(fp32_peak_tf, 2),
@@ -370,6 +370,7 @@ def main(argv=None):
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--allgather", action="store_true")
     ap.add_argument("--kernel", choices=["auto", "row", "group"], default="auto")
+    ap.add_argument("--group-sb", type=int, default=0, choices=[0, 1, 2, 4])
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=12.0)

@@ -63,6 +63,7 @@ typedef struct {
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
                                multiple of 8                                                        */
+  int32_t group_sb;         /* group kernel sub-block rows: 0 = auto (cost model), 1, 2 or 4         */
   uint32_t flags;           /* reserved, must be 0                                                   */
 } sdnn_perm_opts;
 
@@ -75,6 +76,8 @@ typedef struct {
   int32_t permuted;         /* 1 if Algorithm 1 was applied                                           */
   int32_t kernel;           /* 1 = row kernel, 2 = group kernel                                       */
   int32_t group_entries_per_nnz_x1000; /* group format: union entries per nonzero · 1000            */
+  int32_t group_sb;         /* group kernel sub-block rows (0 for the row kernel)                     */
+  int32_t group_subblocks_per_nnz_x1000; /* nonzero sub-blocks per nonzero · 1000                    */
   int32_t panel_rows;       /* R_w: rows per warp panel                                               */
   int32_t cta_panels;       /* W_c: panels per CTA                                                    */
   int32_t num_panels;       /* P = num_row_blocks · W_c (trailing panels may be empty)               */

@@ -40,13 +40,15 @@ class SdnnError(RuntimeError):
 class PermOpts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("permute", ctypes.c_int32), ("kernel", ctypes.c_int32),
                 ("panel_rows_max", ctypes.c_int32),
-                ("cta_panels", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+                ("cta_panels", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("group_sb", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
 
 
 class Info(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("M", ctypes.c_int32), ("K", ctypes.c_int32),
                 ("nnz", ctypes.c_int64), ("device", ctypes.c_int32), ("permuted", ctypes.c_int32),
                 ("kernel", ctypes.c_int32), ("group_entries_per_nnz_x1000", ctypes.c_int32),
+                ("group_sb", ctypes.c_int32), ("group_subblocks_per_nnz_x1000", ctypes.c_int32),
                 ("panel_rows", ctypes.c_int32), ("cta_panels", ctypes.c_int32), ("num_panels", ctypes.c_int32),
                 ("num_row_blocks", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("meta_bytes", ctypes.c_int64), ("max_block_bytes", ctypes.c_int32), ("reserved0", ctypes.c_int32),
@@ -95,9 +97,10 @@ def _csr(row_ptr, col_idx, vals):
 KERNELS = {"auto": 0, "row": 1, "group": 2}
 
 
-def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0):
+def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0):
     k = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
-    return PermOpts(ctypes.sizeof(PermOpts), int(bool(permute)), k, int(panel_rows), int(cta_panels), int(k_chunk), 0)
+    return PermOpts(ctypes.sizeof(PermOpts), int(bool(permute)), k, int(panel_rows), int(cta_panels), int(k_chunk),
+                    int(group_sb), 0)
 
 
 def _act(act) -> int:

@@ -24,6 +24,8 @@ struct Plan {
   int32_t permuted = 0;
   int32_t kernel = 1;          // 1 = row kernel, 2 = group kernel
   int64_t group_entries = 0;   // union entries of the group format
+  int32_t group_sb = 0;        // group kernel sub-block rows (1, 2 or 4)
+  int64_t group_subblocks = 0; // nonzero sub-blocks over all entries
   int32_t panel_rows = 0, cta_panels = 0, num_panels = 0, num_row_blocks = 0;
   int32_t k_chunk = 0, num_chunks = 0;
   int32_t max_block_bytes = 0;

@@ -88,21 +88,26 @@ void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32
 //  row kernel   header: R_cta uint32 words (start_entry << 16 | count), padded to 16 B; then 8-byte
 //               entries {uint32 col_local, float w}, each row segment starting at an even entry.
 //  group kernel header: W_c × 16 B {head_off_words, n_entries, w_off_words, 0}; per warp the
-//               entry heads (uint32: col_local | mask_bank0 << 16 | mask_bank1 << 24) padded to
-//               16 B; then per warp the weights, in entry order, rows in descending order.
+//               entry heads (uint32: col_local | sub-block mask << 16; 16/SB sub-blocks of SB
+//               rows) padded to 16 B; then per warp the weights: for each entry, for each nonzero
+//               sub-block in ascending order, SB weights (0 for rows without a nonzero), 16-B aligned.
 // Emitter: walks blocks in order; with `out` == nullptr it only computes the block sizes.
 // ------------------------------------------------------------------------------------------------
 struct Geometry {
-  int32_t kernel, rw, wc, kc, nch, nrb;
+  int32_t kernel, rw, wc, kc, nch, nrb, sb;
+};
+struct EmitStats {
+  int64_t entries = 0;    // row kernel: padded entries; group kernel: union entries
+  int64_t subblocks = 0;  // group kernel: nonzero sub-blocks over all entries
 };
 
 static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals,
                         const std::vector<int32_t>& row_orig, const Geometry& g, std::vector<int64_t>& sizes,
-                        uint8_t* out, const std::vector<int64_t>* offs, int64_t* entries_total) {
+                        uint8_t* out, const std::vector<int64_t>* offs, EmitStats* stats) {
   const int32_t rcta = g.rw * g.wc;
   sizes.assign(size_t(g.nrb) * g.nch, 0);
   std::vector<int32_t> cur(rcta);
-  int64_t ent_total = 0;
+  int64_t ent_total = 0, sb_total = 0;
   // group scratch
   std::vector<uint16_t> mask(g.kc);
   std::vector<float> wv(size_t(g.kc) * 16);
@@ -161,12 +166,19 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
           for (int32_t cl = 0; cl < g.kc; ++cl) {
             if (!mask[cl]) continue;
             const uint32_t m = mask[cl];
-            wh[w].push_back(uint32_t(cl) | ((m & 0xffu) << 16) | ((m >> 8) << 24));
-            for (int32_t r = 15; r >= 0; --r)  // descending rows: the kernel walks bits MSB first
-              if (m >> r & 1u) ww[w].push_back(wv[size_t(cl) * 16 + r]);
+            uint32_t sbm = 0;
+            for (int32_t sb = 0; sb < 16 / g.sb; ++sb) {
+              const uint32_t part = (m >> (sb * g.sb)) & ((1u << g.sb) - 1u);
+              if (!part) continue;
+              sbm |= 1u << sb;
+              for (int32_t i = 0; i < g.sb; ++i)  // SB weights, zero for rows without a nonzero
+                ww[w].push_back(part >> i & 1u ? wv[size_t(cl) * 16 + sb * g.sb + i] : 0.f);
+              ++sb_total;
+            }
+            wh[w].push_back(uint32_t(cl) | (sbm << 16));
           }
           head_words += align_up(int64_t(wh[w].size()), 4);
-          w_words += int64_t(ww[w].size());
+          w_words += align_up(int64_t(ww[w].size()), 4);
           ent_total += int64_t(wh[w].size());
         }
         bytes = align_up(hdr + head_words * 4 + w_words * 4, 16);
@@ -181,14 +193,17 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
             std::memcpy(h32 + hpos, wh[w].data(), wh[w].size() * 4);
             hpos += align_up(int64_t(wh[w].size()), 4);
             std::memcpy(h32 + wpos, ww[w].data(), ww[w].size() * 4);
-            wpos += int64_t(ww[w].size());
+            wpos += align_up(int64_t(ww[w].size()), 4);  // 16-byte aligned vector weight loads
           }
         }
       }
       sizes[size_t(b) * g.nch + j] = bytes;
     }
   }
-  if (entries_total) *entries_total = ent_total;
+  if (stats) {
+    stats->entries = ent_total;
+    stats->subblocks = sb_total;
+  }
 }
 
 static int64_t max_of(const std::vector<int64_t>& v) {
@@ -220,6 +235,8 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     if (o.cta_panels < 0 || o.cta_panels > 16) return fail(SDNN_ERR_INVALID_ARGUMENT, "cta_panels must be 0..16");
     if (o.kernel == 2 && o.cta_panels > kMaxGroupWarps)
       return fail(SDNN_ERR_INVALID_ARGUMENT, "cta_panels must be <= 11 with the group kernel");
+    if (o.group_sb != 0 && o.group_sb != 1 && o.group_sb != 2 && o.group_sb != 4)
+      return fail(SDNN_ERR_INVALID_ARGUMENT, "group_sb must be 0, 1, 2 or 4");
     if (o.k_chunk != 0 && (o.k_chunk < 8 || o.k_chunk > 128 || o.k_chunk % 8))
       return fail(SDNN_ERR_INVALID_ARGUMENT, "k_chunk must be 0 or a multiple of 8 in [8, 128]");
   }
@@ -243,9 +260,10 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     // Candidate geometries: the row kernel (R_w rows per warp) and the group kernel (16 rows per
     // warp).  Launch geometry: W_c warps per CTA, enough row blocks to fill
     // the machine for the typical N.
-    auto make_geo = [&](int32_t kernel) {
+    auto make_geo = [&](int32_t kernel, int32_t sb) {
       Geometry g{};
       g.kernel = kernel;
+      g.sb = sb;
       g.rw = kernel == 2 ? 16 : (o.panel_rows_max ? o.panel_rows_max : (M >= 2048 ? 8 : 4));
       int32_t wc = o.cta_panels;
       if (!wc) {
@@ -263,7 +281,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     };
     // K chunk (split-K tiling along the reduction dimension): the largest KC whose stage
     // (X tile at the widest N tile + metadata block) fits three times in the shared-memory budget.
-    auto choose_kc = [&](Geometry& g, const std::vector<int32_t>& ro, int64_t* entries) -> bool {
+    auto choose_kc = [&](Geometry& g, const std::vector<int32_t>& ro, EmitStats* entries) -> bool {
       std::vector<int64_t> sizes;
       const int32_t cands[] = {64, 32, 16, 8};
       for (int32_t c : cands) {
@@ -283,31 +301,37 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       return false;
     };
 
+    // Cost model (SM cycles per warp-level unit of work at V = 8 floats per lane; DESIGN.md
+    // "Kernel choice"): shared-memory wavefronts at 128 B/clk (≈85 % attainable), FMA pipe at 128
+    // lanes/clk, issue at 4 warp-instructions/clk.  Row kernel per nonzero: 8 X wavefronts + 0.5
+    // entry.  Group kernel per union entry: 8 X wavefronts + 0.25 head + 1 per nonzero sub-block
+    // (weights), 2·SB FMA cycles per nonzero sub-block, issue ≈ (2·16/SB + nsb·(2 + 4·SB) + 8) / 4.
+    auto cost = [&](const Geometry& g, const EmitStats& st) {
+      if (g.kernel == 1) return 8.5 / 0.85 * double(nnz);
+      const double E = double(st.entries), S = double(st.subblocks);
+      const double lds = (8.25 * E + S) / 0.85, fma = 2.0 * g.sb * S / 0.95;
+      const double issue = (2.0 * (16 / g.sb) * E + S * (2 + 4 * g.sb) + 8 * E) / 4.0;
+      return std::max(lds, std::max(fma, issue));
+    };
     Geometry g{};
     std::vector<int32_t> ro;
-    int64_t entries = 0;
-    if (o.kernel == 1 || o.kernel == 2) {
-      g = make_geo(o.kernel);
-      ro = row_orig_for(g);
-      if (!choose_kc(g, ro, &entries))
-        return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
-    } else {
-      // Cost model (shared-memory wavefronts per warp, V = 8 floats per lane): row kernel
-      // 8 per nonzero + 0.5 (entry pairs); group kernel 8 per union entry + 0.25 (heads) + 1 per
-      // nonzero (weights).  Pick the group kernel when it saves >= 10 %.
-      Geometry gr = make_geo(1), gg = make_geo(2);
-      std::vector<int32_t> ror = row_orig_for(gr), rog = row_orig_for(gg);
-      int64_t er = 0, eg = 0;
-      const bool okr = choose_kc(gr, ror, &er);
-      const bool okg = choose_kc(gg, rog, &eg);
-      const double cost_r = 8.5 * double(nnz), cost_g = 8.25 * double(eg) + double(nnz);
-      if (okg && (!okr || cost_g < 0.9 * cost_r)) {
-        g = gg; ro.swap(rog); entries = eg;
-      } else if (okr) {
-        g = gr; ro.swap(ror); entries = er;
-      } else {
-        return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
+    EmitStats stats;
+    {
+      std::vector<Geometry> cands;
+      if (o.kernel != 2) cands.push_back(make_geo(1, 0));
+      if (o.kernel != 1)
+        for (int32_t sb : {1, 2, 4})
+          if (!o.group_sb || o.group_sb == sb) cands.push_back(make_geo(2, sb));
+      double best = 0;
+      bool found = false;
+      for (Geometry c : cands) {
+        std::vector<int32_t> r = row_orig_for(c);
+        EmitStats st;
+        if (!choose_kc(c, r, &st)) continue;
+        const double cc = cost(c, st);
+        if (!found || cc < best) { best = cc; g = c; ro.swap(r); stats = st; found = true; }
       }
+      if (!found) return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
     }
     plan.kernel = g.kernel;
     plan.panel_rows = g.rw;
@@ -326,8 +350,10 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       plan.max_panel_nnz = std::max(plan.max_panel_nnz, s);
     }
     std::vector<int64_t> sizes;
-    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, nullptr, nullptr, &entries);
-    plan.group_entries = g.kernel == 2 ? entries : 0;
+    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, nullptr, nullptr, &stats);
+    plan.group_entries = g.kernel == 2 ? stats.entries : 0;
+    plan.group_sb = g.kernel == 2 ? g.sb : 0;
+    plan.group_subblocks = g.kernel == 2 ? stats.subblocks : 0;
     plan.max_block_bytes = int32_t(max_of(sizes));
     plan.blk_off.assign(sizes.size() + 1, 0);
     for (size_t i = 0; i < sizes.size(); ++i) plan.blk_off[i + 1] = plan.blk_off[i] + sizes[i];
@@ -355,6 +381,8 @@ static void fill_info(const Plan& p, int32_t device, sdnn_info* info) {
   info->permuted = p.permuted;
   info->kernel = p.kernel;
   info->group_entries_per_nnz_x1000 = p.nnz ? int32_t(1000 * p.group_entries / p.nnz) : 0;
+  info->group_sb = p.group_sb;
+  info->group_subblocks_per_nnz_x1000 = p.nnz ? int32_t(1000 * p.group_subblocks / p.nnz) : 0;
   info->panel_rows = p.panel_rows;
   info->cta_panels = p.cta_panels;
   info->num_panels = p.num_panels;

@@ -138,7 +138,7 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
 // row's accumulators statically (group_entry.inc, generated; "statically encoding the
 // accumulation position in the vector register name").  Columns ascend, so every row still
 // accumulates in ascending column order (bitwise identical to the row kernel).
-template <int V>
+template <int V, int SB>
 __device__ __forceinline__ void consume_group(uint64_t (&acc)[16][V / 2], const float* __restrict__ xs,
                                               const uint8_t* __restrict__ ms, int warp, int lane) {
   const uint4 hd = reinterpret_cast<const uint4*>(ms)[warp];
@@ -151,8 +151,12 @@ __device__ __forceinline__ void consume_group(uint64_t (&acc)[16][V / 2], const 
     const int t = e & 3;
     if (t == 0) h4 = *reinterpret_cast<const uint4*>(heads + e);
     const uint32_t h = t == 0 ? h4.x : t == 1 ? h4.y : t == 2 ? h4.z : h4.w;
-    if constexpr (V == 8) group_entry_v8(acc, h, xl, wp);
-    else group_entry_v4(acc, h, xl, wp);
+    if constexpr (V == 8 && SB == 1) group_entry_v8_sb1(acc, h, xl, wp);
+    else if constexpr (V == 8 && SB == 2) group_entry_v8_sb2(acc, h, xl, wp);
+    else if constexpr (V == 8) group_entry_v8_sb4(acc, h, xl, wp);
+    else if constexpr (SB == 1) group_entry_v4_sb1(acc, h, xl, wp);
+    else if constexpr (SB == 2) group_entry_v4_sb2(acc, h, xl, wp);
+    else group_entry_v4_sb4(acc, h, xl, wp);
   }
 }
 
@@ -197,7 +201,7 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
 
 // Fast path: TMA producer warp + W_c consumer warps, mbarrier stage ring.
 // KIND 1 = row kernel (RW rows per warp), KIND 2 = group kernel (RW = 16).
-template <int KIND, int RW, int V>
+template <int KIND, int RW, int V, int SB = 0>
 __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 32, 1)
     spmm_tma_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
     mbar_wait(&full[s], (j / S) & 1);
     const float* xs = reinterpret_cast<const float*>(xstage + size_t(s) * p.x_stage_bytes);
     if constexpr (KIND == 2)
-      consume_group<V>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane);
+      consume_group<V, SB>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane);
     else
       consume_chunk<RW, V>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane, p.hdr_bytes);
     __syncwarp();
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
 
 // Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
 // threads using bounds-checked loads (zero fill) and a block barrier instead of TMA/mbarriers.
-template <int KIND, int RW, int V>
+template <int KIND, int RW, int V, int SB = 0>
 __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) spmm_generic_kernel(const KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * V;
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) 
     for (int idx = threadIdx.x; idx < mbytes / 16; idx += nthr) reinterpret_cast<uint4*>(ms)[idx] = src[idx];
     __syncthreads();
     if constexpr (KIND == 2)
-      consume_group<V>(acc, xs, ms, warp, lane);
+      consume_group<V, SB>(acc, xs, ms, warp, lane);
     else
       consume_chunk<RW, V>(acc, xs, ms, warp, lane, p.hdr_bytes);
   }
@@ -322,12 +326,12 @@ static PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
-template <int KIND, int RW, int V>
+template <int KIND, int RW, int V, int SB = 0>
 static cudaError_t set_smem_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(spmm_tma_kernel<KIND, RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(spmm_tma_kernel<KIND, RW, V, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBudget + 1024);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(spmm_generic_kernel<KIND, RW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(spmm_generic_kernel<KIND, RW, V, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kSmemBudget + 1024);
 }
 
@@ -381,8 +385,13 @@ static sdnn_status launch(const sdnn_handle_s* h, const float* X, int64_t N, con
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
     const dim3 grid{unsigned(nblocks)}, block{unsigned((wc + 1) * 32)};
-    if (pl.kernel == 2 && V == 8) spmm_tma_kernel<2, 16, 8><<<grid, block, smem, stream>>>(tmap, p);
-    else if (pl.kernel == 2) spmm_tma_kernel<2, 16, 4><<<grid, block, smem, stream>>>(tmap, p);
+    const int sb = pl.group_sb;
+    if (pl.kernel == 2 && V == 8 && sb == 1) spmm_tma_kernel<2, 16, 8, 1><<<grid, block, smem, stream>>>(tmap, p);
+    else if (pl.kernel == 2 && V == 8 && sb == 2) spmm_tma_kernel<2, 16, 8, 2><<<grid, block, smem, stream>>>(tmap, p);
+    else if (pl.kernel == 2 && V == 8) spmm_tma_kernel<2, 16, 8, 4><<<grid, block, smem, stream>>>(tmap, p);
+    else if (pl.kernel == 2 && sb == 1) spmm_tma_kernel<2, 16, 4, 1><<<grid, block, smem, stream>>>(tmap, p);
+    else if (pl.kernel == 2 && sb == 2) spmm_tma_kernel<2, 16, 4, 2><<<grid, block, smem, stream>>>(tmap, p);
+    else if (pl.kernel == 2) spmm_tma_kernel<2, 16, 4, 4><<<grid, block, smem, stream>>>(tmap, p);
     else if (rw == 8 && V == 8) spmm_tma_kernel<1, 8, 8><<<grid, block, smem, stream>>>(tmap, p);
     else if (rw == 8 && V == 4) spmm_tma_kernel<1, 8, 4><<<grid, block, smem, stream>>>(tmap, p);
     else if (rw == 4 && V == 8) spmm_tma_kernel<1, 4, 8><<<grid, block, smem, stream>>>(tmap, p);
@@ -391,8 +400,13 @@ static sdnn_status launch(const sdnn_handle_s* h, const float* X, int64_t N, con
     p.stages = 1;
     const size_t smem = size_t(p.x_stage_bytes) + p.m_stage_bytes;
     const dim3 grid{unsigned(nblocks)}, block{unsigned(wc * 32)};
-    if (pl.kernel == 2 && V == 8) spmm_generic_kernel<2, 16, 8><<<grid, block, smem, stream>>>(p);
-    else if (pl.kernel == 2) spmm_generic_kernel<2, 16, 4><<<grid, block, smem, stream>>>(p);
+    const int sb = pl.group_sb;
+    if (pl.kernel == 2 && V == 8 && sb == 1) spmm_generic_kernel<2, 16, 8, 1><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 2 && V == 8 && sb == 2) spmm_generic_kernel<2, 16, 8, 2><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 2 && V == 8) spmm_generic_kernel<2, 16, 8, 4><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 2 && sb == 1) spmm_generic_kernel<2, 16, 4, 1><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 2 && sb == 2) spmm_generic_kernel<2, 16, 4, 2><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 2) spmm_generic_kernel<2, 16, 4, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 8) spmm_generic_kernel<1, 8, 8><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 4) spmm_generic_kernel<1, 8, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 4 && V == 8) spmm_generic_kernel<1, 4, 8><<<grid, block, smem, stream>>>(p);
@@ -445,8 +459,12 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
     if (ae == cudaSuccess) ae = set_smem_attrs<1, 8, 4>();
     if (ae == cudaSuccess) ae = set_smem_attrs<1, 4, 8>();
     if (ae == cudaSuccess) ae = set_smem_attrs<1, 4, 4>();
-    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8>();
-    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8, 1>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8, 2>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8, 4>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 1>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 2>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 4>();
   });
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     cudaFree(h->d_meta);

