@@ -274,9 +274,44 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       g.nrb = (M + g.rw * wc - 1) / (g.rw * wc);
       return g;
     };
+    // Row → (CTA, warp, slot) assignment.  Group kernel: the Algorithm 1 order itself, so rows
+    // with similar patterns share a 16-row group.  Row kernel: every nonzero costs the
+    // same wherever its row sits, so rows are dealt to warps by nnz instead — longest-processing-
+    // time first onto the least-loaded warp with a free slot — which keeps the heavy rows of a
+    // skewed (log-normal) matrix from piling into one warp.  Within a warp the rows keep their
+    // Algorithm 1 order.
     auto row_orig_for = [&](const Geometry& g) {
-      std::vector<int32_t> ro(size_t(g.nrb) * g.wc * g.rw, -1);
-      for (int32_t p = 0; p < M; ++p) ro[p] = plan.perm[p];
+      const int32_t nw = g.nrb * g.wc;
+      std::vector<int32_t> ro(size_t(nw) * g.rw, -1);
+      if (g.kernel == 2) {
+        for (int32_t p = 0; p < M; ++p) ro[p] = plan.perm[p];
+        return ro;
+      }
+      std::vector<int32_t> pos(M), order(M);
+      for (int32_t i = 0; i < M; ++i) { pos[plan.perm[i]] = i; order[i] = i; }
+      auto nz = [&](int32_t r) { return csr_ptr[r + 1] - csr_ptr[r]; };
+      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return nz(a) > nz(b); });
+      // min-heap of (load, warp); warps with full slots leave the heap
+      std::vector<std::pair<int64_t, int32_t>> heap;
+      heap.reserve(nw);
+      for (int32_t w = 0; w < nw; ++w) heap.push_back({0, w});
+      std::vector<int32_t> fill(nw, 0);
+      std::vector<std::vector<int32_t>> rows(nw);
+      auto cmp = [](const std::pair<int64_t, int32_t>& a, const std::pair<int64_t, int32_t>& b) { return a > b; };
+      for (int32_t r : order) {
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        auto [load, w] = heap.back();
+        heap.pop_back();
+        rows[w].push_back(r);
+        if (++fill[w] < g.rw) {
+          heap.push_back({load + nz(r) + 1, w});
+          std::push_heap(heap.begin(), heap.end(), cmp);
+        }
+      }
+      for (int32_t w = 0; w < nw; ++w) {
+        std::sort(rows[w].begin(), rows[w].end(), [&](int32_t a, int32_t b) { return pos[a] < pos[b]; });
+        for (size_t i = 0; i < rows[w].size(); ++i) ro[size_t(w) * g.rw + i] = rows[w][i];
+      }
       return ro;
     };
     // K chunk (split-K tiling along the reduction dimension): the largest KC whose stage
@@ -319,7 +354,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     {
       std::vector<Geometry> cands;
       if (o.kernel != 2) cands.push_back(make_geo(1, 0));
-      if (o.kernel != 1)
+      if (o.kernel == 2)
         for (int32_t sb : {1, 2, 4})
           if (!o.group_sb || o.group_sb == sb) cands.push_back(make_geo(2, sb));
       double best = 0;

@@ -126,10 +126,22 @@ def test_packing_invariants(oracle_mod, key, opts):
     info, row_orig, triples = decode(p, plan)
     # every nonzero appears exactly once with its original row, column and value
     assert sorted(triples) == csr_triples(p)
-    # panels tile the permuted rows: row_orig = perm followed by empty slots
     perm = sdnn.permutation(p.row_ptr, p.col_idx, p.M, p.K) if opts.get("permute", True) else np.arange(p.M)
-    np.testing.assert_array_equal(row_orig[:p.M], perm)
-    assert np.all(row_orig[p.M:] == -1)
+    if info["kernel"] == 2:
+        # group kernel: panels tile the Algorithm 1 order, then empty slots
+        np.testing.assert_array_equal(row_orig[:p.M], perm)
+        assert np.all(row_orig[p.M:] == -1)
+    else:
+        # row kernel: every row in exactly one slot; rows of a warp keep their Algorithm 1 order
+        assert sorted(row_orig[row_orig >= 0].tolist()) == list(range(p.M))
+        pos = np.empty(p.M, int); pos[perm] = np.arange(p.M)
+        for w in range(info["num_panels"]):
+            rs = [r for r in row_orig[w * info["panel_rows"]:(w + 1) * info["panel_rows"]] if r >= 0]
+            assert list(pos[rs]) == sorted(pos[rs])
+        # LPT balance: max warp load <= mean load + heaviest row
+        loads = [sum(int(np.diff(p.row_ptr)[r]) for r in row_orig[w * info["panel_rows"]:(w + 1) * info["panel_rows"]] if r >= 0)
+                 for w in range(info["num_panels"])]
+        assert max(loads) <= p.nnz / info["num_panels"] + np.diff(p.row_ptr).max() + info["panel_rows"]
     assert info["num_row_blocks"] * info["panel_rows"] * info["cta_panels"] >= p.M
     cnt = np.diff(p.row_ptr)
     assert info["max_panel_nnz"] >= cnt.max()
@@ -143,7 +155,7 @@ def test_auto_kernel_choice_and_alg1_benefit():
         a = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="group").info()
         b = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="group", permute=False).info()
         assert a["group_entries_per_nnz_x1000"] < b["group_entries_per_nnz_x1000"], key
-        assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).info()["kernel"] in (1, 2)
+        assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).info()["kernel"] == 1
 
 
 def test_degenerate_shapes():
