@@ -332,8 +332,10 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
                    "M": p.M, "K": p.K, "nnz": p.nnz, "N_total": N_job, "N_per_gpu": Nr,
                    "parallelism": f"column-sharded x{world}, W replicated, no data-path collective",
                    "l2": "inputs larger than L2 (X shard %.0f MiB > 126 MB L2); no flush" % (p.K * Nr * 4 / 2**20),
-                   "kernel": f"{KERNEL}<{'group' if info['kernel'] == 2 else 'row'},R_w={info['panel_rows']},"
-                             f"V={'8' if info['num_row_blocks'] * ((Nr + 255) // 256) >= 296 else '4'}>",
+                   "kernel": (f"sdnn_cg_p<0..{info['num_panels'] - 1}> (generated, {info['panel_rows']} rows/panel)"
+                              if info["kernel"] == 3 else
+                              f"{KERNEL}<{'group' if info['kernel'] == 2 else 'row'},R_w={info['panel_rows']},"
+                              f"V={'8' if info['num_row_blocks'] * ((Nr + 255) // 256) >= 296 else '4'}>"),
                    "group_entries_per_nnz": info["group_entries_per_nnz_x1000"] / 1000, "group_sb": info["group_sb"],
                    "panel_rows": info["panel_rows"], "cta_panels": info["cta_panels"], "k_chunk": info["k_chunk"],
                    "permuted": bool(info["permuted"]), "prep_ms": round(prep_ms, 1), "plan_hash_identical": same},
@@ -369,7 +371,7 @@ def main(argv=None):
     ap.add_argument("--n-total", type=int, default=synth.CONFIGS[WORKLOAD][2])
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--allgather", action="store_true")
-    ap.add_argument("--kernel", choices=["auto", "row", "group"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "row", "group", "codegen"], default="auto")
     ap.add_argument("--group-sb", type=int, default=0, choices=[0, 1, 2, 4])
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -58,7 +58,9 @@ typedef struct {
   int32_t permute;          /* 1 (default): Algorithm 1 greedy row reorder; 0: identity   */
   int32_t kernel;           /* 0 = auto (cost model), 1 = row kernel (each nonzero reads its X row
                                slice from shared memory), 2 = group kernel (16-row groups: one X
-                               load feeds every nonzero of the group in that column)               */
+                               load feeds every nonzero of the group in that column), 3 = codegen
+                               (per-panel generated PTX with the weights as FFMA immediates,
+                               JIT-compiled during sdnn_prepare)                        */
   int32_t panel_rows_max;   /* row kernel: rows per warp panel, 0 = auto, else 4 or 8 (group: 16)   */
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
@@ -156,6 +158,12 @@ SDNN_API sdnn_status sdnn_plan_create(const int32_t* csr_ptr, const int32_t* col
 SDNN_API sdnn_status sdnn_plan_get_info(sdnn_plan p, sdnn_info* info);
 SDNN_API sdnn_status sdnn_plan_export(sdnn_plan p, int32_t* row_orig, int64_t* blk_off, uint8_t* meta);
 SDNN_API sdnn_status sdnn_plan_destroy(sdnn_plan p);
+
+/* sdnn_plan_codegen_ptx: the generated PTX of codegen panel `panel` of a plan created with
+ * kernel = 3 (the same CSR must be passed again; HOST pointers).  If `out` is NULL only *len (bytes
+ * incl. the terminating NUL) is returned; else `out` must hold *len bytes.  For inspection/tests. */
+SDNN_API sdnn_status sdnn_plan_codegen_ptx(sdnn_plan p, const int32_t* csr_ptr, const int32_t* col_idx,
+                                           const float* vals, int32_t panel, char* out, int64_t* len);
 
 /* ------------------------------------------------------------------ errors / version */
 SDNN_API const char* sdnn_status_string(sdnn_status s);

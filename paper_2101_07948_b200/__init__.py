@@ -27,7 +27,7 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
 EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_host", "sdnn_get_permutation", "sdnn_get_info",
            "sdnn_permutation", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_destroy",
-           "sdnn_status_string", "sdnn_last_error_message", "sdnn_abi_version"]
+           "sdnn_plan_codegen_ptx", "sdnn_status_string", "sdnn_last_error_message", "sdnn_abi_version"]
 
 
 class SdnnError(RuntimeError):
@@ -70,6 +70,7 @@ _lib.sdnn_plan_create.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(Perm
 _lib.sdnn_plan_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_plan_export.argtypes = [_vp, _vp, _vp, _vp]
 _lib.sdnn_plan_destroy.argtypes = [_vp]
+_lib.sdnn_plan_codegen_ptx.argtypes = [_vp, _vp, _vp, _vp, _i32, _vp, ctypes.POINTER(_i64)]
 _lib.sdnn_status_string.restype = ctypes.c_char_p
 _lib.sdnn_last_error_message.restype = ctypes.c_char_p
 _lib.sdnn_abi_version.restype = ctypes.c_int32
@@ -94,7 +95,7 @@ def _csr(row_ptr, col_idx, vals):
     return rp, ci, v
 
 
-KERNELS = {"auto": 0, "row": 1, "group": 2}
+KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3}
 
 
 def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0):
@@ -133,6 +134,17 @@ class Plan:
         i.struct_size = ctypes.sizeof(Info)
         _check(_lib.sdnn_plan_get_info(self._h, ctypes.byref(i)), "sdnn_plan_get_info")
         return i.as_dict()
+
+    def codegen_ptx(self, row_ptr, col_idx, vals, panel: int) -> str:
+        """Generated PTX of one codegen panel (plan created with kernel="codegen")."""
+        rp, ci, v = _csr(row_ptr, col_idx, vals)
+        n = _i64(0)
+        _check(_lib.sdnn_plan_codegen_ptx(self._h, _np_ptr(rp), _np_ptr(ci), _np_ptr(v), panel, None, ctypes.byref(n)),
+               "sdnn_plan_codegen_ptx")
+        buf = ctypes.create_string_buffer(n.value)
+        _check(_lib.sdnn_plan_codegen_ptx(self._h, _np_ptr(rp), _np_ptr(ci), _np_ptr(v), panel, buf, ctypes.byref(n)),
+               "sdnn_plan_codegen_ptx")
+        return buf.value.decode()
 
     def export(self):
         i = self.info()

@@ -35,11 +35,37 @@ struct Plan {
   std::vector<int32_t> row_orig;
   std::vector<int64_t> blk_off;
   std::vector<uint8_t> meta;
+  // codegen kernel (kernel == 3): row panels (original row ids, Algorithm 1 order) baked into code
+  std::vector<std::vector<int32_t>> cg_panels;
+  int32_t cg_warps = 0, cg_prefetch = 0;
 };
 
 sdnn_status validate_csr(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K);
 // Algorithm 1 with an inverted index; order must hold M entries.
 void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K, int32_t* order);
+std::string codegen_panel_ptx(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals,
+                              const std::vector<int32_t>& rows, int32_t K, int32_t warps, int32_t D,
+                              const std::string& name);
+}  // namespace sdnn
+#include <cuda.h>
+namespace sdnn {
+// Driver-API entry points, resolved at run time through cudaGetDriverEntryPoint so that libsdnn
+// does not link libcuda (the CPU-only container has none; tests load the library there).
+struct DriverApi {
+  CUresult (*moduleLoadDataEx)(CUmodule*, const void*, unsigned, CUjit_option*, void**) = nullptr;
+  CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*moduleUnload)(CUmodule) = nullptr;
+  CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                           void**, void**) = nullptr;
+  CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*ctxGetCurrent)(CUcontext*) = nullptr;
+  CUresult (*ctxSetCurrent)(CUcontext) = nullptr;
+  bool ok = false;
+};
+const DriverApi& driver();
+sdnn_status codegen_build(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t K,
+                          const std::vector<std::vector<int32_t>>& panels, int32_t warps, int32_t D,
+                          std::vector<CUmodule>& mods, std::vector<CUfunction>& funcs, int32_t threads);
 sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
                        const sdnn_perm_opts* opts, Plan& plan);
 
@@ -47,6 +73,9 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
 constexpr int kSmemBudget = 220 * 1024;
 constexpr int kMaxTN = 256;  // widest N tile (V = 8 floats per lane)
 constexpr int kMaxGroupWarps = 11;  // group kernel: consumer warps per CTA (register budget)
+constexpr int kCgMaxRows = 128;     // codegen kernel: accumulators (rows) per panel
+constexpr int kCgWarps = 6;         // codegen kernel: warps per CTA (2 CTAs/SM at <= 168 registers)
+constexpr int kCgPrefetch = 24;     // codegen kernel: X columns in flight per lane
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 

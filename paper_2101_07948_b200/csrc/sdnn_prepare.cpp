@@ -228,10 +228,14 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     o = *opts;
     if (o.flags != 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.flags must be 0");
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
-    if (o.kernel < 0 || o.kernel > 2) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0, 1 or 2");
-    if (o.panel_rows_max != 0 && o.panel_rows_max != 4 && o.panel_rows_max != 8 &&
-        !(o.panel_rows_max == 16 && o.kernel == 2))
+    if (o.kernel < 0 || o.kernel > 3) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0, 1, 2 or 3");
+    if (o.kernel == 3) {
+      if (o.panel_rows_max < 0 || o.panel_rows_max > kCgMaxRows)
+        return fail(SDNN_ERR_INVALID_ARGUMENT, "panel_rows_max must be 0..128 with the codegen kernel");
+    } else if (o.panel_rows_max != 0 && o.panel_rows_max != 4 && o.panel_rows_max != 8 &&
+               !(o.panel_rows_max == 16 && o.kernel == 2)) {
       return fail(SDNN_ERR_INVALID_ARGUMENT, "panel_rows_max must be 0, 4 or 8 (16 with the group kernel)");
+    }
     if (o.cta_panels < 0 || o.cta_panels > 16) return fail(SDNN_ERR_INVALID_ARGUMENT, "cta_panels must be 0..16");
     if (o.kernel == 2 && o.cta_panels > kMaxGroupWarps)
       return fail(SDNN_ERR_INVALID_ARGUMENT, "cta_panels must be <= 11 with the group kernel");
@@ -256,6 +260,44 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       algorithm1(csr_ptr, col_idx, M, K, plan.perm.data());
     else
       for (int32_t i = 0; i < M; ++i) plan.perm[i] = i;
+
+    if (o.kernel == 3) {
+      // Codegen kernel (sdnn_codegen.cpp): consecutive rows of the Algorithm 1 order form a panel,
+      // so rows with similar patterns share one X load per union column.  Panel count P:
+      // the smallest divisor of the CTA slots (2 per SM on 148 SMs = 296) with ceil(M / P) <= 128,
+      // so every panel gets the same number of persistent CTAs and all panels sweep N in lockstep.
+      const int32_t rmax = o.panel_rows_max ? o.panel_rows_max : kCgMaxRows;
+      const int32_t need = (M + rmax - 1) / rmax;
+      const int32_t slots = 296;
+      int32_t P = need;
+      for (int32_t d = need; d <= slots; ++d)
+        if (slots % d == 0) { P = d; break; }
+      if (P > M) P = M;
+      plan.kernel = 3;
+      plan.cg_warps = kCgWarps;
+      plan.cg_prefetch = kCgPrefetch;
+      plan.cg_panels.assign(P, {});
+      const int32_t rows_per = (M + P - 1) / P;
+      for (int32_t i = 0; i < M; ++i) plan.cg_panels[i / rows_per].push_back(plan.perm[i]);
+      while (!plan.cg_panels.empty() && plan.cg_panels.back().empty()) plan.cg_panels.pop_back();
+      plan.panel_rows = rows_per;
+      plan.cta_panels = 1;
+      plan.num_panels = int32_t(plan.cg_panels.size());
+      plan.num_row_blocks = plan.num_panels;
+      plan.row_orig.assign(size_t(plan.num_panels) * rows_per, -1);
+      for (int32_t pn = 0; pn < plan.num_panels; ++pn) {
+        int64_t s = 0;
+        for (size_t r = 0; r < plan.cg_panels[pn].size(); ++r) {
+          plan.row_orig[size_t(pn) * rows_per + r] = plan.cg_panels[pn][r];
+          s += csr_ptr[plan.cg_panels[pn][r] + 1] - csr_ptr[plan.cg_panels[pn][r]];
+        }
+        plan.max_panel_nnz = std::max(plan.max_panel_nnz, s);
+      }
+      plan.k_chunk = K;
+      plan.num_chunks = 1;
+      plan.blk_off.assign(size_t(plan.num_row_blocks) + 1, 0);
+      return SDNN_OK;
+    }
 
     // Candidate geometries: the row kernel (R_w rows per warp) and the group kernel (16 rows per
     // warp).  Launch geometry: W_c warps per CTA, enough row blocks to fill
@@ -493,6 +535,26 @@ sdnn_status sdnn_plan_export(sdnn_plan p, int32_t* row_orig, int64_t* blk_off, u
   if (row_orig) std::memcpy(row_orig, pl.row_orig.data(), pl.row_orig.size() * 4);
   if (blk_off) std::memcpy(blk_off, pl.blk_off.data(), pl.blk_off.size() * 8);
   if (meta && !pl.meta.empty()) std::memcpy(meta, pl.meta.data(), pl.meta.size());
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_plan_codegen_ptx(sdnn_plan p, const int32_t* csr_ptr, const int32_t* col_idx, const float* vals,
+                                  int32_t panel, char* out, int64_t* len) {
+  if (!p || !len || !csr_ptr) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL plan, csr_ptr or len");
+  const Plan& pl = p->plan;
+  if (pl.kernel != 3) return fail(SDNN_ERR_INVALID_ARGUMENT, "plan was not created with kernel = 3");
+  if (panel < 0 || panel >= int32_t(pl.cg_panels.size())) return fail(SDNN_ERR_INVALID_ARGUMENT, "panel out of range");
+  try {
+    const std::string ptx = codegen_panel_ptx(csr_ptr, col_idx, vals, pl.cg_panels[panel], pl.K, pl.cg_warps,
+                                              pl.cg_prefetch, "sdnn_cg_p" + std::to_string(panel));
+    if (out) {
+      if (*len < int64_t(ptx.size()) + 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "buffer too small");
+      std::memcpy(out, ptx.c_str(), ptx.size() + 1);
+    }
+    *len = int64_t(ptx.size()) + 1;
+  } catch (const std::bad_alloc&) {
+    return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
+  }
   return SDNN_OK;
 }
 

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <string>
 #include <vector>
@@ -35,6 +36,14 @@ struct sdnn_handle_s {
   uint8_t* d_meta = nullptr;
   int64_t* d_blk_off = nullptr;
   int32_t* d_row_orig = nullptr;
+  // codegen kernel: one JIT module per panel, one stream per panel (all panels run concurrently)
+  std::vector<CUmodule> cg_mods;
+  std::vector<CUfunction> cg_funcs;
+  std::vector<cudaStream_t> cg_streams;
+  std::vector<cudaEvent_t> cg_join;
+  cudaEvent_t cg_fork = nullptr;
+  int32_t cg_ctas = 1;  // persistent CTAs per panel kernel
+  std::mutex cg_mu;     // the per-panel streams are shared by concurrent calls on one handle
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -335,9 +344,38 @@ static cudaError_t set_smem_attrs() {
                               kSmemBudget + 1024);
 }
 
-static sdnn_status launch(const sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
+static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                                  float* Y, cudaStream_t stream) {
+  const Plan& pl = h->plan;
+  if (N >= (int64_t(1) << 30)) return fail(SDNN_ERR_UNSUPPORTED, "codegen kernel needs N < 2^30");
+  const int32_t tile = 32 * pl.cg_warps;
+  uint32_t ntiles = uint32_t((N + tile - 1) / tile);
+  uint64_t px = reinterpret_cast<uint64_t>(X), py = reinterpret_cast<uint64_t>(Y),
+           pb = reinterpret_cast<uint64_t>(bias);
+  uint32_t ld4 = uint32_t(N * 4), n32 = uint32_t(N), a32 = uint32_t(act);
+  void* args[] = {&px, &py, &pb, &ld4, &ld4, &n32, &a32, &ntiles};
+  const unsigned grid = unsigned(std::min<int64_t>(h->cg_ctas, ntiles));
+  std::lock_guard<std::mutex> lk(h->cg_mu);
+  SDNN_CUDA_TRY(cudaEventRecord(h->cg_fork, stream));
+  for (size_t p = 0; p < h->cg_funcs.size(); ++p) {
+    SDNN_CUDA_TRY(cudaStreamWaitEvent(h->cg_streams[p], h->cg_fork, 0));
+    CUresult r = driver().launchKernel(h->cg_funcs[p], grid, 1, 1, unsigned(tile), 1, 1, 0,
+                                       reinterpret_cast<CUstream>(h->cg_streams[p]), args, nullptr);
+    if (r != CUDA_SUCCESS) {
+      const char* es = nullptr;
+      driver().getErrorString(r, &es);
+      return fail(SDNN_ERR_CUDA, std::string("codegen launch: ") + (es ? es : "?"));
+    }
+    SDNN_CUDA_TRY(cudaEventRecord(h->cg_join[p], h->cg_streams[p]));
+    SDNN_CUDA_TRY(cudaStreamWaitEvent(stream, h->cg_join[p], 0));
+  }
+  return SDNN_OK;
+}
+
+static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
                           cudaStream_t stream) {
   const Plan& pl = h->plan;
+  if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, Y, stream);
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
   int V = 8;
@@ -489,6 +527,31 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
   if (e != cudaSuccess) return cleanup(SDNN_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
   pl.meta_size_uploaded = int64_t(pl.meta.size());
   std::vector<uint8_t>().swap(pl.meta);
+  if (pl.kernel == 3) {
+    cudaFree(0);  // make the runtime's primary context current for the driver API
+    const int32_t threads = int32_t(std::max(1u, std::thread::hardware_concurrency()));
+    sdnn_status cs = codegen_build(csr_ptr, col_idx, vals, K, pl.cg_panels, pl.cg_warps, pl.cg_prefetch, h->cg_mods,
+                                   h->cg_funcs, threads);
+    if (cs != SDNN_OK) {
+      std::string m = sdnn_last_error_message();
+      sdnn_destroy(h);
+      return fail(cs, m);
+    }
+    const int32_t P = int32_t(pl.cg_panels.size());
+    const int32_t slots = prop.multiProcessorCount * (pl.cg_warps * 32 <= 192 ? 2 : 1);
+    h->cg_ctas = std::max(1, slots / P);
+    h->cg_streams.assign(size_t(P), nullptr);
+    h->cg_join.assign(size_t(P), nullptr);
+    cudaError_t ce = cudaEventCreateWithFlags(&h->cg_fork, cudaEventDisableTiming);
+    for (int32_t p = 0; p < P && ce == cudaSuccess; ++p) {
+      ce = cudaStreamCreateWithFlags(&h->cg_streams[p], cudaStreamNonBlocking);
+      if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->cg_join[p], cudaEventDisableTiming);
+    }
+    if (ce != cudaSuccess) {
+      sdnn_destroy(h);
+      return fail(SDNN_ERR_CUDA, std::string("codegen streams: ") + cudaGetErrorString(ce));
+    }
+  }
   *out = h;
   return SDNN_OK;
 }
@@ -501,6 +564,13 @@ sdnn_status sdnn_destroy(sdnn_handle h) {
   cudaFree(h->d_meta);
   cudaFree(h->d_blk_off);
   cudaFree(h->d_row_orig);
+  for (cudaStream_t st : h->cg_streams)
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : h->cg_join)
+    if (ev) cudaEventDestroy(ev);
+  if (h->cg_fork) cudaEventDestroy(h->cg_fork);
+  for (CUmodule m : h->cg_mods)
+    if (m) driver().moduleUnload(m);
   if (cur != h->device && cur >= 0) cudaSetDevice(cur);
   delete h;
   return SDNN_OK;

@@ -60,7 +60,7 @@ def test_worked_example(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ BASELINE configs c1-c4 (full size)
-@pytest.mark.parametrize("kernel", ["auto", "row", "group1", "group2", "group4"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "group1", "group2", "group4", "codegen"])
 @pytest.mark.parametrize("key", [k for k in synth.CONFIGS if k != "c5"])
 def test_config_parity(sdnn, oracle_mod, key, kernel):
     p = synth.config_problem(key)
@@ -75,7 +75,7 @@ def test_c2_no_act(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ desk grid
-@pytest.mark.parametrize("kernel", ["row", "group"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
 @pytest.mark.parametrize("g", list(synth.desk_grid()), ids=lambda g: f"{g['name']}_s{g['seed']}")
 def test_desk_grid(sdnn, oracle_mod, g, kernel):
     p = synth.make_problem(g["name"], g["M"], g["K"], g["N"], g["sparsity"], seed=g["seed"])
@@ -83,7 +83,7 @@ def test_desk_grid(sdnn, oracle_mod, g, kernel):
 
 
 # ------------------------------------------------------------------ c5 at full size, launch config of bench.py
-@pytest.mark.parametrize("kernel", ["auto", "row"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "codegen"])
 def test_c5_full_size_sampled_columns(sdnn, oracle_mod, kernel):
     p = synth.config_problem("c5")
     h = sdnn.Handle.from_problem(p, kernel=kernel)
@@ -103,14 +103,14 @@ def test_c5_full_size_sampled_columns(sdnn, oracle_mod, kernel):
 
 
 # ------------------------------------------------------------------ edge cases
-@pytest.mark.parametrize("kernel", ["row", "group"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
 @pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 127, 129, 300, 1000])
 def test_ragged_n(sdnn, oracle_mod, N, kernel):
     p = synth.make_problem("ragged", 200, 150, N, 0.9, mask="lognormal", seed=N)
     check(sdnn, oracle_mod, p, kernel=kernel)
 
 
-@pytest.mark.parametrize("kernel", ["row", "group"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
 def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     p = synth.make_problem("unal", 100, 90, 64, 0.8, seed=1)
     X = p.x()
@@ -125,7 +125,7 @@ def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     assert_parity(Yv.cpu().numpy(), Yo, S, "unaligned")
 
 
-@pytest.mark.parametrize("kernel", ["row", "group"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
 @pytest.mark.parametrize("M,K,N,dens", [(1, 1, 4, 1.0), (1, 500, 8, 0.3), (500, 1, 8, 0.5), (37, 65, 12, 1.0),
                                         (129, 257, 20, 0.0), (64, 64, 64, 1.0), (2100, 70, 40, 0.05)])
 def test_degenerate_shapes(sdnn, oracle_mod, M, K, N, dens, kernel):
@@ -166,7 +166,8 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
     for opts in [dict(permute=False), dict(panel_rows=8), dict(cta_panels=1), dict(k_chunk=8),
                  dict(k_chunk=96, panel_rows=4, cta_panels=2), dict(kernel="group"), dict(kernel="row"),
                  dict(kernel="group", permute=False), dict(kernel="group", cta_panels=3, k_chunk=16),
-                 dict(kernel="group", group_sb=1), dict(kernel="group", group_sb=2), dict(kernel="group", group_sb=4)]:
+                 dict(kernel="group", group_sb=1), dict(kernel="group", group_sb=2), dict(kernel="group", group_sb=4),
+                 dict(kernel="codegen"), dict(kernel="codegen", permute=False), dict(kernel="codegen", panel_rows=7)]:
         Y, _ = run_gpu(sdnn, p, X, p.bias, 1, **opts)
         np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
 
@@ -192,19 +193,21 @@ def test_repeat_bitwise_and_linearity(sdnn):
     np.testing.assert_array_equal(Y3, 2 * Y1)
 
 
-def test_host_entry_point_matches_device(sdnn):
+@pytest.mark.parametrize("kernel", ["row", "codegen"])
+def test_host_entry_point_matches_device(sdnn, kernel):
     p = synth.config_problem("c3_256x128")
     X = p.x()
-    h = sdnn.Handle.from_problem(p)
+    h = sdnn.Handle.from_problem(p, kernel=kernel)
     ref, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
     for bc in (0, 512, 1000, 4):
         Y = h.spmm_host(X, p.bias, act=1, block_cols=bc)
         np.testing.assert_array_equal(Y, ref)
 
 
-def test_cuda_graph_capture(sdnn):
+@pytest.mark.parametrize("kernel", ["row", "codegen"])
+def test_cuda_graph_capture(sdnn, kernel):
     p = synth.config_problem("c3_512x512")
-    h = sdnn.Handle.from_problem(p)
+    h = sdnn.Handle.from_problem(p, kernel=kernel)
     X = torch.from_numpy(p.x()).cuda()
     b = torch.from_numpy(p.bias).cuda()
     Y = torch.empty((p.M, p.N), device="cuda")

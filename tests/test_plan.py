@@ -179,3 +179,29 @@ def test_plan_deterministic():
     b = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K).export()
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+def test_codegen_plan_and_ptx(tmp_path):
+    """Codegen plan: panels partition the Algorithm 1 order; the generated PTX has one FFMA with an
+    immediate weight per nonzero of the panel (P:139 registers named by position) and assembles."""
+    import shutil
+    import subprocess
+    p = synth.config_problem("c3_512x512", N=4)
+    plan = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="codegen")
+    info = plan.info()
+    row_orig, _, _ = plan.export()
+    perm = sdnn.permutation(p.row_ptr, p.col_idx, p.M, p.K)
+    np.testing.assert_array_equal(row_orig[row_orig >= 0], perm)
+    assert info["kernel"] == 3 and info["panel_rows"] <= 128 and 296 % info["num_panels"] == 0
+    ptx = plan.codegen_ptx(p.row_ptr, p.col_idx, p.vals, 0)
+    rows0 = [r for r in row_orig[:info["panel_rows"]] if r >= 0]
+    nnz0 = int(sum(np.diff(p.row_ptr)[rows0]))
+    assert ptx.count("fma.rn.f32 ") == nnz0
+    import struct
+    w = struct.unpack("<I", struct.pack("<f", p.vals[p.row_ptr[rows0[0]]]))[0]
+    assert f"0f{w:08X}" in ptx
+    ptxas = shutil.which("ptxas") or "/usr/local/cuda/bin/ptxas"
+    f = tmp_path / "p0.ptx"
+    f.write_text(ptx)
+    r = subprocess.run([ptxas, "-arch=sm_100a", "-O1", str(f), "-o", str(tmp_path / "p0.cubin")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -14,6 +14,7 @@
 __constant__ float c_w[64];
 
 constexpr int ITERS = 4096;
+constexpr int BIG_N = 16384;
 
 __global__ void k_ffma_reg(float* out, float w0, float w1, long long* clk) {
   float a[16];
@@ -116,6 +117,45 @@ __global__ void k_ffma2(float* out, float w0, float w1, long long* clk) {
   if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
 }
 
+__global__ void k_ffma2_imm(float* out, float w0, long long* clk) {
+  unsigned long long a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (unsigned long long)(threadIdx.x + i);
+  unsigned long long x = __double_as_longlong((double)w0 + threadIdx.x);
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("{.reg .b64 w; mov.b64 w, 0x3F9E06523F9E0652; fma.rn.f32x2 %0, w, %1, %0;}" : "+l"(a[i]) : "l"(x));
+  }
+  long long t1 = clock64();
+  unsigned long long s = 0; for (int i = 0; i < 8; ++i) s ^= a[i];
+  if (s == 12345) out[0] = 1.f;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
+// straight-line code far larger than the I-cache: every FMA distinct (immediates), 8 accumulators
+template <int FORM>
+__global__ void k_bigcode(float* out, float w0, long long* clk) {
+  unsigned long long a[8];
+  float f[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { a[i] = (unsigned long long)(threadIdx.x + i); f[i] = threadIdx.x * 1e-3f + i; }
+  unsigned long long x = __double_as_longlong((double)w0 + threadIdx.x);
+  float xf = w0 + threadIdx.x;
+  long long t0 = clock64();
+if (FORM == 2) {
+#include "bigcode2.inc"
+  } else {
+#include "bigcode1.inc"
+  }
+
+  long long t1 = clock64();
+  unsigned long long s = 0; for (int i = 0; i < 8; ++i) s ^= a[i] ^ __float_as_uint(f[i]);
+  if (s == 12345) out[0] = 1.f;
+  if (threadIdx.x == 0 && blockIdx.x == 0) clk[0] = t1 - t0;
+}
+
 __global__ void k_lds128(float* out, long long* clk) {
   __shared__ float4 buf[2048];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_float4(i, i + 1, i + 2, i + 3);
@@ -197,7 +237,7 @@ int main() {
            name, ms, rate / 1e9, per_sm_clk, sec_clk / 1e6, bytes_per_thread > 0 ? "smem " : "",
            bytes_per_thread > 0 ? bytes_per_thread * blocks * threads / (ms * 1e-3) / 1e9 : 0.0);
   };
-  for (int occ : {1, 2, 4}) {
+  for (int occ : {1, 2, 3, 4}) {
     int blocks = SM * occ, threads = 256;
     printf("--- %d blocks x %d threads\n", blocks, threads);
     report("ffma_reg (fma/thr)", [&] { k_ffma_reg<<<blocks, threads>>>(out, 1.f, 0.5f, clk); }, 16.0 * ITERS, blocks, threads, 0);
@@ -205,6 +245,9 @@ int main() {
     report("ffma_imm_distinct", [&] { k_ffma_imm_distinct<<<blocks, threads>>>(out, 1.f, clk); }, 16.0 * ITERS, blocks, threads, 0);
     report("ffma_const", [&] { k_ffma_const<<<blocks, threads>>>(out, 1.f, clk); }, 16.0 * ITERS, blocks, threads, 0);
     report("ffma2 (fma/thr)", [&] { k_ffma2<<<blocks, threads>>>(out, 1.f, 0.5f, clk); }, 16.0 * ITERS, blocks, threads, 0);
+    report("ffma2_imm (fma/thr)", [&] { k_ffma2_imm<<<blocks, threads>>>(out, 1.f, clk); }, 16.0 * ITERS, blocks, threads, 0);
+    report("bigcode ffma_imm", [&] { k_bigcode<1><<<blocks, threads>>>(out, 1.f, clk); }, 1.0 * BIG_N, blocks, threads, 0);
+    report("bigcode ffma2_imm", [&] { k_bigcode<2><<<blocks, threads>>>(out, 1.f, clk); }, 2.0 * BIG_N, blocks, threads, 0);
     report("lds128 (B/thr)", [&] { k_lds128<<<blocks, threads>>>(out, clk); }, 8.0 * ITERS * 16, blocks, threads, 8.0 * ITERS * 16);
     report("rho1 R4 (fma/thr)", [&] { k_rho1<4><<<blocks, threads>>>(out, clk); }, 4.0 * 8 * 4 * (ITERS / 4), blocks, threads, 0);
     report("rho1 R8 (fma/thr)", [&] { k_rho1<8><<<blocks, threads>>>(out, clk); }, 8.0 * 8 * 4 * (ITERS / 4), blocks, threads, 0);
