@@ -1,5 +1,5 @@
 // Runs a proto_codegen5 cubin: X (K×N) via a TMA tensor map with {64 × KC} boxes.
-// usage: run_cg5 file.cubin nnz_per_panel N W KC S
+// usage: run_cg5 file.cubin nnz_per_panel N W KC S R
 #include <cstdio>
 #include <cstdlib>
 #include <cuda.h>
@@ -12,7 +12,7 @@ int main(int argc, char** argv) {
   CKD(cuModuleLoad(&mod, argv[1]));
   CKD(cuModuleGetFunction(&f, mod, "cg"));
   double nnzp = atof(argv[2]); unsigned N = atoi(argv[3]); int W = atoi(argv[4]); int KC = atoi(argv[5]); int S = atoi(argv[6]);
-  const int K = 4096, R = 64;
+  const int K = 4096; const int R = argc > 7 ? atoi(argv[7]) : 64;
   float *X, *Y;
   cudaMalloc(&X, size_t(K) * N * 4); cudaMalloc(&Y, size_t(R) * N * 4);
   cudaMemset(X, 0, size_t(K) * N * 4);
