@@ -95,7 +95,7 @@ def _csr(row_ptr, col_idx, vals):
     return rp, ci, v
 
 
-KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3}
+KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4}
 
 
 def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0):

@@ -77,6 +77,16 @@ constexpr int kCgMaxRows = 128;     // codegen kernel: accumulators (rows) per p
 constexpr int kCgWarps = 6;         // codegen kernel: warps per CTA (2 CTAs/SM at <= 168 registers)
 constexpr int kCgPrefetch = 24;     // codegen kernel: X columns in flight per lane
 
+// TMEM kernel geometry: X tile lives in tensor memory, lane = 4 consecutive columns of N (128 lanes →
+// N tile 512), TMEM column = 4·k_local + v; two halves of 256 columns → K chunk 64; 16 consumer warps
+// = 4 warp slots per lane quarter, each slot a 16-row panel → 64 rows per CTA.
+constexpr int kTmemRows = 16;
+constexpr int kTmemPanels = 4;
+constexpr int kTmemKc = 64;
+constexpr int kTmemTN = 512;
+constexpr int kTmemPieceK = 16;   // K rows per TMA piece (16 × 512 × 4 B = 32 KB)
+constexpr int kTmemPieces = 4;    // smem ring depth (pieces)
+
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace sdnn

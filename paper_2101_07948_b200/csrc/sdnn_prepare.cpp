@@ -228,8 +228,11 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     o = *opts;
     if (o.flags != 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.flags must be 0");
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
-    if (o.kernel < 0 || o.kernel > 3) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0, 1, 2 or 3");
-    if (o.kernel == 3) {
+    if (o.kernel < 0 || o.kernel > 4) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..4");
+    if (o.kernel == 4) {
+      if (o.panel_rows_max != 0 || o.cta_panels != 0 || (o.k_chunk != 0 && o.k_chunk != kTmemKc) || o.group_sb != 0)
+        return fail(SDNN_ERR_INVALID_ARGUMENT, "the TMEM kernel has a fixed geometry (leave the tiling options 0)");
+    } else if (o.kernel == 3) {
       if (o.panel_rows_max < 0 || o.panel_rows_max > kCgMaxRows)
         return fail(SDNN_ERR_INVALID_ARGUMENT, "panel_rows_max must be 0..128 with the codegen kernel");
     } else if (o.panel_rows_max != 0 && o.panel_rows_max != 4 && o.panel_rows_max != 8 &&
@@ -304,6 +307,16 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     // the machine for the typical N.
     auto make_geo = [&](int32_t kernel, int32_t sb) {
       Geometry g{};
+      if (kernel == 4) {
+        // TMEM kernel (sdnn_spmm.cu): row-kernel format, 16-row warp panels, 4 panels per CTA row
+        // block (one per warp slot of a TMEM lane quarter), K chunk = one TMEM half (256 columns /
+        // 4 floats per lane) = 64.
+        g.kernel = 1;
+        g.rw = kTmemRows;
+        g.wc = kTmemPanels;
+        g.nrb = (M + g.rw * g.wc - 1) / (g.rw * g.wc);
+        return g;
+      }
       g.kernel = kernel;
       g.sb = sb;
       g.rw = kernel == 2 ? 16 : (o.panel_rows_max ? o.panel_rows_max : (M >= 2048 ? 8 : 4));
@@ -395,7 +408,12 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     EmitStats stats;
     {
       std::vector<Geometry> cands;
-      if (o.kernel != 2) cands.push_back(make_geo(1, 0));
+      if (o.kernel == 4) {
+        o.k_chunk = kTmemKc;
+        cands.push_back(make_geo(4, 0));
+      } else if (o.kernel != 2) {
+        cands.push_back(make_geo(1, 0));
+      }
       if (o.kernel == 2)
         for (int32_t sb : {1, 2, 4})
           if (!o.group_sb || o.group_sb == sb) cands.push_back(make_geo(2, sb));
@@ -410,7 +428,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       }
       if (!found) return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
     }
-    plan.kernel = g.kernel;
+    plan.kernel = o.kernel == 4 ? 4 : g.kernel;
     plan.panel_rows = g.rw;
     plan.cta_panels = g.wc;
     plan.num_row_blocks = g.nrb;

@@ -310,6 +310,234 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) 
 }
 
 // ------------------------------------------------------------------------------------------------
+// TMEM kernel (DESIGN.md §6 "TMEM kernel").  The row kernel reads one 4-byte X operand per FMA from
+// shared memory, and shared memory delivers 128 B/clk/SM — a 25 % ceiling on the FMA pipe.  Tensor
+// memory is read into registers by tcgen05.ld at up to ~357 B/clk/SM (.32x32b.x16) / ~200 B/clk/SM
+// (.x4) (tools/microbench/tmem_bw.cu, profiles/r01_tmem_bw.log), so here the X tile lives in TMEM
+// and the CUDA cores read their operands from there:
+//   * TMEM lane L (0..127) holds columns n0 + 4L .. 4L+3 of N; TMEM column 4·k + v holds
+//     X[k0 + k][n0 + 4L + v].  Two halves of 256 columns = two K chunks of 64 (double buffer).
+//   * a producer thread streams X[k0:k0+16, n0:n0+512] pieces (TMA, 3-D map so a K row of the tile
+//     is 2 KB contiguous) into a 4-slot shared-memory ring and moves each K row into TMEM with one
+//     tcgen05.cp.128x128b (lane L ← bytes 16L..16L+15 of the row); tcgen05.commit → mbarriers
+//     signal "slot reusable" and "chunk in TMEM";
+//   * consumer warp w reads TMEM lane quarter q = w % 4 (hardware rule: warp w%4 owns lanes
+//     32q..32q+31), i.e. N columns n0 + 128q + 4·lane + v, for the 16 rows of warp slot w / 4;
+//     per nonzero (col, w): tcgen05.ld.32x32b.x4 at TMEM column 4·col → 4 floats → 2 FFMA2;
+//   * metadata (row-kernel format, 64 rows per block) arrives by bulk copy; the epilogue is the
+//     row kernel's (bias, ReLU, store to the original row).
+// Every row still accumulates its nonzeros in ascending column order with fp32 FMA: results are
+// bitwise identical to the row kernel's.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float4& v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(taddr));
+}
+// Completes this thread's tcgen05.ld; the loaded registers pass through the asm so that no use of
+// them can be scheduled above the wait.
+__device__ __forceinline__ void tmem_wait_ld(float4& a) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+f"(a.x), "+f"(a.y), "+f"(a.z), "+f"(a.w) : : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld(float4& a, float4& b) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(a.x), "+f"(a.y), "+f"(a.z), "+f"(a.w), "+f"(b.x), "+f"(b.y), "+f"(b.z), "+f"(b.w)
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld(float4& a, float4& b, float4& c, float4& d) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(a.x), "+f"(a.y), "+f"(a.z), "+f"(a.w), "+f"(b.x), "+f"(b.y), "+f"(b.z), "+f"(b.w),
+                 "+f"(c.x), "+f"(c.y), "+f"(c.z), "+f"(c.w), "+f"(d.x), "+f"(d.y), "+f"(d.z), "+f"(d.w)
+               :
+               : "memory");
+}
+// acc[0..1] (4 columns of one row) += w · x
+__device__ __forceinline__ void fma4(float2 (&acc)[2], float w, const float4& x) {
+  const float2 w2 = make_float2(w, w);
+  acc[0] = __ffma2_rn(w2, make_float2(x.x, x.y), acc[0]);
+  acc[1] = __ffma2_rn(w2, make_float2(x.z, x.w), acc[1]);
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_cp_128x128b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
+// Shared-memory matrix descriptor (tcgen05): no swizzle, K-major canonical layout — 8-row × 16-byte
+// core matrices, 128 B apart along the 128 rows (SBO); one 16-byte column so LBO is unused.
+__device__ __forceinline__ uint64_t cp_desc(uint32_t saddr) {
+  return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(2048 >> 4) << 16) | (uint64_t(128 >> 4) << 32) |
+         (uint64_t(1) << 46);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kTmemConsumers = 4 * kTmemPanels;  // 16 consumer warps
+constexpr int kTmemPieceBytes = kTmemPieceK * kTmemTN * 4;
+constexpr int kTmemMetaSlots = 2;
+constexpr size_t tmem_smem_bytes(int m_stage_bytes) {
+  return size_t(kTmemPieces) * kTmemPieceBytes + size_t(kTmemMetaSlots) * m_stage_bytes + 16 * 8 + 16;
+}
+
+__global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
+    spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int RW = kTmemRows;
+  constexpr int PPC = kTmemKc / kTmemPieceK;  // pieces per K chunk
+  constexpr int S = kTmemPieces, MS = kTmemMetaSlots;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = blockIdx.x % p.nrb;
+  const int64_t n0 = int64_t(blockIdx.x / p.nrb) * kTmemTN;
+  uint8_t* xring = smem;
+  uint8_t* mring = smem + size_t(S) * kTmemPieceBytes;
+  uint64_t* slot_full = reinterpret_cast<uint64_t*>(mring + size_t(MS) * p.m_stage_bytes);
+  uint64_t* slot_empty = slot_full + S;
+  uint64_t* tfull = slot_empty + S;  // [2]: K chunk resident in TMEM half h
+  uint64_t* tfree = tfull + 2;       // [2]: every consumer warp is done with TMEM half h
+  uint64_t* mfull = tfree + 2;       // [MS]
+  uint64_t* mempty = mfull + MS;     // [MS]
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(mempty + MS);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&slot_full[s], 1);
+      mbar_init(&slot_empty[s], 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&tfull[h], 1);
+      mbar_init(&tfree[h], kTmemConsumers);
+    }
+    for (int m = 0; m < MS; ++m) {
+      mbar_init(&mfull[m], 1);
+      mbar_init(&mempty[m], kTmemConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tbase_s;
+
+  if (warp == kTmemConsumers) {  // producer: TMA → smem ring → tcgen05.cp → TMEM half
+    if (lane == 0) {
+      const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
+      const int total = p.nch * PPC;
+      const int32_t nb = int32_t(n0 / 128);
+      auto load_piece = [&](int i) {
+        const int s = i % S;
+        mbar_expect_tx(&slot_full[s], kTmemPieceBytes);
+        tma_load_3d(xring + size_t(s) * kTmemPieceBytes, &tmap, 0, nb, i * kTmemPieceK, &slot_full[s]);
+      };
+      auto load_meta = [&](int j) {
+        const int m = j % MS;
+        const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
+        mbar_expect_tx(&mfull[m], mbytes);
+        bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[j], mbytes, &mfull[m]);
+      };
+      for (int i = 0; i < S && i < total; ++i) load_piece(i);
+      for (int j = 0; j < MS && j < p.nch; ++j) load_meta(j);
+      for (int i = 0; i < total; ++i) {
+        const int s = i % S, j = i / PPC, h = j & 1, pc = i % PPC;
+        if (pc == 0 && j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
+          mbar_wait(&tfree[h], ((j >> 1) - 1) & 1);
+          tc_fence_after();
+          mbar_wait(&mempty[j % MS], ((j >> 1) - 1) & 1);
+          load_meta(j);
+        }
+        mbar_wait(&slot_full[s], (i / S) & 1);
+        const uint32_t src = smem_u32(xring + size_t(s) * kTmemPieceBytes);
+#pragma unroll
+        for (int kk = 0; kk < kTmemPieceK; ++kk)
+          tc_cp_128x128b(tbase + uint32_t(h * 256 + (pc * kTmemPieceK + kk) * 4), cp_desc(src + kk * kTmemTN * 4));
+        tc_commit(&slot_empty[s]);
+        if (pc == PPC - 1) tc_commit(&tfull[h]);
+        if (i + S < total) {
+          mbar_wait(&slot_empty[s], (i / S) & 1);
+          load_piece(i + S);
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3, wi = warp >> 2;
+    const uint32_t tl = tbase + (uint32_t(q * 32) << 16);
+    float2 acc[RW][2];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+    for (int j = 0; j < p.nch; ++j) {
+      const int h = j & 1, m = j % MS;
+      mbar_wait(&mfull[m], (j / MS) & 1);
+      mbar_wait(&tfull[h], (j >> 1) & 1);
+      tc_fence_after();
+      const uint8_t* ms = mring + size_t(m) * p.m_stage_bytes;
+      const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + wi * RW;
+      const float4* ent = reinterpret_cast<const float4*>(ms + p.hdr_bytes);
+      const uint32_t hb = tl + uint32_t(h * 256);
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        const uint32_t hh = hdr[r];
+        const int cnt = int(hh & 0xffffu);
+        const float4* e = ent + (hh >> 16) / 2;
+        int i = 0;
+        for (; i + 4 <= cnt; i += 4) {  // 4 nonzeros: 4 TMEM loads in flight, then 8 FFMA2
+          const float4 e0 = e[i >> 1], e1 = e[(i >> 1) + 1];
+          float4 xa, xb, xc, xd;
+          tmem_ld4(hb + (__float_as_uint(e0.x) << 2), xa);
+          tmem_ld4(hb + (__float_as_uint(e0.z) << 2), xb);
+          tmem_ld4(hb + (__float_as_uint(e1.x) << 2), xc);
+          tmem_ld4(hb + (__float_as_uint(e1.z) << 2), xd);
+          tmem_wait_ld(xa, xb, xc, xd);
+          fma4(acc[r], e0.y, xa);
+          fma4(acc[r], e0.w, xb);
+          fma4(acc[r], e1.y, xc);
+          fma4(acc[r], e1.w, xd);
+        }
+        if (i + 2 <= cnt) {
+          const float4 e0 = e[i >> 1];
+          float4 xa, xb;
+          tmem_ld4(hb + (__float_as_uint(e0.x) << 2), xa);
+          tmem_ld4(hb + (__float_as_uint(e0.z) << 2), xb);
+          tmem_wait_ld(xa, xb);
+          fma4(acc[r], e0.y, xa);
+          fma4(acc[r], e0.w, xb);
+          i += 2;
+        }
+        if (i < cnt) {
+          const float4 e0 = e[i >> 1];
+          float4 xa;
+          tmem_ld4(hb + (__float_as_uint(e0.x) << 2), xa);
+          tmem_wait_ld(xa);
+          fma4(acc[r], e0.y, xa);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&tfree[h]);
+        mbar_arrive(&mempty[m]);
+      }
+    }
+    epilogue<RW, 4, true>(acc, p, rb * kTmemPanels + wi, lane, n0 + q * 128);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+// ------------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------------
 #define SDNN_CUDA_TRY(call)                                                                            \
@@ -372,14 +600,60 @@ static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, c
   return SDNN_OK;
 }
 
+static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                               float* Y, cudaStream_t stream) {
+  const Plan& pl = h->plan;
+  const int64_t ntiles = (N + kTmemTN - 1) / kTmemTN;
+  const int64_t nblocks = ntiles * pl.num_row_blocks;
+  if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "N too large for one launch");
+  KParams p{};
+  p.meta = h->d_meta;
+  p.blk_off = h->d_blk_off;
+  p.row_orig = h->d_row_orig;
+  p.X = X;
+  p.bias = bias;
+  p.Y = Y;
+  p.N = N;
+  p.K = pl.K;
+  p.nch = pl.num_chunks;
+  p.kc = pl.k_chunk;
+  p.wc = pl.cta_panels;
+  p.nrb = pl.num_row_blocks;
+  p.m_stage_bytes = int32_t(align_up(pl.max_block_bytes, 128));
+  p.hdr_bytes = int32_t(align_up(int64_t(pl.panel_rows) * pl.cta_panels * 4, 16));
+  p.act = act;
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  // 3-D view of X: {128 columns, N/128 column blocks, K rows}, so one box {128, 4, 16} lands in
+  // shared memory as 16 contiguous 512-column K rows.
+  CUtensorMap tmap;
+  const cuuint64_t dims[3] = {128, cuuint64_t(N / 128), cuuint64_t(pl.K)};
+  const cuuint64_t strides[2] = {512, cuuint64_t(N) * 4};
+  const cuuint32_t box[3] = {128, kTmemTN / 128, kTmemPieceK};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(int(cr)));
+  const size_t smem = tmem_smem_bytes(p.m_stage_bytes);
+  if (smem > size_t(kSmemBudget) + 1024) return fail(SDNN_ERR_INTERNAL, "TMEM kernel stage does not fit shared memory");
+  spmm_tmem_kernel<<<unsigned(nblocks), (kTmemConsumers + 1) * 32, smem, stream>>>(tmap, p);
+  SDNN_CUDA_TRY(cudaGetLastError());
+  return SDNN_OK;
+}
+
 static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
                           cudaStream_t stream) {
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, Y, stream);
+  if (pl.kernel == 4 && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(Y) % 16 == 0)
+    return launch_tmem(h, X, N, bias, act, Y, stream);
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
   int V = 8;
   if (int64_t(pl.num_row_blocks) * ((N + 255) / 256) < 2 * 148) V = 4;
+  if (pl.kernel == 4) V = 4;  // TMEM plan on a ragged / unaligned call: generic kernel, 16-row panels
   const int TN = 32 * V;
   const int64_t ntiles = (N + TN - 1) / TN;
   const int64_t nblocks = ntiles * pl.num_row_blocks;
@@ -404,7 +678,7 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
   p.act = act;
 
   const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
-                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0) && pl.kernel != 4;
   if (fast) {
     int S = int(kSmemBudget / (p.x_stage_bytes + p.m_stage_bytes));
     S = std::min(S, std::min(pl.num_chunks, 4));
@@ -445,6 +719,7 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
     else if (pl.kernel == 2 && sb == 1) spmm_generic_kernel<2, 16, 4, 1><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 2 && sb == 2) spmm_generic_kernel<2, 16, 4, 2><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 2) spmm_generic_kernel<2, 16, 4, 4><<<grid, block, smem, stream>>>(p);
+    else if (rw == 16) spmm_generic_kernel<1, 16, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 8) spmm_generic_kernel<1, 8, 8><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 4) spmm_generic_kernel<1, 8, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 4 && V == 8) spmm_generic_kernel<1, 4, 8><<<grid, block, smem, stream>>>(p);
@@ -503,6 +778,11 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 1>();
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 2>();
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 4>();
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_generic_kernel<1, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
   });
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     cudaFree(h->d_meta);
