@@ -234,6 +234,12 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
     bias = torch.from_numpy(p.bias).to(dev)
     Y = torch.empty((p.M, Nr), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    kid = h.kernel_for(Nr, X.data_ptr(), Y.data_ptr())
+    kernel_desc = {1: f"spmm_tma_kernel<row,R_w={info['panel_rows']}>", 2: "spmm_tma_kernel<group>",
+                   3: f"sdnn_cg_p<0..{info['num_panels'] - 1}> (generated PTX)",
+                   4: "spmm_tmem_kernel<V=4,FILL=1> (X tile in TMEM, tcgen05.ld operands, 16-row panels)",
+                   5: "spmm_tmem_kernel<V=8,FILL=1> (X tile in TMEM, tcgen05.ld operands, 8-row panels)"
+                   }.get(abs(kid), str(kid)) + (" [generic fallback]" if kid < 0 else "")
 
     def step():
         h.spmm(X, bias, act=1, out=Y)
@@ -332,10 +338,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
                    "M": p.M, "K": p.K, "nnz": p.nnz, "N_total": N_job, "N_per_gpu": Nr,
                    "parallelism": f"column-sharded x{world}, W replicated, no data-path collective",
                    "l2": "inputs larger than L2 (X shard %.0f MiB > 126 MB L2); no flush" % (p.K * Nr * 4 / 2**20),
-                   "kernel": (f"sdnn_cg_p<0..{info['num_panels'] - 1}> (generated, {info['panel_rows']} rows/panel)"
-                              if info["kernel"] == 3 else
-                              f"{KERNEL}<{'group' if info['kernel'] == 2 else 'row'},R_w={info['panel_rows']},"
-                              f"V={'8' if info['num_row_blocks'] * ((Nr + 255) // 256) >= 296 else '4'}>"),
+                   "kernel": kernel_desc,
                    "group_entries_per_nnz": info["group_entries_per_nnz_x1000"] / 1000, "group_sb": info["group_sb"],
                    "panel_rows": info["panel_rows"], "cta_panels": info["cta_panels"], "k_chunk": info["k_chunk"],
                    "permuted": bool(info["permuted"]), "prep_ms": round(prep_ms, 1), "plan_hash_identical": same},
@@ -347,7 +350,8 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
                                     "re-measured in profiles/r01_microbench.log)",
                      "hbm": {"achieved_gbs": round(hbm_gbs, 1), "peak_gbs": hbm_peak,
                              "frac": round(hbm_gbs / hbm_peak, 4), "alg_bytes_per_launch": alg_bytes},
-                     "lds_ceiling_frac": 0.25},
+                     "operand_path": ("TMEM (tcgen05.ld) -> FFMA2" if abs(kid) in (4, 5)
+                                      else "shared memory (LDS.128) -> FFMA2; design ceiling 25% of fp32 peak")},
         "cpu_baseline": cpu,
         "e2e": {"value": round(flops_job / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": int(p.K * Nr * 4 + p.M * 4), "d2h_bytes_per_step": int(p.M * Nr * 4),

@@ -56,11 +56,19 @@ typedef enum { SDNN_ACT_NONE = 0, SDNN_ACT_RELU = 1 } sdnn_act;
 typedef struct {
   uint32_t struct_size;
   int32_t permute;          /* 1 (default): Algorithm 1 greedy row reorder; 0: identity   */
-  int32_t kernel;           /* 0 = auto (cost model), 1 = row kernel (each nonzero reads its X row
-                               slice from shared memory), 2 = group kernel (16-row groups: one X
-                               load feeds every nonzero of the group in that column), 3 = codegen
-                               (per-panel generated PTX with the weights as FFMA immediates,
-                               JIT-compiled during sdnn_prepare)                        */
+  int32_t kernel;           /* 0 = auto: the row kernel's plan (or the group kernel's, by cost model)
+                               plus the TMEM kernel's plan; each sdnn_spmm call takes the TMEM
+                               kernel when N % 128 == 0, X/Y are 16-byte aligned and the call fills
+                               one wave (row blocks · N tiles ≥ SMs), else the row plan.
+                               1 = row kernel (each nonzero reads its X row slice from shared
+                               memory), 2 = group kernel (16-row groups: one X load feeds every
+                               nonzero of the group in that column), 3 = codegen (per-panel
+                               generated PTX with the weights as FFMA immediates, JIT-compiled
+                               during sdnn_prepare), 4 = TMEM kernel (X tile staged in
+                               tensor memory, 4 columns of N per TMEM lane, operands read by
+                               tcgen05.ld; 16-row warp panels), 5 = TMEM kernel with 8 columns per
+                               lane (8-row panels).  4 and 5 take their fast path when N % 128 == 0
+                               and X/Y are 16-byte aligned, else a generic kernel on the same plan. */
   int32_t panel_rows_max;   /* row kernel: rows per warp panel, 0 = auto, else 4 or 8 (group: 16)   */
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
@@ -76,7 +84,7 @@ typedef struct {
   int64_t nnz;
   int32_t device;           /* CUDA ordinal, −1 for a host-only plan                                  */
   int32_t permuted;         /* 1 if Algorithm 1 was applied                                           */
-  int32_t kernel;           /* 1 = row kernel, 2 = group kernel                                       */
+  int32_t kernel;           /* the primary plan's kernel: 1 row, 2 group, 3 codegen, 4/5 TMEM         */
   int32_t group_entries_per_nnz_x1000; /* group format: union entries per nonzero · 1000            */
   int32_t group_sb;         /* group kernel sub-block rows (0 for the row kernel)                     */
   int32_t group_subblocks_per_nnz_x1000; /* nonzero sub-blocks per nonzero · 1000                    */
@@ -88,7 +96,7 @@ typedef struct {
   int32_t num_chunks;       /* ⌈K / KC⌉                                                               */
   int64_t meta_bytes;       /* device bytes of the execution-ordered stream                           */
   int32_t max_block_bytes;  /* largest (row block, chunk) metadata block, bytes                       */
-  int32_t reserved0;
+  int32_t alt_kernel;       /* auto handles: kernel of the second (TMEM) plan, else 0                 */
   int64_t max_panel_nnz;
 } sdnn_info;
 
@@ -138,6 +146,10 @@ SDNN_API sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t 
  * sdnn_get_permutation: out_perm (HOST, M entries) receives order[i] = original row at permuted
  * position i (Algorithm 1 output, SPEC S:295 convention).  sdnn_get_info fills *info. */
 SDNN_API sdnn_status sdnn_get_permutation(sdnn_handle h, int32_t* out_perm);
+/* Which kernel sdnn_spmm launches for these arguments (no launch, no device access; X and Y only
+ * for their alignment): 1 row, 2 group, 3 codegen, 4/5 TMEM; negative = that plan's generic
+ * (non-TMA) fallback kernel, used when N % 4 != 0 (N % 128 != 0 for 4/5) or X/Y are unaligned. */
+SDNN_API sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const float* Y, int32_t* kernel);
 SDNN_API sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info);
 
 /* ------------------------------------------------------------------ host-only planning (no GPU)

@@ -3,7 +3,7 @@
 Argument marshalling only: every step of the hot path (Algorithm 1, packing, the SpMM kernel, the
 fused epilogue) runs inside libsdnn.so.  PyTorch supplies device memory and streams.  There is no
 CPU fallback: if the in-tree library is missing this module raises on import; build it with
-`python -m paper_2101_07948_b200.build` or `__graft_entry__.build()`.
+`python paper_2101_07948_b200/build.py` or `__graft_entry__.build()`.
 """
 from __future__ import annotations
 
@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsdnn.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"libsdnn.so not built at {LIB_PATH}; run `python -m paper_2101_07948_b200.build`")
+    raise ImportError(f"libsdnn.so not built at {LIB_PATH}; run `python paper_2101_07948_b200/build.py`")
 
 _lib = ctypes.CDLL(LIB_PATH)
 
@@ -25,7 +25,8 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
           4: "SDNN_ERR_OUT_OF_MEMORY", 5: "SDNN_ERR_CUDA", 6: "SDNN_ERR_DEVICE_MISMATCH", 7: "SDNN_ERR_INTERNAL"}
 
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
-EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_host", "sdnn_get_permutation", "sdnn_get_info",
+EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_host", "sdnn_spmm_kernel", "sdnn_get_permutation",
+           "sdnn_get_info",
            "sdnn_permutation", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_destroy",
            "sdnn_plan_codegen_ptx", "sdnn_status_string", "sdnn_last_error_message", "sdnn_abi_version"]
 
@@ -51,11 +52,11 @@ class Info(ctypes.Structure):
                 ("group_sb", ctypes.c_int32), ("group_subblocks_per_nnz_x1000", ctypes.c_int32),
                 ("panel_rows", ctypes.c_int32), ("cta_panels", ctypes.c_int32), ("num_panels", ctypes.c_int32),
                 ("num_row_blocks", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
-                ("meta_bytes", ctypes.c_int64), ("max_block_bytes", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("meta_bytes", ctypes.c_int64), ("max_block_bytes", ctypes.c_int32), ("alt_kernel", ctypes.c_int32),
                 ("max_panel_nnz", ctypes.c_int64)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_ if f not in ("struct_size", "reserved0")}
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "struct_size"}
 
 
 _vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
@@ -64,6 +65,7 @@ _lib.sdnn_destroy.argtypes = [_vp]
 _lib.sdnn_spmm.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _vp]
 _lib.sdnn_spmm_host.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64]
 _lib.sdnn_get_permutation.argtypes = [_vp, _vp]
+_lib.sdnn_spmm_kernel.argtypes = [_vp, _i64, _vp, _vp, ctypes.POINTER(_i32)]
 _lib.sdnn_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
 _lib.sdnn_plan_create.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts), ctypes.POINTER(_vp)]
@@ -95,7 +97,7 @@ def _csr(row_ptr, col_idx, vals):
     return rp, ci, v
 
 
-KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4}
+KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4, "tmem8": 5}
 
 
 def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0):
@@ -181,6 +183,12 @@ class Handle:
         i.struct_size = ctypes.sizeof(Info)
         _check(_lib.sdnn_get_info(self._h, ctypes.byref(i)), "sdnn_get_info")
         return i.as_dict()
+
+    def kernel_for(self, N: int, x_ptr: int = 0, y_ptr: int = 0) -> int:
+        """Kernel id sdnn_spmm launches for N columns at these X/Y addresses (negative = generic)."""
+        k = _i32(0)
+        _check(_lib.sdnn_spmm_kernel(self._h, int(N), x_ptr or None, y_ptr or None, ctypes.byref(k)), "sdnn_spmm_kernel")
+        return k.value
 
     def permutation(self) -> np.ndarray:
         out = np.empty(self.M, np.int32)

@@ -38,6 +38,7 @@ struct Plan {
   // codegen kernel (kernel == 3): row panels (original row ids, Algorithm 1 order) baked into code
   std::vector<std::vector<int32_t>> cg_panels;
   int32_t cg_warps = 0, cg_prefetch = 0;
+  int32_t tmem_fill = 1;       // TMEM kernels: 1 = filler warps (tcgen05.st), 0 = tcgen05.cp
 };
 
 sdnn_status validate_csr(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K);
@@ -77,15 +78,21 @@ constexpr int kCgMaxRows = 128;     // codegen kernel: accumulators (rows) per p
 constexpr int kCgWarps = 6;         // codegen kernel: warps per CTA (2 CTAs/SM at <= 168 registers)
 constexpr int kCgPrefetch = 24;     // codegen kernel: X columns in flight per lane
 
-// TMEM kernel geometry: X tile lives in tensor memory, lane = 4 consecutive columns of N (128 lanes →
-// N tile 512), TMEM column = 4·k_local + v; two halves of 256 columns → K chunk 64; 16 consumer warps
-// = 4 warp slots per lane quarter, each slot a 16-row panel → 64 rows per CTA.
-constexpr int kTmemRows = 16;
+// TMEM kernels (sdnn_spmm.cu): the X tile lives in tensor memory.  TMEM lane L holds V columns of
+// N (n0 + 4L + v and, for V = 8, n0 + 512 + 4L + v): N tile 128·V; TMEM column V·k_local + v; two
+// halves of 256 columns → K chunk 256 / V.  16 consumer warps = 4 warp slots per lane quarter, each
+// slot a panel of tmem_rows(V) rows (accumulators: rows · V registers per thread).
+#ifdef __CUDACC__
+#define SDNN_HD __host__ __device__
+#else
+#define SDNN_HD
+#endif
+SDNN_HD constexpr int tmem_rows(int V) { return V == 4 ? 16 : 8; }
+SDNN_HD constexpr int tmem_kc(int V) { return 256 / V; }
+SDNN_HD constexpr int tmem_pad(int V) { return V == 4 ? 4 : 2; }  // row segments padded to multiples of this
 constexpr int kTmemPanels = 4;
-constexpr int kTmemKc = 64;
-constexpr int kTmemTN = 512;
-constexpr int kTmemPieceK = 16;   // K rows per TMA piece (16 × 512 × 4 B = 32 KB)
-constexpr int kTmemPieces = 4;    // smem ring depth (pieces)
+constexpr int kTmemPieces = 4;  // smem ring depth (32 KB TMA pieces)
+inline int tmem_v(int kernel) { return kernel == 5 ? 8 : 4; }
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 

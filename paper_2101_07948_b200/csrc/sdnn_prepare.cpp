@@ -95,6 +95,7 @@ void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32
 // ------------------------------------------------------------------------------------------------
 struct Geometry {
   int32_t kernel, rw, wc, kc, nch, nrb, sb;
+  int32_t tmem = 0;  // TMEM kernel variant of the row format (see emit_blocks)
 };
 struct EmitStats {
   int64_t entries = 0;    // row kernel: padded entries; group kernel: union entries
@@ -121,7 +122,12 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
       uint8_t* blk = out ? out + (*offs)[size_t(b) * g.nch + j] : nullptr;
       int64_t bytes = 0;
       if (g.kernel == 1) {
+        // TMEM variant (g.tmem = V): the column field is the TMEM column offset of X[col] in the
+        // chunk's TMEM half (V·col_local + 256·(j mod 2)), and every row segment is padded to a
+        // multiple of tmem_pad(V) entries with zero weights (the count in the header includes the
+        // padding) so the kernel runs one unrolled loop body per row; the padding adds 0·X (X finite).
         const int64_t hdr = align_up(int64_t(rcta) * 4, 16);
+        const uint32_t half = uint32_t(j & 1) * 256u;
         int32_t e = 0;
         for (int32_t s = 0; s < rcta; ++s) {
           const int32_t orow = row_orig[size_t(b) * rcta + s];
@@ -130,7 +136,7 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
             int32_t& p = cur[s];
             while (p < csr_ptr[orow + 1] && col_idx[p] < hi) {
               if (blk) {
-                const uint32_t cl = uint32_t(col_idx[p] - lo);
+                const uint32_t cl = g.tmem ? uint32_t(col_idx[p] - lo) * uint32_t(g.tmem) + half : uint32_t(col_idx[p] - lo);
                 std::memcpy(blk + hdr + size_t(e + c) * 8, &cl, 4);
                 std::memcpy(blk + hdr + size_t(e + c) * 8 + 4, &vals[p], 4);
               }
@@ -138,8 +144,12 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
               ++p;
             }
           }
-          if (blk) reinterpret_cast<uint32_t*>(blk)[s] = (uint32_t(e) << 16) | uint32_t(c);
-          e += int32_t(align_up(c, 2));
+          const int32_t cpad = g.tmem ? int32_t(align_up(c, tmem_pad(g.tmem))) : c;
+          if (blk) {
+            for (int32_t t = c; t < cpad; ++t) std::memcpy(blk + hdr + size_t(e + t) * 8, &half, 4);
+            reinterpret_cast<uint32_t*>(blk)[s] = (uint32_t(e) << 16) | uint32_t(cpad);
+          }
+          e += int32_t(align_up(cpad, 2));
         }
         ent_total += e;
         bytes = align_up(hdr + int64_t(e) * 8, 16);
@@ -228,9 +238,10 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     o = *opts;
     if (o.flags != 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.flags must be 0");
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
-    if (o.kernel < 0 || o.kernel > 4) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..4");
-    if (o.kernel == 4) {
-      if (o.panel_rows_max != 0 || o.cta_panels != 0 || (o.k_chunk != 0 && o.k_chunk != kTmemKc) || o.group_sb != 0)
+    if (o.kernel < 0 || o.kernel > 5) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..5");
+    if (o.kernel == 4 || o.kernel == 5) {
+      if (o.panel_rows_max != 0 || o.cta_panels != 0 || (o.k_chunk != 0 && o.k_chunk != tmem_kc(tmem_v(o.kernel))) ||
+          o.group_sb != 0)
         return fail(SDNN_ERR_INVALID_ARGUMENT, "the TMEM kernel has a fixed geometry (leave the tiling options 0)");
     } else if (o.kernel == 3) {
       if (o.panel_rows_max < 0 || o.panel_rows_max > kCgMaxRows)
@@ -307,12 +318,12 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     // the machine for the typical N.
     auto make_geo = [&](int32_t kernel, int32_t sb) {
       Geometry g{};
-      if (kernel == 4) {
-        // TMEM kernel (sdnn_spmm.cu): row-kernel format, 16-row warp panels, 4 panels per CTA row
-        // block (one per warp slot of a TMEM lane quarter), K chunk = one TMEM half (256 columns /
-        // 4 floats per lane) = 64.
+      if (kernel == 4 || kernel == 5) {
+        // TMEM kernels (sdnn_spmm.cu): row-kernel format, tmem_rows(V)-row warp panels, 4 panels
+        // per CTA row block (one per warp slot of a TMEM lane quarter), K chunk = one TMEM half.
         g.kernel = 1;
-        g.rw = kTmemRows;
+        g.tmem = tmem_v(kernel);
+        g.rw = tmem_rows(g.tmem);
         g.wc = kTmemPanels;
         g.nrb = (M + g.rw * g.wc - 1) / (g.rw * g.wc);
         return g;
@@ -408,9 +419,9 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     EmitStats stats;
     {
       std::vector<Geometry> cands;
-      if (o.kernel == 4) {
-        o.k_chunk = kTmemKc;
-        cands.push_back(make_geo(4, 0));
+      if (o.kernel == 4 || o.kernel == 5) {
+        o.k_chunk = tmem_kc(tmem_v(o.kernel));
+        cands.push_back(make_geo(o.kernel, 0));
       } else if (o.kernel != 2) {
         cands.push_back(make_geo(1, 0));
       }
@@ -428,7 +439,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       }
       if (!found) return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
     }
-    plan.kernel = o.kernel == 4 ? 4 : g.kernel;
+    plan.kernel = (o.kernel == 4 || o.kernel == 5) ? o.kernel : g.kernel;
     plan.panel_rows = g.rw;
     plan.cta_panels = g.wc;
     plan.num_row_blocks = g.nrb;
@@ -486,7 +497,7 @@ static void fill_info(const Plan& p, int32_t device, sdnn_info* info) {
   info->num_chunks = p.num_chunks;
   info->meta_bytes = int64_t(p.meta.size());
   info->max_block_bytes = p.max_block_bytes;
-  info->reserved0 = 0;
+  info->alt_kernel = 0;
   info->max_panel_nnz = p.max_panel_nnz;
 }
 

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -44,6 +45,10 @@ struct sdnn_handle_s {
   cudaEvent_t cg_fork = nullptr;
   int32_t cg_ctas = 1;  // persistent CTAs per panel kernel
   std::mutex cg_mu;     // the per-panel streams are shared by concurrent calls on one handle
+  // auto handles (kernel = 0): the TMEM plan prepared beside the row plan; sdnn_spmm takes it when
+  // the call fits its fast path and fills at least one wave of CTAs (tmem_worth)
+  sdnn_handle_s* alt = nullptr;
+  int32_t sms = 148;
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -95,11 +100,14 @@ struct KParams {
   int32_t K, nch, kc, wc, nrb, stages;
   int32_t x_stage_bytes, m_stage_bytes, hdr_bytes;
   int32_t act;
+  int32_t dbg;  // TMEM kernels, diagnostics only (SDNN_DEBUG_TMEM): bit 0 skip the X loads, bit 1 skip the FMAs
 };
 
 // Consume one chunk: for each of the warp's RW rows, every (col, w) entry of the chunk:
 // acc[r] += w · X_stage[col][lane·4 .. +4] (and +128 for V = 8), ascending column order.
-template <int RW, int V>
+// TF = log2 of the TMEM-kernel metadata scale (column field = 2^TF·col_local + 256·half; 0 = row format),
+// read by the generic fallback of a TMEM plan.
+template <int RW, int V, int TF = 0>
 __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const float* __restrict__ xs,
                                               const uint8_t* __restrict__ ms, int warp, int lane, int hdr_bytes) {
   constexpr int TN = 32 * V;
@@ -114,7 +122,7 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
     for (int i = 0; i < cnt; i += 2) {
       const float4 ee = e[i >> 1];
       {
-        const float* xp = xl + __float_as_int(ee.x) * TN;
+        const float* xp = xl + (TF ? ((__float_as_int(ee.x) & 255) >> TF) : __float_as_int(ee.x)) * TN;
         const float2 w2 = make_float2(ee.y, ee.y);
         const float4 x0 = *reinterpret_cast<const float4*>(xp);
         acc[r][0] = __ffma2_rn(w2, make_float2(x0.x, x0.y), acc[r][0]);
@@ -126,7 +134,7 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
         }
       }
       if (i + 1 < cnt) {
-        const float* xp = xl + __float_as_int(ee.z) * TN;
+        const float* xp = xl + (TF ? ((__float_as_int(ee.z) & 255) >> TF) : __float_as_int(ee.z)) * TN;
         const float2 w2 = make_float2(ee.w, ee.w);
         const float4 x0 = *reinterpret_cast<const float4*>(xp);
         acc[r][0] = __ffma2_rn(w2, make_float2(x0.x, x0.y), acc[r][0]);
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) 
     if constexpr (KIND == 2)
       consume_group<V, SB>(acc, xs, ms, warp, lane);
     else
-      consume_chunk<RW, V>(acc, xs, ms, warp, lane, p.hdr_bytes);
+      consume_chunk<RW, V, (KIND >= 4 ? KIND - 2 : 0)>(acc, xs, ms, warp, lane, p.hdr_bytes);
   }
   epilogue<RW, V, false>(acc, p, rb * p.wc + warp, lane, n0);
 }
@@ -358,17 +366,24 @@ __device__ __forceinline__ void fma4(float2 (&acc)[2], float w, const float4& x)
   acc[0] = __ffma2_rn(w2, make_float2(x.x, x.y), acc[0]);
   acc[1] = __ffma2_rn(w2, make_float2(x.z, x.w), acc[1]);
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float4 (&v)[4]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "f"(v[0].x), "f"(v[0].y), "f"(v[0].z), "f"(v[0].w), "f"(v[1].x), "f"(v[1].y), "f"(v[1].z), "f"(v[1].w),
+      "f"(v[2].x), "f"(v[2].y), "f"(v[2].z), "f"(v[2].w), "f"(v[3].x), "f"(v[3].y), "f"(v[3].z), "f"(v[3].w));
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tc_cp_128x128b(uint32_t taddr, uint64_t desc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+__device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
 }
 // Shared-memory matrix descriptor (tcgen05): no swizzle, K-major canonical layout — 8-row × 16-byte
-// core matrices, 128 B apart along the 128 rows (SBO); one 16-byte column so LBO is unused.
+// core matrices, 128 B apart along the 128 rows (SBO); the second 16-byte column 2 KB further (LBO).
 __device__ __forceinline__ uint64_t cp_desc(uint32_t saddr) {
   return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(2048 >> 4) << 16) | (uint64_t(128 >> 4) << 32) |
          (uint64_t(1) << 46);
@@ -383,21 +398,48 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 constexpr int kTmemConsumers = 4 * kTmemPanels;  // 16 consumer warps
-constexpr int kTmemPieceBytes = kTmemPieceK * kTmemTN * 4;
+constexpr int kTmemPieceBytes = 32 * 1024;        // one TMA piece: 8192 / (128·V) K rows × 128·V columns
 constexpr int kTmemMetaSlots = 2;
 constexpr size_t tmem_smem_bytes(int m_stage_bytes) {
   return size_t(kTmemPieces) * kTmemPieceBytes + size_t(kTmemMetaSlots) * m_stage_bytes + 16 * 8 + 16;
 }
 
-__global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
+template <int V> struct TmemLd;
+template <> struct TmemLd<4> {
+  static __device__ __forceinline__ void ld(uint32_t taddr, float4 (&v)[1]) { tmem_ld4(taddr, v[0]); }
+};
+template <> struct TmemLd<8> {
+  static __device__ __forceinline__ void ld(uint32_t taddr, float4 (&v)[2]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[0].z), "=f"(v[0].w), "=f"(v[1].x), "=f"(v[1].y), "=f"(v[1].z),
+                   "=f"(v[1].w)
+                 : "r"(taddr));
+  }
+};
+
+// V = 4: TMEM lane L ↔ columns n0 + 4L + {0..3}; V = 8: also n0 + 512 + 4L + {0..3} (TMEM columns
+// 8k + 4..7), so both halves of a lane's data come from contiguous 2 KB runs of an X row and the
+// epilogue stores two coalesced float4 per row.
+// FILL 0: one producer warp moves each TMA piece into TMEM with tcgen05.cp (~46 B/clk/SM at most,
+// profiles/r01_tmem_cp.log); FILL 1: four filler warps (one per TMEM lane quarter) read the piece
+// with LDS.128 and write TMEM with tcgen05.st.32x32b.x16 (~216 B/clk/SM), filler 0 lane 0 also
+// issues the TMA and metadata copies.
+template <int FILL> __host__ __device__ constexpr int tmem_side_warps() { return FILL ? 4 : 1; }
+template <int V, int FILL>
+__global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 32, 1)
     spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int RW = kTmemRows;
-  constexpr int PPC = kTmemKc / kTmemPieceK;  // pieces per K chunk
+  constexpr int RW = tmem_rows(V);
+  constexpr int TN = 128 * V;
+  constexpr int KC = tmem_kc(V);
+  constexpr int PK = 8192 / TN;  // K rows per 32 KB piece
+  constexpr int PPC = KC / PK;   // pieces per K chunk
   constexpr int S = kTmemPieces, MS = kTmemMetaSlots;
+  constexpr int G = V / 4;       // float4 groups per lane
+  constexpr int U = tmem_pad(V); // nonzeros per unrolled step (row segments are padded to U)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = blockIdx.x % p.nrb;
-  const int64_t n0 = int64_t(blockIdx.x / p.nrb) * kTmemTN;
+  const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
   uint8_t* xring = smem;
   uint8_t* mring = smem + size_t(S) * kTmemPieceBytes;
   uint64_t* slot_full = reinterpret_cast<uint64_t*>(mring + size_t(MS) * p.m_stage_bytes);
@@ -410,10 +452,10 @@ __global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&slot_full[s], 1);
-      mbar_init(&slot_empty[s], 1);
+      mbar_init(&slot_empty[s], tmem_side_warps<FILL>());
     }
     for (int h = 0; h < 2; ++h) {
-      mbar_init(&tfull[h], 1);
+      mbar_init(&tfull[h], tmem_side_warps<FILL>());
       mbar_init(&tfree[h], kTmemConsumers);
     }
     for (int m = 0; m < MS; ++m) {
@@ -431,7 +473,71 @@ __global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
   tc_fence_after();
   const uint32_t tbase = *tbase_s;
 
-  if (warp == kTmemConsumers) {  // producer: TMA → smem ring → tcgen05.cp → TMEM half
+  if (FILL == 1 && warp >= kTmemConsumers) {  // fillers: TMA → smem ring → LDS.128 → tcgen05.st → TMEM half
+    const int q = warp & 3;  // warps 16..19 → lane quarters 0..3
+    const uint32_t tq = tbase + (uint32_t(q * 32) << 16);
+    const bool leader = warp == kTmemConsumers && lane == 0;
+    const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
+    const int total = p.nch * PPC;
+    const int32_t nb = int32_t(n0 / 128);
+    auto load_piece = [&](int i) {
+      const int s = i % S;
+      if (p.dbg & 1) {
+        mbar_arrive(&slot_full[s]);
+        return;
+      }
+      mbar_expect_tx(&slot_full[s], kTmemPieceBytes);
+      tma_load_3d(xring + size_t(s) * kTmemPieceBytes, &tmap, 0, nb, i * PK, &slot_full[s]);
+    };
+    auto load_meta = [&](int j) {
+      const int m = j % MS;
+      const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
+      mbar_expect_tx(&mfull[m], mbytes);
+      bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[j], mbytes, &mfull[m]);
+    };
+    if (leader) {
+      for (int i = 0; i < S && i < total; ++i) load_piece(i);
+      for (int j = 0; j < MS && j < p.nch; ++j) load_meta(j);
+    }
+    for (int j = 0; j < p.nch; ++j) {
+      const int h = j & 1;
+      if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
+        mbar_wait(&tfree[h], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        if (leader) {
+          mbar_wait(&mempty[j % MS], ((j >> 1) - 1) & 1);
+          load_meta(j);
+        }
+      }
+      for (int pc = 0; pc < PPC; ++pc) {
+        const int i = j * PPC + pc, s = i % S;
+        mbar_wait(&slot_full[s], (i / S) & 1);
+        const float4* src = reinterpret_cast<const float4*>(xring + size_t(s) * kTmemPieceBytes) + q * 32 + lane;
+        // all PK·V/4 LDS.128 of the piece first (latency overlapped), then the tcgen05.st.x16s
+        constexpr int NST = PK * V / 16;
+        float4 v[NST][4];
+#pragma unroll
+        for (int u = 0; u < NST; ++u)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int kk = u * (16 / V);
+            v[u][t] = V == 4 ? src[(kk + t) * (TN / 4)] : src[(kk + (t >> 1)) * (TN / 4) + (t & 1) * 128];
+          }
+#pragma unroll
+        for (int u = 0; u < NST; ++u) tmem_st16(tq + uint32_t(h * 256 + (pc * PK + u * (16 / V)) * V), v[u]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&slot_empty[s]);
+        if (leader && i + S < total) {
+          mbar_wait(&slot_empty[s], (i / S) & 1);
+          load_piece(i + S);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfull[h]);
+    }
+  } else if (warp == kTmemConsumers) {  // producer: TMA → smem ring → tcgen05.cp → TMEM half
     if (lane == 0) {
       const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
       const int total = p.nch * PPC;
@@ -439,7 +545,7 @@ __global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
       auto load_piece = [&](int i) {
         const int s = i % S;
         mbar_expect_tx(&slot_full[s], kTmemPieceBytes);
-        tma_load_3d(xring + size_t(s) * kTmemPieceBytes, &tmap, 0, nb, i * kTmemPieceK, &slot_full[s]);
+        tma_load_3d(xring + size_t(s) * kTmemPieceBytes, &tmap, 0, nb, i * PK, &slot_full[s]);
       };
       auto load_meta = [&](int j) {
         const int m = j % MS;
@@ -459,9 +565,13 @@ __global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
         }
         mbar_wait(&slot_full[s], (i / S) & 1);
         const uint32_t src = smem_u32(xring + size_t(s) * kTmemPieceBytes);
+        // tcgen05.cp.128x256b: lane L ← 16 B at 16L (SBO 128 B per 8 lanes) and 16 B one LBO =
+        // 2 KB further: V = 4 → K rows kk, kk+1 (TMEM columns 4kk..4kk+7); V = 8 → columns n0+4L
+        // and n0+512+4L of row kk (TMEM columns 8kk..8kk+7).  ~90 cycles per copy whatever its
+        // size (profiles/r01_tmem_cp.log), so the widest shape.
 #pragma unroll
-        for (int kk = 0; kk < kTmemPieceK; ++kk)
-          tc_cp_128x128b(tbase + uint32_t(h * 256 + (pc * kTmemPieceK + kk) * 4), cp_desc(src + kk * kTmemTN * 4));
+        for (int kk = 0; kk < PK; kk += 8 / V)
+          tc_cp_128x256b(tbase + uint32_t(h * 256 + (pc * PK + kk) * V), cp_desc(src + uint32_t(kk * TN) * 4));
         tc_commit(&slot_empty[s]);
         if (pc == PPC - 1) tc_commit(&tfull[h]);
         if (i + S < total) {
@@ -473,9 +583,11 @@ __global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
   } else {
     const int q = warp & 3, wi = warp >> 2;
     const uint32_t tl = tbase + (uint32_t(q * 32) << 16);
-    float2 acc[RW][2];
+    float2 acc[RW][2 * G];
 #pragma unroll
-    for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int c = 0; c < 2 * G; ++c) acc[r][c] = make_float2(0.f, 0.f);
     for (int j = 0; j < p.nch; ++j) {
       const int h = j & 1, m = j % MS;
       mbar_wait(&mfull[m], (j / MS) & 1);
@@ -484,42 +596,33 @@ __global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
       const uint8_t* ms = mring + size_t(m) * p.m_stage_bytes;
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + wi * RW;
       const float4* ent = reinterpret_cast<const float4*>(ms + p.hdr_bytes);
-      const uint32_t hb = tl + uint32_t(h * 256);
 #pragma unroll
       for (int r = 0; r < RW; ++r) {
         const uint32_t hh = hdr[r];
         const int cnt = int(hh & 0xffffu);
         const float4* e = ent + (hh >> 16) / 2;
-        int i = 0;
-        for (; i + 4 <= cnt; i += 4) {  // 4 nonzeros: 4 TMEM loads in flight, then 8 FFMA2
-          const float4 e0 = e[i >> 1], e1 = e[(i >> 1) + 1];
-          float4 xa, xb, xc, xd;
-          tmem_ld4(hb + (__float_as_uint(e0.x) << 2), xa);
-          tmem_ld4(hb + (__float_as_uint(e0.z) << 2), xb);
-          tmem_ld4(hb + (__float_as_uint(e1.x) << 2), xc);
-          tmem_ld4(hb + (__float_as_uint(e1.z) << 2), xd);
-          tmem_wait_ld(xa, xb, xc, xd);
-          fma4(acc[r], e0.y, xa);
-          fma4(acc[r], e0.w, xb);
-          fma4(acc[r], e1.y, xc);
-          fma4(acc[r], e1.w, xd);
-        }
-        if (i + 2 <= cnt) {
-          const float4 e0 = e[i >> 1];
-          float4 xa, xb;
-          tmem_ld4(hb + (__float_as_uint(e0.x) << 2), xa);
-          tmem_ld4(hb + (__float_as_uint(e0.z) << 2), xb);
-          tmem_wait_ld(xa, xb);
-          fma4(acc[r], e0.y, xa);
-          fma4(acc[r], e0.w, xb);
-          i += 2;
-        }
-        if (i < cnt) {
-          const float4 e0 = e[i >> 1];
-          float4 xa;
-          tmem_ld4(hb + (__float_as_uint(e0.x) << 2), xa);
-          tmem_wait_ld(xa);
-          fma4(acc[r], e0.y, xa);
+        if (p.dbg & 2) continue;
+        for (int i = 0; i < cnt; i += U) {  // U nonzeros (zero-padded): U TMEM loads, then the FFMA2s
+          float4 ee[U / 2];
+#pragma unroll
+          for (int t = 0; t < U / 2; ++t) ee[t] = e[(i >> 1) + t];
+          float4 x[U][G];
+#pragma unroll
+          for (int t = 0; t < U / 2; ++t) {
+            TmemLd<V>::ld(tl + __float_as_uint(ee[t].x), x[2 * t]);
+            TmemLd<V>::ld(tl + __float_as_uint(ee[t].z), x[2 * t + 1]);
+          }
+          if constexpr (U == 4 && G == 1) tmem_wait_ld(x[0][0], x[1][0], x[2][0], x[3][0]);
+          else tmem_wait_ld(x[0][0], x[0][1], x[1][0], x[1][1]);
+#pragma unroll
+          for (int t = 0; t < U; ++t) {
+            const float w = (t & 1) ? ee[t >> 1].w : ee[t >> 1].y;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              float2 (&a)[2] = *reinterpret_cast<float2(*)[2]>(&acc[r][2 * g]);
+              fma4(a, w, x[t][g]);
+            }
+          }
         }
       }
       tc_fence_before();
@@ -529,7 +632,24 @@ __global__ void __launch_bounds__((kTmemConsumers + 1) * 32, 1)
         mbar_arrive(&mempty[m]);
       }
     }
-    epilogue<RW, 4, true>(acc, p, rb * kTmemPanels + wi, lane, n0 + q * 128);
+    // epilogue: row panel rb·4 + wi; lane columns n0 + 128q + 4·lane (+ 512 for the second group)
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int32_t orow = p.row_orig[(rb * kTmemPanels + wi) * RW + r];
+      if (orow < 0) continue;
+      const float b = p.bias ? p.bias[orow] : 0.f;
+      float* yrow = p.Y + int64_t(orow) * p.N;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int64_t n = n0 + g * 512 + q * 128 + lane * 4;
+        float v[4] = {acc[r][2 * g].x + b, acc[r][2 * g].y + b, acc[r][2 * g + 1].x + b, acc[r][2 * g + 1].y + b};
+        if (p.act == SDNN_ACT_RELU) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) v[t] = v[t] > 0.f ? v[t] : 0.f;
+        }
+        if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -603,7 +723,8 @@ static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, c
 static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                float* Y, cudaStream_t stream) {
   const Plan& pl = h->plan;
-  const int64_t ntiles = (N + kTmemTN - 1) / kTmemTN;
+  const int V = tmem_v(pl.kernel), TN = 128 * V;
+  const int64_t ntiles = (N + TN - 1) / TN;
   const int64_t nblocks = ntiles * pl.num_row_blocks;
   if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "N too large for one launch");
   KParams p{};
@@ -622,14 +743,21 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   p.m_stage_bytes = int32_t(align_up(pl.max_block_bytes, 128));
   p.hdr_bytes = int32_t(align_up(int64_t(pl.panel_rows) * pl.cta_panels * 4, 16));
   p.act = act;
+  {
+    static const int dbg = [] {
+      const char* e = getenv("SDNN_DEBUG_TMEM");
+      return e ? atoi(e) : 0;
+    }();
+    p.dbg = dbg;
+  }
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  // 3-D view of X: {128 columns, N/128 column blocks, K rows}, so one box {128, 4, 16} lands in
-  // shared memory as 16 contiguous 512-column K rows.
+  // 3-D view of X: {128 columns, N/128 column blocks, K rows}, so one box {128, V, 8192/TN} lands in
+  // shared memory as contiguous TN-column K rows (32 KB).
   CUtensorMap tmap;
   const cuuint64_t dims[3] = {128, cuuint64_t(N / 128), cuuint64_t(pl.K)};
   const cuuint64_t strides[2] = {512, cuuint64_t(N) * 4};
-  const cuuint32_t box[3] = {128, kTmemTN / 128, kTmemPieceK};
+  const cuuint32_t box[3] = {128, cuuint32_t(V), cuuint32_t(8192 / TN)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -637,23 +765,36 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(int(cr)));
   const size_t smem = tmem_smem_bytes(p.m_stage_bytes);
   if (smem > size_t(kSmemBudget) + 1024) return fail(SDNN_ERR_INTERNAL, "TMEM kernel stage does not fit shared memory");
-  spmm_tmem_kernel<<<unsigned(nblocks), (kTmemConsumers + 1) * 32, smem, stream>>>(tmap, p);
+  const int fill = pl.tmem_fill;
+  const unsigned threads = unsigned(kTmemConsumers + (fill ? 4 : 1)) * 32;
+  if (V == 8 && fill) spmm_tmem_kernel<8, 1><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
+  else if (V == 8) spmm_tmem_kernel<8, 0><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
+  else if (fill) spmm_tmem_kernel<4, 1><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
+  else spmm_tmem_kernel<4, 0><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
   SDNN_CUDA_TRY(cudaGetLastError());
   return SDNN_OK;
 }
 
+// The TMEM kernel runs one CTA per SM: it pays when the call fills at least one wave.
+static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const float* Y) {
+  return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 &&
+         int64_t(a->plan.num_row_blocks) * ((N + 128 * tmem_v(a->plan.kernel) - 1) / (128 * tmem_v(a->plan.kernel))) >=
+             a->sms;
+}
+
 static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
                           cudaStream_t stream) {
+  if (tmem_worth(h->alt, X, N, Y)) return launch_tmem(h->alt, X, N, bias, act, Y, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, Y, stream);
-  if (pl.kernel == 4 && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+  if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(Y) % 16 == 0)
     return launch_tmem(h, X, N, bias, act, Y, stream);
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
   int V = 8;
   if (int64_t(pl.num_row_blocks) * ((N + 255) / 256) < 2 * 148) V = 4;
-  if (pl.kernel == 4) V = 4;  // TMEM plan on a ragged / unaligned call: generic kernel, 16-row panels
+  if (pl.kernel == 4 || pl.kernel == 5) V = 4;  // TMEM plan, ragged / unaligned call: generic kernel
   const int TN = 32 * V;
   const int64_t ntiles = (N + TN - 1) / TN;
   const int64_t nblocks = ntiles * pl.num_row_blocks;
@@ -678,7 +819,7 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
   p.act = act;
 
   const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
-                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0) && pl.kernel != 4;
+                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0) && pl.kernel < 4;
   if (fast) {
     int S = int(kSmemBudget / (p.x_stage_bytes + p.m_stage_bytes));
     S = std::min(S, std::min(pl.num_chunks, 4));
@@ -719,7 +860,8 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
     else if (pl.kernel == 2 && sb == 1) spmm_generic_kernel<2, 16, 4, 1><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 2 && sb == 2) spmm_generic_kernel<2, 16, 4, 2><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 2) spmm_generic_kernel<2, 16, 4, 4><<<grid, block, smem, stream>>>(p);
-    else if (rw == 16) spmm_generic_kernel<1, 16, 4><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 4) spmm_generic_kernel<4, 16, 4><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 5) spmm_generic_kernel<5, 8, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 8) spmm_generic_kernel<1, 8, 8><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 4) spmm_generic_kernel<1, 8, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 4 && V == 8) spmm_generic_kernel<1, 4, 8><<<grid, block, smem, stream>>>(p);
@@ -746,8 +888,8 @@ static sdnn_status check_device(const sdnn_handle_s* h) {
 
 extern "C" {
 
-sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
-                         const sdnn_perm_opts* perm_opts, sdnn_handle* out) {
+static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M,
+                               int32_t K, const sdnn_perm_opts* perm_opts, sdnn_handle* out) {
   if (!out) return fail(SDNN_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   int dev = -1;
@@ -765,6 +907,7 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
     return st;
   }
   h->device = dev;
+  h->sms = prop.multiProcessorCount;
   static std::once_flag attr_once[64];
   cudaError_t ae = cudaSuccess;
   std::call_once(attr_once[dev & 63], [&] {
@@ -779,10 +922,19 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 2>();
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 4>();
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_generic_kernel<1, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ae = cudaFuncSetAttribute(spmm_generic_kernel<4, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+      ae = cudaFuncSetAttribute(spmm_generic_kernel<5, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
   });
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     cudaFree(h->d_meta);
@@ -836,8 +988,31 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
   return SDNN_OK;
 }
 
+sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
+                         const sdnn_perm_opts* perm_opts, sdnn_handle* out) {
+  sdnn_status st = prepare_one(csr_ptr, col_idx, vals, M, K, perm_opts, out);
+  if (st != SDNN_OK || (perm_opts && perm_opts->kernel != 0)) return st;
+  // auto: also the TMEM plan (same permutation, same per-row accumulation order → the two give
+  // bitwise-identical results up to the sign of an exact zero)
+  sdnn_perm_opts o{};
+  o.struct_size = sizeof(o);
+  o.permute = perm_opts ? perm_opts->permute : 1;
+  o.kernel = 4;
+  sdnn_handle alt = nullptr;
+  st = prepare_one(csr_ptr, col_idx, vals, M, K, &o, &alt);
+  if (st != SDNN_OK) {
+    std::string m = sdnn_last_error_message();
+    sdnn_destroy(*out);
+    *out = nullptr;
+    return fail(st, m);
+  }
+  (*out)->alt = alt;
+  return SDNN_OK;
+}
+
 sdnn_status sdnn_destroy(sdnn_handle h) {
   if (!h) return SDNN_OK;
+  if (h->alt) sdnn_destroy(h->alt);
   int cur = -1;
   cudaGetDevice(&cur);
   if (cur != h->device) cudaSetDevice(h->device);
@@ -958,6 +1133,18 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
   return SDNN_OK;
 }
 
+sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const float* Y, int32_t* kernel) {
+  if (!h || !kernel || N < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle / kernel or N < 0");
+  if (tmem_worth(h->alt, X, N, Y)) {
+    *kernel = h->alt->plan.kernel;
+    return SDNN_OK;
+  }
+  const int k = h->plan.kernel;
+  const bool tma = N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0;
+  *kernel = (k == 4 || k == 5) ? (N % 128 == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
+  return SDNN_OK;
+}
+
 sdnn_status sdnn_get_permutation(sdnn_handle h, int32_t* out_perm) {
   if (!h || !out_perm) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle or out_perm");
   std::memcpy(out_perm, h->plan.perm.data(), h->plan.perm.size() * 4);
@@ -969,6 +1156,7 @@ sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info) {
   if (info->struct_size != sizeof(sdnn_info)) return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_info.struct_size mismatch");
   plan_fill_info(h->plan, h->device, info);
   info->meta_bytes = h->plan.meta_size_uploaded;
+  info->alt_kernel = h->alt ? h->alt->plan.kernel : 0;
   return SDNN_OK;
 }
 

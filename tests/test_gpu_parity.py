@@ -60,7 +60,7 @@ def test_worked_example(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ BASELINE configs c1-c4 (full size)
-@pytest.mark.parametrize("kernel", ["auto", "row", "group1", "group2", "group4", "codegen"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "group1", "group2", "group4", "codegen", "tmem", "tmem8"])
 @pytest.mark.parametrize("key", [k for k in synth.CONFIGS if k != "c5"])
 def test_config_parity(sdnn, oracle_mod, key, kernel):
     p = synth.config_problem(key)
@@ -75,7 +75,7 @@ def test_c2_no_act(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ desk grid
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
 @pytest.mark.parametrize("g", list(synth.desk_grid()), ids=lambda g: f"{g['name']}_s{g['seed']}")
 def test_desk_grid(sdnn, oracle_mod, g, kernel):
     p = synth.make_problem(g["name"], g["M"], g["K"], g["N"], g["sparsity"], seed=g["seed"])
@@ -83,7 +83,7 @@ def test_desk_grid(sdnn, oracle_mod, g, kernel):
 
 
 # ------------------------------------------------------------------ c5 at full size, launch config of bench.py
-@pytest.mark.parametrize("kernel", ["auto", "row", "codegen"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "codegen", "tmem", "tmem8"])
 def test_c5_full_size_sampled_columns(sdnn, oracle_mod, kernel):
     p = synth.config_problem("c5")
     h = sdnn.Handle.from_problem(p, kernel=kernel)
@@ -103,14 +103,14 @@ def test_c5_full_size_sampled_columns(sdnn, oracle_mod, kernel):
 
 
 # ------------------------------------------------------------------ edge cases
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
-@pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 127, 129, 300, 1000])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 127, 128, 129, 256, 300, 384, 1000, 1024])
 def test_ragged_n(sdnn, oracle_mod, N, kernel):
     p = synth.make_problem("ragged", 200, 150, N, 0.9, mask="lognormal", seed=N)
     check(sdnn, oracle_mod, p, kernel=kernel)
 
 
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
 def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     p = synth.make_problem("unal", 100, 90, 64, 0.8, seed=1)
     X = p.x()
@@ -125,9 +125,11 @@ def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     assert_parity(Yv.cpu().numpy(), Yo, S, "unaligned")
 
 
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
 @pytest.mark.parametrize("M,K,N,dens", [(1, 1, 4, 1.0), (1, 500, 8, 0.3), (500, 1, 8, 0.5), (37, 65, 12, 1.0),
-                                        (129, 257, 20, 0.0), (64, 64, 64, 1.0), (2100, 70, 40, 0.05)])
+                                        (129, 257, 20, 0.0), (64, 64, 64, 1.0), (2100, 70, 40, 0.05),
+                                        (1, 500, 128, 0.3), (500, 1, 256, 0.5), (129, 257, 384, 0.0),
+                                        (2100, 70, 128, 0.05), (65, 300, 1024, 1.0)])
 def test_degenerate_shapes(sdnn, oracle_mod, M, K, N, dens, kernel):
     rng = np.random.default_rng(M + K + N)
     mask = rng.random((M, K)) < dens
@@ -167,7 +169,9 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
                  dict(k_chunk=96, panel_rows=4, cta_panels=2), dict(kernel="group"), dict(kernel="row"),
                  dict(kernel="group", permute=False), dict(kernel="group", cta_panels=3, k_chunk=16),
                  dict(kernel="group", group_sb=1), dict(kernel="group", group_sb=2), dict(kernel="group", group_sb=4),
-                 dict(kernel="codegen"), dict(kernel="codegen", permute=False), dict(kernel="codegen", panel_rows=7)]:
+                 dict(kernel="codegen"), dict(kernel="codegen", permute=False), dict(kernel="codegen", panel_rows=7),
+                 dict(kernel="tmem"), dict(kernel="tmem", permute=False), dict(kernel="tmem8"),
+                 dict(kernel="tmem8", permute=False)]:
         Y, _ = run_gpu(sdnn, p, X, p.bias, 1, **opts)
         np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
 
@@ -193,18 +197,18 @@ def test_repeat_bitwise_and_linearity(sdnn):
     np.testing.assert_array_equal(Y3, 2 * Y1)
 
 
-@pytest.mark.parametrize("kernel", ["row", "codegen"])
+@pytest.mark.parametrize("kernel", ["row", "codegen", "tmem", "auto"])
 def test_host_entry_point_matches_device(sdnn, kernel):
     p = synth.config_problem("c3_256x128")
     X = p.x()
     h = sdnn.Handle.from_problem(p, kernel=kernel)
     ref, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
-    for bc in (0, 512, 1000, 4):
+    for bc in (0, 512, 1000, 4, 2048):
         Y = h.spmm_host(X, p.bias, act=1, block_cols=bc)
         np.testing.assert_array_equal(Y, ref)
 
 
-@pytest.mark.parametrize("kernel", ["row", "codegen"])
+@pytest.mark.parametrize("kernel", ["row", "codegen", "tmem", "tmem8", "auto"])
 def test_cuda_graph_capture(sdnn, kernel):
     p = synth.config_problem("c3_512x512")
     h = sdnn.Handle.from_problem(p, kernel=kernel)
@@ -219,6 +223,21 @@ def test_cuda_graph_capture(sdnn, kernel):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(Y, ref)
+
+
+def test_auto_takes_tmem_plan_when_it_fills_a_wave(sdnn):
+    """kernel=auto keeps a TMEM plan beside the row plan (info alt_kernel = 4) and uses it when the
+    call is on its fast path and fills one wave; either way the result equals the row kernel's."""
+    p = synth.config_problem("c4_2048x512_s80")  # 32 row blocks × 25 N tiles ≥ 148 SMs
+    X = p.x()
+    h = sdnn.Handle.from_problem(p)
+    assert h.info()["alt_kernel"] == 4 and h.info()["kernel"] == 1
+    Ya, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    Yr, _ = run_gpu(sdnn, p, X, p.bias, 1, kernel="row")
+    np.testing.assert_array_equal(Ya, Yr)
+    Xs = np.ascontiguousarray(X[:, :100])  # ragged: the row plan
+    Ya, _ = run_gpu(sdnn, p, Xs, p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Ya, Yr[:, :100])
 
 
 def test_get_permutation_and_info(sdnn, oracle_mod):

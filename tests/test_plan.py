@@ -14,6 +14,9 @@ def decode(p, plan):
         return decode_group(p, plan)
     row_orig, blk_off, meta = plan.export()
     rw, wc, kc, nch, nrb = (info[k] for k in ("panel_rows", "cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
+    V = {4: 4, 5: 8}.get(info["kernel"], 0)
+    if V:
+        assert (rw, wc, kc) == ((16, 4, 64) if V == 4 else (8, 4, 32))
     rcta = rw * wc
     hdr_bytes = (rcta * 4 + 15) // 16 * 16
     assert blk_off[0] == 0 and blk_off[-1] == meta.size and np.all(np.diff(blk_off) > 0)
@@ -33,10 +36,19 @@ def decode(p, plan):
                 if orow < 0:
                     assert cnt == 0
                     continue
+                if V:  # TMEM format: segments padded to multiples of 4 (V = 4) / 2 (V = 8)
+                    assert cnt % (4 if V == 4 else 2) == 0
                 for i in range(cnt):
                     e = ent[(start + i) * 8:(start + i) * 8 + 8]
                     cl = int(e[:4].view(np.uint32)[0])
                     w = e[4:].view(np.float32)[0]
+                    if V:  # column field = V·col_local + 256·(chunk parity): the TMEM column of X[col]
+                        half = 256 * (j & 1)
+                        if w == 0:
+                            assert cl == half  # padding entry
+                            continue
+                        assert (cl - half) % V == 0 and 0 <= cl - half < 256
+                        cl = (cl - half) // V
                     assert 0 <= cl < kc
                     col = j * kc + cl
                     assert col > last_col.get(orow, -1)  # ascending column order per row
@@ -119,6 +131,8 @@ def test_c_alg1_equals_bruteforce_random(oracle_mod, seed):
     ("c4_2048x512_s95", dict(kernel="group", k_chunk=16)), ("c2_768x768", dict(kernel="group", permute=False)),
     ("c2_768x768", dict(kernel="group", group_sb=1)), ("c3_512x512", dict(kernel="group", group_sb=2)),
     ("c4_512x2048_s80", dict(kernel="group", group_sb=4)),
+    ("c1", dict(kernel="tmem")), ("c2_768x3072", dict(kernel="tmem")), ("c4_2048x512_s95", dict(kernel="tmem", permute=False)),
+    ("c1", dict(kernel="tmem8")), ("c2_768x768", dict(kernel="tmem8")), ("c4_512x2048_s80", dict(kernel="tmem8")),
 ])
 def test_packing_invariants(oracle_mod, key, opts):
     p = synth.config_problem(key, N=4)
@@ -167,10 +181,19 @@ def test_degenerate_shapes():
         v = rng.standard_normal(ci.size).astype(np.float32)
         p = synth.Problem("d", M, K, 1, 0, "x", rp, ci, v, None, 0, 0)
         v[v == 0] = 1.0  # decode treats 0.0 weights as padding
-        for kernel, sb in (("row", 0), ("group", 1), ("group", 2), ("group", 4)):
+        for kernel, sb in (("row", 0), ("group", 1), ("group", 2), ("group", 4), ("tmem", 0), ("tmem8", 0)):
             plan = sdnn.Plan(rp, ci, v, M, K, kernel=kernel, group_sb=sb)
             _, _, triples = decode(p, plan)
             assert sorted(triples) == csr_triples(p)
+
+
+def test_tmem_plan_options():
+    p = synth.config_problem("c1", N=4)
+    with pytest.raises(sdnn.SdnnError):
+        sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem", panel_rows=8)
+    with pytest.raises(sdnn.SdnnError):
+        sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem8", k_chunk=64)
+    assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem8", k_chunk=32).info()["kernel"] == 5
 
 
 def test_plan_deterministic():

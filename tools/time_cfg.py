@@ -1,0 +1,45 @@
+"""Time one configuration with one kernel (CUDA events, mean of --iters launches after warm-up).
+usage: python tools/time_cfg.py --config c5 --kernel tmem [--n N] [--iters 5]"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2101_07948_b200 as sdnn  # noqa: E402
+import sdnn_synth as synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--kernel", default="tmem")
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--iters", type=int, default=5)
+    a = ap.parse_args()
+    p = synth.config_problem(a.config)
+    N = a.n or p.N
+    X = torch.randn((p.K, N), device="cuda")
+    b = torch.from_numpy(p.bias).cuda()
+    Y = torch.empty((p.M, N), device="cuda")
+    for k in a.kernel.split(","):
+        h = sdnn.Handle.from_problem(p, kernel=k)
+        for _ in range(2):
+            h.spmm(X, b, act=1, out=Y)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.iters):
+            h.spmm(X, b, act=1, out=Y)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.iters
+        print(f"{a.config} N={N} {k:8s} dbg={os.environ.get('SDNN_DEBUG_TMEM', '0')} {ms:9.3f} ms "
+              f"{2 * p.nnz * N / ms / 1e9:8.2f} TF", flush=True)
+        h.close()
+
+
+if __name__ == "__main__":
+    main()
