@@ -375,7 +375,7 @@ def main(argv=None):
     ap.add_argument("--n-total", type=int, default=synth.CONFIGS[WORKLOAD][2])
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--allgather", action="store_true")
-    ap.add_argument("--kernel", choices=["auto", "row", "group", "codegen"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "row", "group", "codegen", "tmem", "tmem8"], default="auto")
     ap.add_argument("--group-sb", type=int, default=0, choices=[0, 1, 2, 4])
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -425,6 +425,8 @@ template <> struct TmemLd<8> {
 // with LDS.128 and write TMEM with tcgen05.st.32x32b.x16 (~216 B/clk/SM), filler 0 lane 0 also
 // issues the TMA and metadata copies.
 template <int FILL> __host__ __device__ constexpr int tmem_side_warps() { return FILL ? 4 : 1; }
+// FILL 2: odd pieces of a chunk by tcgen05.cp (issued by filler 0 lane 0), even pieces by the four
+// filler warps with tcgen05.st — the two fill paths run side by side.
 template <int V, int FILL>
 __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 32, 1)
     spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
@@ -473,7 +475,7 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
   tc_fence_after();
   const uint32_t tbase = *tbase_s;
 
-  if (FILL == 1 && warp >= kTmemConsumers) {  // fillers: TMA → smem ring → LDS.128 → tcgen05.st → TMEM half
+  if (FILL >= 1 && warp >= kTmemConsumers) {  // fillers: TMA → smem ring → LDS.128 → tcgen05.st → TMEM half
     const int q = warp & 3;  // warps 16..19 → lane quarters 0..3
     const uint32_t tq = tbase + (uint32_t(q * 32) << 16);
     const bool leader = warp == kTmemConsumers && lane == 0;
@@ -511,22 +513,35 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
       }
       for (int pc = 0; pc < PPC; ++pc) {
         const int i = j * PPC + pc, s = i % S;
-        mbar_wait(&slot_full[s], (i / S) & 1);
-        const float4* src = reinterpret_cast<const float4*>(xring + size_t(s) * kTmemPieceBytes) + q * 32 + lane;
-        // all PK·V/4 LDS.128 of the piece first (latency overlapped), then the tcgen05.st.x16s
-        constexpr int NST = PK * V / 16;
-        float4 v[NST][4];
+        if (FILL == 2 && (pc & 1)) {  // this piece goes through the tcgen05.cp engine
+          if (leader) {
+            mbar_wait(&slot_full[s], (i / S) & 1);
+            const uint32_t src = smem_u32(xring + size_t(s) * kTmemPieceBytes);
 #pragma unroll
-        for (int u = 0; u < NST; ++u)
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int kk = u * (16 / V);
-            v[u][t] = V == 4 ? src[(kk + t) * (TN / 4)] : src[(kk + (t >> 1)) * (TN / 4) + (t & 1) * 128];
+            for (int kk = 0; kk < PK; kk += 8 / V)
+              tc_cp_128x256b(tbase + uint32_t(h * 256 + (pc * PK + kk) * V), cp_desc(src + uint32_t(kk * TN) * 4));
+            tc_commit(&slot_empty[s]);
+          } else if (lane == 0) {
+            mbar_arrive(&slot_empty[s]);
           }
+        } else {
+          mbar_wait(&slot_full[s], (i / S) & 1);
+          const float4* src = reinterpret_cast<const float4*>(xring + size_t(s) * kTmemPieceBytes) + q * 32 + lane;
+          // all PK·V/4 LDS.128 of the piece first (latency overlapped), then the tcgen05.st.x16s
+          constexpr int NST = PK * V / 16;
+          float4 v[NST][4];
 #pragma unroll
-        for (int u = 0; u < NST; ++u) tmem_st16(tq + uint32_t(h * 256 + (pc * PK + u * (16 / V)) * V), v[u]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&slot_empty[s]);
+          for (int u = 0; u < NST; ++u)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int kk = u * (16 / V);
+              v[u][t] = V == 4 ? src[(kk + t) * (TN / 4)] : src[(kk + (t >> 1)) * (TN / 4) + (t & 1) * 128];
+            }
+#pragma unroll
+          for (int u = 0; u < NST; ++u) tmem_st16(tq + uint32_t(h * 256 + (pc * PK + u * (16 / V)) * V), v[u]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slot_empty[s]);
+        }
         if (leader && i + S < total) {
           mbar_wait(&slot_empty[s], (i / S) & 1);
           load_piece(i + S);
@@ -535,7 +550,8 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tfull[h]);
+      if (FILL == 2 && leader) tc_commit(&tfull[h]);  // also covers this thread's tcgen05.cp of the chunk
+      else if (lane == 0) mbar_arrive(&tfull[h]);
     }
   } else if (warp == kTmemConsumers) {  // producer: TMA → smem ring → tcgen05.cp → TMEM half
     if (lane == 0) {
@@ -765,12 +781,19 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(int(cr)));
   const size_t smem = tmem_smem_bytes(p.m_stage_bytes);
   if (smem > size_t(kSmemBudget) + 1024) return fail(SDNN_ERR_INTERNAL, "TMEM kernel stage does not fit shared memory");
-  const int fill = pl.tmem_fill;
+  static const int fill_env = [] {
+    const char* e = getenv("SDNN_TMEM_FILL");
+    return e ? atoi(e) : -1;
+  }();
+  const int fill = fill_env >= 0 ? fill_env : pl.tmem_fill;
   const unsigned threads = unsigned(kTmemConsumers + (fill ? 4 : 1)) * 32;
-  if (V == 8 && fill) spmm_tmem_kernel<8, 1><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
-  else if (V == 8) spmm_tmem_kernel<8, 0><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
-  else if (fill) spmm_tmem_kernel<4, 1><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
-  else spmm_tmem_kernel<4, 0><<<unsigned(nblocks), threads, smem, stream>>>(tmap, p);
+  const unsigned grid = unsigned(nblocks);
+  if (V == 8 && fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (V == 8 && fill == 1) spmm_tmem_kernel<8, 1><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (V == 8) spmm_tmem_kernel<8, 0><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (fill == 2) spmm_tmem_kernel<4, 2><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (fill == 1) spmm_tmem_kernel<4, 1><<<grid, threads, smem, stream>>>(tmap, p);
+  else spmm_tmem_kernel<4, 0><<<grid, threads, smem, stream>>>(tmap, p);
   SDNN_CUDA_TRY(cudaGetLastError());
   return SDNN_OK;
 }
@@ -935,6 +958,10 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
   });
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     cudaFree(h->d_meta);
