@@ -75,6 +75,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Same, but each try_wait may suspend the thread until the phase completes (time hint in ns), so a
+// warp that waits long (a filler ahead of the consumers) does not spin on issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, 1000000;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -100,7 +111,8 @@ struct KParams {
   int32_t K, nch, kc, wc, nrb, stages;
   int32_t x_stage_bytes, m_stage_bytes, hdr_bytes;
   int32_t act;
-  int32_t dbg;  // TMEM kernels, diagnostics only (SDNN_DEBUG_TMEM): bit 0 skip the X loads, bit 1 skip the FMAs
+  int32_t dbg;  // TMEM kernels, diagnostics only (SDNN_DEBUG_TMEM): bit 0 skip the X loads, bit 1 skip the FMAs,
+               // bit 2 skip the smem → TMEM fill
 };
 
 // Consume one chunk: for each of the warp's RW rows, every (col, w) entry of the chunk:
@@ -417,6 +429,99 @@ template <> struct TmemLd<8> {
   }
 };
 
+// Consumer warp of TMEM lane quarter Q, warp slot wi: the chunk loop (wait for the chunk's
+// metadata and TMEM half, 4 / 2 nonzeros per step: tcgen05.ld → FFMA2) and the fused epilogue.
+template <int V, int Q>
+__device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, uint64_t* mfull, uint64_t* mempty,
+                                             uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0, int wi, int lane) {
+  constexpr int RW = tmem_rows(V);
+  constexpr int MS = kTmemMetaSlots;
+  constexpr int G = V / 4;
+  constexpr int U = tmem_pad(V);
+  constexpr int D = 1;  // groups per step (2 measured slower: profiles/r01_tmem_fill_diag.log)
+constexpr int q = Q;
+constexpr uint32_t tl = uint32_t(Q * 32) << 16;
+  float2 acc[RW][2 * G];
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int c = 0; c < 2 * G; ++c) acc[r][c] = make_float2(0.f, 0.f);
+  for (int j = 0; j < p.nch; ++j) {
+    const int h = j & 1, m = j % MS;
+    mbar_wait(&mfull[m], (j / MS) & 1);
+    mbar_wait(&tfull[h], (j >> 1) & 1);
+    tc_fence_after();
+    const uint8_t* ms = mring + size_t(m) * p.m_stage_bytes;
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + wi * RW;
+    const float4* ent = reinterpret_cast<const float4*>(ms + p.hdr_bytes);
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const uint32_t hh = hdr[r];
+      const int cnt = int(hh & 0xffffu);
+      const float4* e = ent + (hh >> 16) / 2;
+      if (p.dbg & 2) continue;
+      // D groups of U nonzeros (zero-padded to U) per step: up to D·U TMEM loads in flight, then the
+      // FFMA2s in ascending column order; the second group only if the row has it
+      for (int i = 0; i < cnt; i += D * U) {
+        float4 ee[D][U / 2];
+        float4 x[D][U][G];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          if (d == 0 || i + d * U < cnt) {
+#pragma unroll
+            for (int t = 0; t < U / 2; ++t) ee[d][t] = e[((i + d * U) >> 1) + t];
+#pragma unroll
+            for (int t = 0; t < U / 2; ++t) {
+              TmemLd<V>::ld(tl + __float_as_uint(ee[d][t].x), x[d][2 * t]);
+              TmemLd<V>::ld(tl + __float_as_uint(ee[d][t].z), x[d][2 * t + 1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          if (d == 0 || i + d * U < cnt) {
+            if constexpr (U == 4 && G == 1) tmem_wait_ld(x[d][0][0], x[d][1][0], x[d][2][0], x[d][3][0]);
+            else tmem_wait_ld(x[d][0][0], x[d][0][1], x[d][1][0], x[d][1][1]);
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+              const float w = (t & 1) ? ee[d][t >> 1].w : ee[d][t >> 1].y;
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                float2 (&a)[2] = *reinterpret_cast<float2(*)[2]>(&acc[r][2 * g]);
+                fma4(a, w, x[d][t][g]);
+              }
+            }
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&tfree[h]);
+      mbar_arrive(&mempty[m]);
+    }
+  }
+  // epilogue: row panel rb·4 + wi; lane columns n0 + 128q + 4·lane (+ 512 for the second group)
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int32_t orow = p.row_orig[(rb * kTmemPanels + wi) * RW + r];
+    if (orow < 0) continue;
+    const float b = p.bias ? p.bias[orow] : 0.f;
+    float* yrow = p.Y + int64_t(orow) * p.N;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t n = n0 + g * 512 + q * 128 + lane * 4;
+      float v[4] = {acc[r][2 * g].x + b, acc[r][2 * g].y + b, acc[r][2 * g + 1].x + b, acc[r][2 * g + 1].y + b};
+      if (p.act == SDNN_ACT_RELU) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v[t] = v[t] > 0.f ? v[t] : 0.f;
+      }
+      if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
+    }
+  }
+}
+
 // V = 4: TMEM lane L ↔ columns n0 + 4L + {0..3}; V = 8: also n0 + 512 + 4L + {0..3} (TMEM columns
 // 8k + 4..7), so both halves of a lane's data come from contiguous 2 KB runs of an X row and the
 // epilogue stores two coalesced float4 per row.
@@ -431,14 +536,12 @@ template <int V, int FILL>
 __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 32, 1)
     spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int RW = tmem_rows(V);
   constexpr int TN = 128 * V;
   constexpr int KC = tmem_kc(V);
   constexpr int PK = 8192 / TN;  // K rows per 32 KB piece
   constexpr int PPC = KC / PK;   // pieces per K chunk
   constexpr int S = kTmemPieces, MS = kTmemMetaSlots;
   constexpr int G = V / 4;       // float4 groups per lane
-  constexpr int U = tmem_pad(V); // nonzeros per unrolled step (row segments are padded to U)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = blockIdx.x % p.nrb;
   const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
@@ -524,6 +627,10 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
           } else if (lane == 0) {
             mbar_arrive(&slot_empty[s]);
           }
+        } else if (p.dbg & 4) {  // diagnostics: no fill at all (TMEM keeps stale data)
+          mbar_wait(&slot_full[s], (i / S) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slot_empty[s]);
         } else {
           mbar_wait(&slot_full[s], (i / S) & 1);
           const float4* src = reinterpret_cast<const float4*>(xring + size_t(s) * kTmemPieceBytes) + q * 32 + lane;
@@ -597,74 +704,15 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
       }
     }
   } else {
-    const int q = warp & 3, wi = warp >> 2;
-    const uint32_t tl = tbase + (uint32_t(q * 32) << 16);
-    float2 acc[RW][2 * G];
-#pragma unroll
-    for (int r = 0; r < RW; ++r)
-#pragma unroll
-      for (int c = 0; c < 2 * G; ++c) acc[r][c] = make_float2(0.f, 0.f);
-    for (int j = 0; j < p.nch; ++j) {
-      const int h = j & 1, m = j % MS;
-      mbar_wait(&mfull[m], (j / MS) & 1);
-      mbar_wait(&tfull[h], (j >> 1) & 1);
-      tc_fence_after();
-      const uint8_t* ms = mring + size_t(m) * p.m_stage_bytes;
-      const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + wi * RW;
-      const float4* ent = reinterpret_cast<const float4*>(ms + p.hdr_bytes);
-#pragma unroll
-      for (int r = 0; r < RW; ++r) {
-        const uint32_t hh = hdr[r];
-        const int cnt = int(hh & 0xffffu);
-        const float4* e = ent + (hh >> 16) / 2;
-        if (p.dbg & 2) continue;
-        for (int i = 0; i < cnt; i += U) {  // U nonzeros (zero-padded): U TMEM loads, then the FFMA2s
-          float4 ee[U / 2];
-#pragma unroll
-          for (int t = 0; t < U / 2; ++t) ee[t] = e[(i >> 1) + t];
-          float4 x[U][G];
-#pragma unroll
-          for (int t = 0; t < U / 2; ++t) {
-            TmemLd<V>::ld(tl + __float_as_uint(ee[t].x), x[2 * t]);
-            TmemLd<V>::ld(tl + __float_as_uint(ee[t].z), x[2 * t + 1]);
-          }
-          if constexpr (U == 4 && G == 1) tmem_wait_ld(x[0][0], x[1][0], x[2][0], x[3][0]);
-          else tmem_wait_ld(x[0][0], x[0][1], x[1][0], x[1][1]);
-#pragma unroll
-          for (int t = 0; t < U; ++t) {
-            const float w = (t & 1) ? ee[t >> 1].w : ee[t >> 1].y;
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-              float2 (&a)[2] = *reinterpret_cast<float2(*)[2]>(&acc[r][2 * g]);
-              fma4(a, w, x[t][g]);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&tfree[h]);
-        mbar_arrive(&mempty[m]);
-      }
-    }
-    // epilogue: row panel rb·4 + wi; lane columns n0 + 128q + 4·lane (+ 512 for the second group)
-#pragma unroll
-    for (int r = 0; r < RW; ++r) {
-      const int32_t orow = p.row_orig[(rb * kTmemPanels + wi) * RW + r];
-      if (orow < 0) continue;
-      const float b = p.bias ? p.bias[orow] : 0.f;
-      float* yrow = p.Y + int64_t(orow) * p.N;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int64_t n = n0 + g * 512 + q * 128 + lane * 4;
-        float v[4] = {acc[r][2 * g].x + b, acc[r][2 * g].y + b, acc[r][2 * g + 1].x + b, acc[r][2 * g + 1].y + b};
-        if (p.act == SDNN_ACT_RELU) {
-#pragma unroll
-          for (int t = 0; t < 4; ++t) v[t] = v[t] > 0.f ? v[t] : 0.f;
-        }
-        if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
-      }
+    // one code copy per TMEM lane quarter: the quarter's lane base (q·32 << 16) is a compile-time
+    // constant of the TMEM address (the 512-column allocation starts at lane 0, column 0)
+    if (tbase != 0) __trap();
+    const int wi = warp >> 2;
+    switch (warp & 3) {
+      case 0: tmem_consume<V, 0>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
+      case 1: tmem_consume<V, 1>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
+      case 2: tmem_consume<V, 2>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
+      default: tmem_consume<V, 3>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
     }
   }
   tc_fence_before();
