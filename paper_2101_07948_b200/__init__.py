@@ -237,7 +237,10 @@ class Handle:
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.sdnn_destroy(self._h)
+            try:
+                _lib.sdnn_destroy(self._h)
+            except (AttributeError, TypeError):  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
     def __del__(self):

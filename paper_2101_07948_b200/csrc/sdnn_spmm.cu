@@ -31,6 +31,17 @@ void plan_fill_info(const Plan& p, int32_t device, sdnn_info* info);
 }
 using namespace sdnn;
 
+// Persistent state of the host-buffer entry point: 3 streams (H2D, kernel, D2H), their events and
+// two device X/Y column-block buffers.
+struct HostStage {
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[3][2] = {};
+  float* x[2] = {nullptr, nullptr};
+  float* y[2] = {nullptr, nullptr};
+  float* bias = nullptr;
+  int64_t cols = 0;
+};
+
 struct sdnn_handle_s {
   Plan plan;            // host copy (meta cleared after upload to save memory)
   int32_t device = -1;
@@ -49,6 +60,8 @@ struct sdnn_handle_s {
   // the call fits its fast path and fills at least one wave of CTAs (tmem_worth)
   sdnn_handle_s* alt = nullptr;
   int32_t sms = 148;
+  HostStage hs;         // sdnn_spmm_host staging (created on first use)
+  std::mutex host_mu;
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -1091,6 +1104,20 @@ sdnn_status sdnn_destroy(sdnn_handle h) {
   int cur = -1;
   cudaGetDevice(&cur);
   if (cur != h->device) cudaSetDevice(h->device);
+  {
+    HostStage& hs = h->hs;
+    for (int i = 0; i < 3; ++i) {
+      if (hs.s[i]) cudaStreamSynchronize(hs.s[i]);
+      for (int b = 0; b < 2; ++b)
+        if (hs.ev[i][b]) cudaEventDestroy(hs.ev[i][b]);
+      if (hs.s[i]) cudaStreamDestroy(hs.s[i]);
+    }
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(hs.x[b]);
+      cudaFree(hs.y[b]);
+    }
+    cudaFree(hs.bias);
+  }
   cudaFree(h->d_meta);
   cudaFree(h->d_blk_off);
   cudaFree(h->d_row_orig);
@@ -1132,15 +1159,14 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
   if (st != SDNN_OK) return st;
   const int64_t M = h->plan.M, K = h->plan.K;
   int64_t nc = block_cols;
-  if (nc == 0) {  // ~128 MiB of X+Y per block, multiple of 256 columns
-    nc = std::max<int64_t>(256, (int64_t(128) << 20) / ((M + K) * 4) / 256 * 256);
+  if (nc == 0) {  // ~128 MiB of X+Y per block, multiple of 512 columns (a TMEM N tile)
+    nc = std::max<int64_t>(512, (int64_t(128) << 20) / ((M + K) * 4) / 512 * 512);
   }
   nc = std::min(nc, N);
-  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev[3][2] = {};
-  float* xd[2] = {nullptr, nullptr};
-  float* yd[2] = {nullptr, nullptr};
-  float* bd = nullptr;
+  // The staging state (streams, events, two X/Y block buffers, bias) lives in the handle and is
+  // reused by every call; calls on one handle are serialised on its mutex.
+  std::lock_guard<std::mutex> lk(h->host_mu);
+  HostStage& hs = h->hs;
   sdnn_status rs = SDNN_OK;
   std::string msg;
   auto ck = [&](cudaError_t e, const char* what) {
@@ -1150,60 +1176,64 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
     }
     return rs == SDNN_OK;
   };
-  for (int i = 0; i < 3 && rs == SDNN_OK; ++i) {
-    ck(cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking), "cudaStreamCreate");
-    for (int b = 0; b < 2 && rs == SDNN_OK; ++b) ck(cudaEventCreateWithFlags(&ev[i][b], cudaEventDisableTiming), "cudaEventCreate");
+  if (!hs.s[0]) {
+    for (int i = 0; i < 3 && rs == SDNN_OK; ++i) {
+      ck(cudaStreamCreateWithFlags(&hs.s[i], cudaStreamNonBlocking), "cudaStreamCreate");
+      for (int b = 0; b < 2 && rs == SDNN_OK; ++b)
+        ck(cudaEventCreateWithFlags(&hs.ev[i][b], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    if (rs == SDNN_OK) ck(cudaMalloc(reinterpret_cast<void**>(&hs.bias), size_t(M * 4)), "cudaMalloc(bias)");
   }
-  for (int b = 0; b < 2 && rs == SDNN_OK; ++b) {
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&xd[b]), size_t(K * nc * 4), s[1]), "cudaMallocAsync");
-    if (rs == SDNN_OK) ck(cudaMallocAsync(reinterpret_cast<void**>(&yd[b]), size_t(M * nc * 4), s[1]), "cudaMallocAsync");
+  if (rs == SDNN_OK && hs.cols < nc) {
+    ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(hs.x[b]);
+      cudaFree(hs.y[b]);
+      hs.x[b] = hs.y[b] = nullptr;
+    }
+    hs.cols = 0;
+    for (int b = 0; b < 2 && rs == SDNN_OK; ++b) {
+      ck(cudaMalloc(reinterpret_cast<void**>(&hs.x[b]), size_t(K * nc * 4)), "cudaMalloc(X block)");
+      if (rs == SDNN_OK) ck(cudaMalloc(reinterpret_cast<void**>(&hs.y[b]), size_t(M * nc * 4)), "cudaMalloc(Y block)");
+    }
+    if (rs == SDNN_OK) hs.cols = nc;
   }
+  cudaStream_t* s = hs.s;
+  const float* bd = nullptr;
   if (rs == SDNN_OK && bias_host) {
-    if (ck(cudaMallocAsync(reinterpret_cast<void**>(&bd), size_t(M * 4), s[1]), "cudaMallocAsync"))
-      ck(cudaMemcpyAsync(bd, bias_host, size_t(M * 4), cudaMemcpyHostToDevice, s[1]), "cudaMemcpyAsync(bias)");
+    ck(cudaMemcpyAsync(hs.bias, bias_host, size_t(M * 4), cudaMemcpyHostToDevice, s[1]), "cudaMemcpyAsync(bias)");
+    bd = hs.bias;
   }
   if (rs == SDNN_OK) {
     // s[0]: H2D copies, s[1]: kernels, s[2]: D2H copies.  ev[0][b]: X block in buffer b ready;
     // ev[1][b]: kernel on buffer b done; ev[2][b]: Y buffer b drained to host.
-    ck(cudaEventRecord(ev[1][0], s[1]), "cudaEventRecord");
-    ck(cudaEventRecord(ev[1][1], s[1]), "cudaEventRecord");
-    ck(cudaEventRecord(ev[2][0], s[1]), "cudaEventRecord");
-    ck(cudaEventRecord(ev[2][1], s[1]), "cudaEventRecord");
+    for (int b = 0; b < 2; ++b) {
+      ck(cudaEventRecord(hs.ev[1][b], s[1]), "cudaEventRecord");
+      ck(cudaEventRecord(hs.ev[2][b], s[1]), "cudaEventRecord");
+    }
     int i = 0;
     for (int64_t c0 = 0; c0 < N && rs == SDNN_OK; c0 += nc, ++i) {
       const int b = i & 1;
       const int64_t w = std::min(nc, N - c0);
-      ck(cudaStreamWaitEvent(s[0], ev[1][b], 0), "cudaStreamWaitEvent");
-      ck(cudaMemcpy2DAsync(xd[b], size_t(w * 4), X_host + c0, size_t(N * 4), size_t(w * 4), size_t(K),
+      ck(cudaStreamWaitEvent(s[0], hs.ev[1][b], 0), "cudaStreamWaitEvent");
+      ck(cudaMemcpy2DAsync(hs.x[b], size_t(w * 4), X_host + c0, size_t(N * 4), size_t(w * 4), size_t(K),
                            cudaMemcpyHostToDevice, s[0]), "cudaMemcpy2DAsync(X)");
-      ck(cudaEventRecord(ev[0][b], s[0]), "cudaEventRecord");
-      ck(cudaStreamWaitEvent(s[1], ev[0][b], 0), "cudaStreamWaitEvent");
-      ck(cudaStreamWaitEvent(s[1], ev[2][b], 0), "cudaStreamWaitEvent");
+      ck(cudaEventRecord(hs.ev[0][b], s[0]), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(s[1], hs.ev[0][b], 0), "cudaStreamWaitEvent");
+      ck(cudaStreamWaitEvent(s[1], hs.ev[2][b], 0), "cudaStreamWaitEvent");
       if (rs == SDNN_OK) {
-        sdnn_status ls = launch(h, xd[b], w, bd, act, yd[b], s[1]);
+        sdnn_status ls = launch(h, hs.x[b], w, bd, act, hs.y[b], s[1]);
         if (ls != SDNN_OK) { rs = ls; msg = sdnn_last_error_message(); }
       }
-      ck(cudaEventRecord(ev[1][b], s[1]), "cudaEventRecord");
-      ck(cudaStreamWaitEvent(s[2], ev[1][b], 0), "cudaStreamWaitEvent");
-      ck(cudaMemcpy2DAsync(Y_host + c0, size_t(N * 4), yd[b], size_t(w * 4), size_t(w * 4), size_t(M),
+      ck(cudaEventRecord(hs.ev[1][b], s[1]), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(s[2], hs.ev[1][b], 0), "cudaStreamWaitEvent");
+      ck(cudaMemcpy2DAsync(Y_host + c0, size_t(N * 4), hs.y[b], size_t(w * 4), size_t(w * 4), size_t(M),
                            cudaMemcpyDeviceToHost, s[2]), "cudaMemcpy2DAsync(Y)");
-      ck(cudaEventRecord(ev[2][b], s[2]), "cudaEventRecord");
+      ck(cudaEventRecord(hs.ev[2][b], s[2]), "cudaEventRecord");
     }
   }
-  // drain everything before freeing
   for (int i = 0; i < 3; ++i)
     if (s[i]) ck(cudaStreamSynchronize(s[i]), "cudaStreamSynchronize");
-  for (int b = 0; b < 2; ++b) {
-    if (xd[b]) cudaFreeAsync(xd[b], s[1]);
-    if (yd[b]) cudaFreeAsync(yd[b], s[1]);
-  }
-  if (bd) cudaFreeAsync(bd, s[1]);
-  if (s[1]) cudaStreamSynchronize(s[1]);
-  for (int i = 0; i < 3; ++i) {
-    for (int b = 0; b < 2; ++b)
-      if (ev[i][b]) cudaEventDestroy(ev[i][b]);
-    if (s[i]) cudaStreamDestroy(s[i]);
-  }
   if (rs != SDNN_OK) return fail(rs, msg);
   return SDNN_OK;
 }
