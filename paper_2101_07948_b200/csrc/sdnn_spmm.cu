@@ -859,10 +859,12 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   return SDNN_OK;
 }
 
-// The TMEM kernel runs one CTA per SM: it pays when the call fills at least one wave.
+// The TMEM kernel runs one CTA per SM and pays once the call has at least a third of a wave of
+// CTAs (measured per config, profiles/r01_configs_v3.jsonl: it wins from ~50 CTAs up, the row
+// kernel's smaller tiles win on the tiny ones).
 static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const float* Y) {
   return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 &&
-         int64_t(a->plan.num_row_blocks) * ((N + 128 * tmem_v(a->plan.kernel) - 1) / (128 * tmem_v(a->plan.kernel))) >=
+         3 * int64_t(a->plan.num_row_blocks) * ((N + 128 * tmem_v(a->plan.kernel) - 1) / (128 * tmem_v(a->plan.kernel))) >=
              a->sms;
 }
 

@@ -3,7 +3,10 @@ variant, median of `--iters` launches bracketed by CUDA events, L2 flushed befor
 (memset of a 2×L2 scratch buffer outside the events).  Prints one JSON line per (config, variant)
 with effective GFLOP/s, algorithmic GB/s and the fraction of the fp32 / HBM roofline.
 
-usage: python tools/bench_configs.py [--configs c1,c2_768x768,...] [--variants auto,row,group1,group2,group4]
+Also (--graph) the warm per-launch time: a CUDA graph of 50 back-to-back launches, replayed, time / 50
+(the SURVEY §8(d) "warm" protocol; small configs then stay L2-resident and launch overhead is amortised).
+
+usage: python tools/bench_configs.py [--configs c1,c2_768x768,...] [--variants auto,row,tmem,tmem8,group2] [--graph]
 """
 import argparse
 import json
@@ -27,6 +30,7 @@ def main():
     ap.add_argument("--variants", default="auto,row,group1,group2,group4")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warm", action="store_true", help="no L2 flush (L2-resident timing)")
+    ap.add_argument("--graph", action="store_true", help="also time a CUDA graph of 50 launches")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     props = torch.cuda.get_device_properties(dev)
@@ -58,12 +62,33 @@ def main():
                 if i >= 3:
                     ts.append(e0.elapsed_time(e1) * 1e-3)
             t = statistics.median(ts)
-            print(json.dumps({"config": key, "variant": var, "kernel": info["kernel"], "sb": info["group_sb"],
+            graph_us = None
+            if args.graph:
+                s_ = torch.cuda.Stream()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s_):
+                    for _ in range(50):
+                        h.spmm(X, b, act=1, out=Y)
+                g.replay()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                graph_us = e0.elapsed_time(e1) * 1e3 / 50
+                del g
+            kid = h.kernel_for(p.N, X.data_ptr(), Y.data_ptr())
+            print(json.dumps({"config": key, "variant": var, "kernel": info["kernel"], "launched": kid, "sb": info["group_sb"],
                               "M": p.M, "K": p.K, "N": p.N, "nnz": p.nnz, "us": round(t * 1e6, 2),
                               "gflops": round(flops / t / 1e9, 1), "gbs": round(alg_bytes / t / 1e9, 1),
                               "fp32_frac": round(flops / t / fp32_peak, 4), "hbm_frac": round(alg_bytes / t / hbm_peak, 4),
                               "roof_frac": round(max(flops / fp32_peak, alg_bytes / hbm_peak) / t, 4),
-                              "l2": "warm" if args.warm else "flushed"}), flush=True)
+                              "l2": "warm" if args.warm else "flushed",
+                              **({} if graph_us is None else {
+                                  "graph_us": round(graph_us, 2), "graph_gflops": round(flops / graph_us / 1e3, 1),
+                                  "graph_roof_frac": round(max(flops / fp32_peak, alg_bytes / hbm_peak) / (graph_us * 1e-6), 4)})}),
+                  flush=True)
             h.close()
 
 
