@@ -238,7 +238,7 @@ def test_auto_takes_tmem_plan_when_it_fills_a_wave(sdnn):
     Xs = np.ascontiguousarray(X[:, :100])  # ragged: the row plan
     Ya, _ = run_gpu(sdnn, p, Xs, p.bias, 1, handle=h)
     np.testing.assert_array_equal(Ya, Yr[:, :100])
-    assert h.kernel_for(p.N) == 4 and h.kernel_for(100) == -1 and h.kernel_for(128) == 1  # 32·1·3 < 148
+    assert h.kernel_for(p.N) == 4 and h.kernel_for(102) == -1 and h.kernel_for(128) == 1  # 32·1·3 < 148
 
 
 def test_get_permutation_and_info(sdnn, oracle_mod):
