@@ -126,29 +126,45 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
         // chunk's TMEM half (V·col_local + 256·(j mod 2)), and every row segment is padded to a
         // multiple of tmem_pad(V) entries with zero weights (the count in the header includes the
         // padding) so the kernel runs one unrolled loop body per row; the padding adds 0·X (X finite).
+        // V = 4 also counts leading runs: while a row segment starts with aligned 1×4 runs (four
+        // nonzeros at columns k..k+3, k % 4 == 0 — the blocks of a block-clustered mask), their
+        // number goes into header bits 8..15 so the kernel fetches each run's four X row slices with
+        // one tcgen05.ld.x16 in a loop of its own; later runs are ordinary entries (ascending column
+        // order is kept).  The count field is then bits 0..7 (a segment has at most 64 + 3 entries).
         const int64_t hdr = align_up(int64_t(rcta) * 4, 16);
         const uint32_t half = uint32_t(j & 1) * 256u;
         int32_t e = 0;
         for (int32_t s = 0; s < rcta; ++s) {
           const int32_t orow = row_orig[size_t(b) * rcta + s];
-          int32_t c = 0;
+          int32_t c = 0, runs = 0;
+          bool leading = true;
+          auto put = [&](uint32_t cl, float w) {
+            if (blk) {
+              std::memcpy(blk + hdr + size_t(e + c) * 8, &cl, 4);
+              std::memcpy(blk + hdr + size_t(e + c) * 8 + 4, &w, 4);
+            }
+            ++c;
+          };
           if (orow >= 0) {
             int32_t& p = cur[s];
-            while (p < csr_ptr[orow + 1] && col_idx[p] < hi) {
-              if (blk) {
-                const uint32_t cl = g.tmem ? uint32_t(col_idx[p] - lo) * uint32_t(g.tmem) + half : uint32_t(col_idx[p] - lo);
-                std::memcpy(blk + hdr + size_t(e + c) * 8, &cl, 4);
-                std::memcpy(blk + hdr + size_t(e + c) * 8 + 4, &vals[p], 4);
+            const int32_t end = csr_ptr[orow + 1];
+            while (p < end && col_idx[p] < hi) {
+              const int32_t col = col_idx[p];
+              if (g.tmem == 4 && leading && col % 4 == 0 && p + 3 < end && col_idx[p + 3] == col + 3 &&
+                  col + 3 < hi) {
+                for (int32_t t = 0; t < 4; ++t) put(uint32_t(col + t - lo) * 4u + half, vals[p + t]);
+                p += 4;
+                ++runs;
+                continue;
               }
-              ++c;
+              leading = false;
+              put(g.tmem ? uint32_t(col - lo) * uint32_t(g.tmem) + half : uint32_t(col - lo), vals[p]);
               ++p;
             }
           }
           const int32_t cpad = g.tmem ? int32_t(align_up(c, tmem_pad(g.tmem))) : c;
-          if (blk) {
-            for (int32_t t = c; t < cpad; ++t) std::memcpy(blk + hdr + size_t(e + t) * 8, &half, 4);
-            reinterpret_cast<uint32_t*>(blk)[s] = (uint32_t(e) << 16) | uint32_t(cpad);
-          }
+          while (c < cpad) put(half, 0.f);
+          if (blk) reinterpret_cast<uint32_t*>(blk)[s] = (uint32_t(e) << 16) | (uint32_t(runs) << 8) | uint32_t(cpad);
           e += int32_t(align_up(cpad, 2));
         }
         ent_total += e;

@@ -142,7 +142,7 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
     const uint32_t h = hdr[r];
-    const int cnt = int(h & 0xffffu);
+    const int cnt = int(TF ? (h & 0xffu) : (h & 0xffffu));  // TMEM format: bits 8..15 count leading runs
     const float4* e = ent + (h >> 16) / 2;
     for (int i = 0; i < cnt; i += 2) {
       const float4 ee = e[i >> 1];
@@ -429,6 +429,14 @@ constexpr size_t tmem_smem_bytes(int m_stage_bytes) {
   return size_t(kTmemPieces) * kTmemPieceBytes + size_t(kTmemMetaSlots) * m_stage_bytes + 16 * 8 + 16;
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float4& a, float4& b, float4& c, float4& d) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+      "[%16];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w), "=f"(c.x), "=f"(c.y),
+        "=f"(c.z), "=f"(c.w), "=f"(d.x), "=f"(d.y), "=f"(d.z), "=f"(d.w)
+      : "r"(taddr));
+}
 template <int V> struct TmemLd;
 template <> struct TmemLd<4> {
   static __device__ __forceinline__ void ld(uint32_t taddr, float4 (&v)[1]) { tmem_ld4(taddr, v[0]); }
@@ -442,18 +450,17 @@ template <> struct TmemLd<8> {
   }
 };
 
-// Consumer warp of TMEM lane quarter Q, warp slot wi: the chunk loop (wait for the chunk's
+// Consumer warp of TMEM lane quarter q, warp slot wi: the chunk loop (wait for the chunk's
 // metadata and TMEM half, 4 / 2 nonzeros per step: tcgen05.ld → FFMA2) and the fused epilogue.
-template <int V, int Q>
+template <int V>
 __device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, uint64_t* mfull, uint64_t* mempty,
-                                             uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0, int wi, int lane) {
+                                             uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0, int q, int wi,
+                                             int lane) {
   constexpr int RW = tmem_rows(V);
   constexpr int MS = kTmemMetaSlots;
   constexpr int G = V / 4;
   constexpr int U = tmem_pad(V);
-  constexpr int D = 1;  // groups per step (2 measured slower: profiles/r01_tmem_fill_diag.log)
-constexpr int q = Q;
-constexpr uint32_t tl = uint32_t(Q * 32) << 16;
+  const uint32_t tl = uint32_t(q * 32) << 16;  // this warp's TMEM lane quarter (allocation at lane 0, column 0)
   float2 acc[RW][2 * G];
 #pragma unroll
   for (int r = 0; r < RW; ++r)
@@ -470,41 +477,42 @@ constexpr uint32_t tl = uint32_t(Q * 32) << 16;
 #pragma unroll
     for (int r = 0; r < RW; ++r) {
       const uint32_t hh = hdr[r];
-      const int cnt = int(hh & 0xffffu);
+      const int cnt = int(hh & 0xffu);
       const float4* e = ent + (hh >> 16) / 2;
       if (p.dbg & 2) continue;
-      // D groups of U nonzeros (zero-padded to U) per step: up to D·U TMEM loads in flight, then the
-      // FFMA2s in ascending column order; the second group only if the row has it
-      for (int i = 0; i < cnt; i += D * U) {
-        float4 ee[D][U / 2];
-        float4 x[D][U][G];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          if (d == 0 || i + d * U < cnt) {
-#pragma unroll
-            for (int t = 0; t < U / 2; ++t) ee[d][t] = e[((i + d * U) >> 1) + t];
-#pragma unroll
-            for (int t = 0; t < U / 2; ++t) {
-              TmemLd<V>::ld(tl + __float_as_uint(ee[d][t].x), x[d][2 * t]);
-              TmemLd<V>::ld(tl + __float_as_uint(ee[d][t].z), x[d][2 * t + 1]);
-            }
-          }
+      int i = 0;
+      if constexpr (V == 4) {  // leading aligned 1×4 runs: one x16 load each
+        const int nrun = int((hh >> 8) & 0xffu);
+        for (; i < 4 * nrun; i += 4) {
+          const float4 e0 = e[i >> 1], e1 = e[(i >> 1) + 1];
+          float4 xa, xb, xc, xd;
+          tmem_ld16(tl + __float_as_uint(e0.x), xa, xb, xc, xd);
+          tmem_wait_ld(xa, xb, xc, xd);
+          fma4(*reinterpret_cast<float2(*)[2]>(&acc[r][0]), e0.y, xa);
+          fma4(*reinterpret_cast<float2(*)[2]>(&acc[r][0]), e0.w, xb);
+          fma4(*reinterpret_cast<float2(*)[2]>(&acc[r][0]), e1.y, xc);
+          fma4(*reinterpret_cast<float2(*)[2]>(&acc[r][0]), e1.w, xd);
         }
+      }
+      // steps of U nonzeros (zero-padded to U): U TMEM loads in flight, then the FFMA2s in
+      // ascending column order
+      for (; i < cnt; i += U) {
+        float4 ee[U / 2];
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-          if (d == 0 || i + d * U < cnt) {
-            if constexpr (U == 4 && G == 1) tmem_wait_ld(x[d][0][0], x[d][1][0], x[d][2][0], x[d][3][0]);
-            else tmem_wait_ld(x[d][0][0], x[d][0][1], x[d][1][0], x[d][1][1]);
+        for (int t = 0; t < U / 2; ++t) ee[t] = e[(i >> 1) + t];
+        float4 x[U][G];
 #pragma unroll
-            for (int t = 0; t < U; ++t) {
-              const float w = (t & 1) ? ee[d][t >> 1].w : ee[d][t >> 1].y;
+        for (int t = 0; t < U / 2; ++t) {
+          TmemLd<V>::ld(tl + __float_as_uint(ee[t].x), x[2 * t]);
+          TmemLd<V>::ld(tl + __float_as_uint(ee[t].z), x[2 * t + 1]);
+        }
+        if constexpr (U == 4 && G == 1) tmem_wait_ld(x[0][0], x[1][0], x[2][0], x[3][0]);
+        else tmem_wait_ld(x[0][0], x[0][1], x[1][0], x[1][1]);
 #pragma unroll
-              for (int g = 0; g < G; ++g) {
-                float2 (&a)[2] = *reinterpret_cast<float2(*)[2]>(&acc[r][2 * g]);
-                fma4(a, w, x[d][t][g]);
-              }
-            }
-          }
+        for (int t = 0; t < U; ++t) {
+          const float w = (t & 1) ? ee[t >> 1].w : ee[t >> 1].y;
+#pragma unroll
+          for (int g = 0; g < G; ++g) fma4(*reinterpret_cast<float2(*)[2]>(&acc[r][2 * g]), w, x[t][g]);
         }
       }
     }
@@ -717,16 +725,10 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
       }
     }
   } else {
-    // one code copy per TMEM lane quarter: the quarter's lane base (q·32 << 16) is a compile-time
-    // constant of the TMEM address (the 512-column allocation starts at lane 0, column 0)
-    if (tbase != 0) __trap();
-    const int wi = warp >> 2;
-    switch (warp & 3) {
-      case 0: tmem_consume<V, 0>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
-      case 1: tmem_consume<V, 1>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
-      case 2: tmem_consume<V, 2>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
-      default: tmem_consume<V, 3>(p, mring, mfull, mempty, tfull, tfree, rb, n0, wi, lane); break;
-    }
+    // one code copy for all four lane quarters (four specialised copies exceed the SM's
+    // instruction cache: profiles/r01_tmem_fill_diag.log)
+    if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0
+    tmem_consume<V>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp & 3, warp >> 2, lane);
   }
   tc_fence_before();
   __syncthreads();

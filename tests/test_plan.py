@@ -24,6 +24,7 @@ def decode(p, plan):
     assert np.diff(blk_off).max() <= info["max_block_bytes"]
     triples = []
     last_col = {}
+    runs = []
     for b in range(nrb):
         for j in range(nch):
             blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]]
@@ -31,6 +32,13 @@ def decode(p, plan):
             ent = blk[hdr_bytes:]
             for s in range(rcta):
                 start, cnt = int(hdr[s] >> 16), int(hdr[s] & 0xFFFF)
+                nrun = 0
+                if V:  # TMEM format: count in bits 0..7, leading aligned 1×4 runs in bits 8..15
+                    cnt, nrun = cnt & 0xFF, cnt >> 8
+                    assert V == 4 or nrun == 0
+                    assert 4 * nrun <= cnt
+                    for u in range(nrun):
+                        runs.append((b, j, start + 4 * u))
                 assert start % 2 == 0
                 orow = int(row_orig[b * rcta + s])
                 if orow < 0:
@@ -54,6 +62,11 @@ def decode(p, plan):
                     assert col > last_col.get(orow, -1)  # ascending column order per row
                     last_col[orow] = col
                     triples.append((orow, col, w))
+    for b, j, at in runs:  # a run is 4 consecutive columns k..k+3, k % 4 == 0
+        blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]]
+        cols = [int(blk[hdr_bytes + (at + t) * 8:hdr_bytes + (at + t) * 8 + 4].view(np.uint32)[0]) for t in range(4)]
+        assert cols == [cols[0] + 4 * t for t in range(4)] and (cols[0] % 256) % 16 == 0
+    decode.runs = len(runs)
     return info, row_orig, triples
 
 
@@ -185,6 +198,18 @@ def test_degenerate_shapes():
             plan = sdnn.Plan(rp, ci, v, M, K, kernel=kernel, group_sb=sb)
             _, _, triples = decode(p, plan)
             assert sorted(triples) == csr_triples(p)
+
+
+def test_tmem_runs_marked_on_block_clustered_masks():
+    """c4's 1×4 runs are counted as leading runs of their row segments (one tcgen05.ld.x16 each)."""
+    p = synth.config_problem("c4_2048x512_s95", N=4)
+    plan = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem")
+    _, _, triples = decode(p, plan)
+    assert sorted(triples) == csr_triples(p)
+    assert decode.runs == p.nnz // 4
+    p = synth.config_problem("c3_512x512", N=4)
+    decode(p, sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem"))
+    assert decode.runs < p.nnz // 500  # chance leading runs of a uniform 85 % mask
 
 
 def test_tmem_plan_options():
