@@ -80,17 +80,19 @@ constexpr int kCgPrefetch = 24;     // codegen kernel: X columns in flight per l
 
 // TMEM kernels (sdnn_spmm.cu): the X tile lives in tensor memory.  TMEM lane L holds V columns of
 // N (n0 + 4L + v and, for V = 8, n0 + 512 + 4L + v): N tile 128·V; TMEM column V·k_local + v; two
-// halves of 256 columns → K chunk 256 / V.  16 consumer warps = 4 warp slots per lane quarter, each
-// slot a panel of tmem_rows(V) rows (accumulators: rows · V registers per thread).
+// halves of 256 columns → K chunk 256 / V.  24 consumer warps = 6 warp slots per lane quarter, each
+// slot a panel of tmem_rows(V) rows (accumulators: rows · V registers per thread; 28 warps → 72
+// registers).  Slots × rows measured on c5 (profiles/r01_tmem_fill_diag.log): 4×16 53.3 ms, 5×12
+// 53.3, 6×10 51.1, 6×11 65.6 (spills), 7×8 56.9.
 #ifdef __CUDACC__
 #define SDNN_HD __host__ __device__
 #else
 #define SDNN_HD
 #endif
-SDNN_HD constexpr int tmem_rows(int V) { return V == 4 ? 16 : 8; }
+SDNN_HD constexpr int tmem_rows(int V) { return V == 4 ? 10 : 5; }
 SDNN_HD constexpr int tmem_kc(int V) { return 256 / V; }
 SDNN_HD constexpr int tmem_pad(int V) { return V == 4 ? 4 : 2; }  // row segments padded to multiples of this
-constexpr int kTmemPanels = 4;
+constexpr int kTmemPanels = 6;
 constexpr int kTmemPieces = 4;  // smem ring depth (32 KB TMA pieces)
 inline int tmem_v(int kernel) { return kernel == 5 ? 8 : 4; }
 

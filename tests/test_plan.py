@@ -16,7 +16,7 @@ def decode(p, plan):
     rw, wc, kc, nch, nrb = (info[k] for k in ("panel_rows", "cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
     V = {4: 4, 5: 8}.get(info["kernel"], 0)
     if V:
-        assert (rw, wc, kc) == ((16, 4, 64) if V == 4 else (8, 4, 32))
+        assert (rw, wc, kc) == ((10, 6, 64) if V == 4 else (5, 6, 32))
     rcta = rw * wc
     hdr_bytes = (rcta * 4 + 15) // 16 * 16
     assert blk_off[0] == 0 and blk_off[-1] == meta.size and np.all(np.diff(blk_off) > 0)
