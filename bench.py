@@ -237,8 +237,8 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
     kid = h.kernel_for(Nr, X.data_ptr(), Y.data_ptr())
     kernel_desc = {1: f"spmm_tma_kernel<row,R_w={info['panel_rows']}>", 2: "spmm_tma_kernel<group>",
                    3: f"sdnn_cg_p<0..{info['num_panels'] - 1}> (generated PTX)",
-                   4: "spmm_tmem_kernel<V=4,FILL=1> (X tile in TMEM, tcgen05.ld operands, 16-row panels)",
-                   5: "spmm_tmem_kernel<V=8,FILL=1> (X tile in TMEM, tcgen05.ld operands, 8-row panels)"
+                   4: "spmm_tmem_kernel<V=4,FILL=1> (X tile in TMEM, tcgen05.ld operands; 24 consumer warps x 10 rows)",
+                   5: "spmm_tmem_kernel<V=8,FILL=1> (X tile in TMEM, tcgen05.ld operands; 24 consumer warps x 5 rows)"
                    }.get(abs(kid), str(kid)) + (" [generic fallback]" if kid < 0 else "")
 
     def step():

@@ -911,6 +911,13 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
   if (fast) {
     int S = int(kSmemBudget / (p.x_stage_bytes + p.m_stage_bytes));
     S = std::min(S, std::min(pl.num_chunks, 4));
+    {
+      static const int s_env = [] {
+        const char* e = getenv("SDNN_ROW_STAGES");
+        return e ? atoi(e) : 0;
+      }();
+      if (s_env > 0) S = std::min(S, s_env);
+    }
     if (S < 1) return fail(SDNN_ERR_INTERNAL, "stage does not fit shared memory");
     p.stages = S;
     const size_t smem = size_t(S) * (p.x_stage_bytes + p.m_stage_bytes) + size_t(2 * S) * 8;
@@ -948,8 +955,8 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
     else if (pl.kernel == 2 && sb == 1) spmm_generic_kernel<2, 16, 4, 1><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 2 && sb == 2) spmm_generic_kernel<2, 16, 4, 2><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 2) spmm_generic_kernel<2, 16, 4, 4><<<grid, block, smem, stream>>>(p);
-    else if (pl.kernel == 4) spmm_generic_kernel<4, 16, 4><<<grid, block, smem, stream>>>(p);
-    else if (pl.kernel == 5) spmm_generic_kernel<5, 8, 4><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 4) spmm_generic_kernel<4, tmem_rows(4), 4><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 5) spmm_generic_kernel<5, tmem_rows(8), 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 8) spmm_generic_kernel<1, 8, 8><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 4) spmm_generic_kernel<1, 8, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 4 && V == 8) spmm_generic_kernel<1, 4, 8><<<grid, block, smem, stream>>>(p);
@@ -1010,10 +1017,10 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 2>();
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 4, 4>();
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_generic_kernel<4, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ae = cudaFuncSetAttribute(spmm_generic_kernel<4, tmem_rows(4), 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_generic_kernel<5, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ae = cudaFuncSetAttribute(spmm_generic_kernel<5, tmem_rows(8), 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
