@@ -6,6 +6,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("SDNN_PKG_DIR"):  # A/B runs: another build of the package (tools/jobs/ab.sh)
+    sys.path.insert(0, os.environ["SDNN_PKG_DIR"])
 
 import torch  # noqa: E402
 
@@ -36,7 +38,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
-        print(f"{a.config} N={N} {k:8s} dbg={os.environ.get('SDNN_DEBUG_TMEM', '0')} {ms:9.3f} ms "
+        print(f"{a.config} N={N} {k:8s} lib={sdnn.LIB_PATH.split('/')[-3]} dbg={os.environ.get('SDNN_DEBUG_TMEM', '0')} {ms:9.3f} ms "
               f"{2 * p.nnz * N / ms / 1e9:8.2f} TF", flush=True)
         h.close()
 
