@@ -59,7 +59,7 @@ typedef struct {
   int32_t kernel;           /* 0 = auto: the row kernel's plan (or the group kernel's, by cost model)
                                plus the TMEM kernel's plan; each sdnn_spmm call takes the TMEM
                                kernel when N % 128 == 0, X/Y are 16-byte aligned and the call has
-                               3 · row blocks · N tiles ≥ SMs, else the row plan.
+                               2 · row blocks · N tiles ≥ SMs, else the row plan.
                                1 = row kernel (each nonzero reads its X row slice from shared
                                memory), 2 = group kernel (16-row groups: one X load feeds every
                                nonzero of the group in that column), 3 = codegen (per-panel

@@ -771,6 +771,21 @@ static cudaError_t set_smem_attrs() {
                               kSmemBudget + 1024);
 }
 
+// Resident CTAs per SM for a kernel at a block size and dynamic shared memory (cached: the query
+// runs once per distinct configuration).
+static int occupancy(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(fn, smem * 4096 + size_t(threads));
+  for (const auto& kv : cache)
+    if (kv.first == key) return kv.second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) n = 1;
+  cache.emplace_back(key, n);
+  return n;
+}
+
 static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                   float* Y, cudaStream_t stream) {
   const Plan& pl = h->plan;
@@ -861,12 +876,12 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   return SDNN_OK;
 }
 
-// The TMEM kernel runs one CTA per SM and pays once the call has at least a third of a wave of
-// CTAs (measured per config, profiles/r01_configs_v3.jsonl: it wins from ~50 CTAs up, the row
-// kernel's smaller tiles win on the tiny ones).
+// The TMEM kernel runs one CTA per SM and pays once the call has at least half a wave of CTAs
+// (measured per config, profiles/r01_configs_v5.jsonl: it wins from ~100 CTAs up — c2 3072×768,
+// c3 512² — while the row kernel, several CTAs per SM, wins on c3 256×128 (65 TMEM CTAs) and below).
 static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const float* Y) {
   return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 &&
-         3 * int64_t(a->plan.num_row_blocks) * ((N + 128 * tmem_v(a->plan.kernel) - 1) / (128 * tmem_v(a->plan.kernel))) >=
+         2 * int64_t(a->plan.num_row_blocks) * ((N + 128 * tmem_v(a->plan.kernel) - 1) / (128 * tmem_v(a->plan.kernel))) >=
              a->sms;
 }
 
@@ -909,18 +924,50 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
   const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(Y) % 16 == 0) && pl.kernel < 4;
   if (fast) {
+    const int sb = pl.group_sb;
+    const void* fn = nullptr;
+    if (pl.kernel == 2 && V == 8 && sb == 1) fn = reinterpret_cast<const void*>(spmm_tma_kernel<2, 16, 8, 1>);
+    else if (pl.kernel == 2 && V == 8 && sb == 2) fn = reinterpret_cast<const void*>(spmm_tma_kernel<2, 16, 8, 2>);
+    else if (pl.kernel == 2 && V == 8) fn = reinterpret_cast<const void*>(spmm_tma_kernel<2, 16, 8, 4>);
+    else if (pl.kernel == 2 && sb == 1) fn = reinterpret_cast<const void*>(spmm_tma_kernel<2, 16, 4, 1>);
+    else if (pl.kernel == 2 && sb == 2) fn = reinterpret_cast<const void*>(spmm_tma_kernel<2, 16, 4, 2>);
+    else if (pl.kernel == 2) fn = reinterpret_cast<const void*>(spmm_tma_kernel<2, 16, 4, 4>);
+    else if (rw == 8 && V == 8) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 8, 8>);
+    else if (rw == 8 && V == 4) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 8, 4>);
+    else if (rw == 4 && V == 8) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 4, 8>);
+    else fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 4, 4>);
+    const int threads = (wc + 1) * 32;
+    auto smem_for = [&](int S) { return size_t(S) * (p.x_stage_bytes + p.m_stage_bytes) + size_t(2 * S) * 8; };
     int S = int(kSmemBudget / (p.x_stage_bytes + p.m_stage_bytes));
     S = std::min(S, std::min(pl.num_chunks, 4));
+    if (S < 1) return fail(SDNN_ERR_INTERNAL, "stage does not fit shared memory");
+    // Stage depth vs. resident CTAs: a small grid runs faster with fewer stages and more CTAs per
+    // SM (profiles/r01_row_stages.log: c2 768² 52 → 30 µs at 2 stages, c3 256×128 22 → 12 µs at 1).
+    // Take fewer stages while that cuts the number of waves by ≥ 10 %, and only for grids within
+    // two waves; large grids keep the deep pipeline.
     {
+      auto waves = [&](int s) {
+        const int occ = std::max(1, occupancy(fn, threads, smem_for(s)));
+        return double(nblocks) / (double(h->sms) * occ);
+      };
+      double best = waves(S);
+      int best_s = S;
+      for (int s = S - 1; s >= 1 && best > 1.0; --s) {
+        const double w = waves(s);
+        if (w < 0.9 * best) {
+          best = w;
+          best_s = s;
+        }
+      }
+      if (best <= 2.0) S = best_s;
       static const int s_env = [] {
         const char* e = getenv("SDNN_ROW_STAGES");
         return e ? atoi(e) : 0;
       }();
       if (s_env > 0) S = std::min(S, s_env);
     }
-    if (S < 1) return fail(SDNN_ERR_INTERNAL, "stage does not fit shared memory");
     p.stages = S;
-    const size_t smem = size_t(S) * (p.x_stage_bytes + p.m_stage_bytes) + size_t(2 * S) * 8;
+    const size_t smem = smem_for(S);
     PFN_encodeTiled enc = get_encode_fn();
     if (!enc) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     CUtensorMap tmap;
@@ -932,18 +979,8 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
-    const dim3 grid{unsigned(nblocks)}, block{unsigned((wc + 1) * 32)};
-    const int sb = pl.group_sb;
-    if (pl.kernel == 2 && V == 8 && sb == 1) spmm_tma_kernel<2, 16, 8, 1><<<grid, block, smem, stream>>>(tmap, p);
-    else if (pl.kernel == 2 && V == 8 && sb == 2) spmm_tma_kernel<2, 16, 8, 2><<<grid, block, smem, stream>>>(tmap, p);
-    else if (pl.kernel == 2 && V == 8) spmm_tma_kernel<2, 16, 8, 4><<<grid, block, smem, stream>>>(tmap, p);
-    else if (pl.kernel == 2 && sb == 1) spmm_tma_kernel<2, 16, 4, 1><<<grid, block, smem, stream>>>(tmap, p);
-    else if (pl.kernel == 2 && sb == 2) spmm_tma_kernel<2, 16, 4, 2><<<grid, block, smem, stream>>>(tmap, p);
-    else if (pl.kernel == 2) spmm_tma_kernel<2, 16, 4, 4><<<grid, block, smem, stream>>>(tmap, p);
-    else if (rw == 8 && V == 8) spmm_tma_kernel<1, 8, 8><<<grid, block, smem, stream>>>(tmap, p);
-    else if (rw == 8 && V == 4) spmm_tma_kernel<1, 8, 4><<<grid, block, smem, stream>>>(tmap, p);
-    else if (rw == 4 && V == 8) spmm_tma_kernel<1, 4, 8><<<grid, block, smem, stream>>>(tmap, p);
-    else spmm_tma_kernel<1, 4, 4><<<grid, block, smem, stream>>>(tmap, p);
+    void* args[] = {&tmap, &p};
+    SDNN_CUDA_TRY(cudaLaunchKernel(fn, dim3(unsigned(nblocks)), dim3(unsigned(threads)), args, smem, stream));
   } else {
     p.stages = 1;
     const size_t smem = size_t(p.x_stage_bytes) + p.m_stage_bytes;

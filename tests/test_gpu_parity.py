@@ -228,7 +228,7 @@ def test_cuda_graph_capture(sdnn, kernel):
 def test_auto_takes_tmem_plan_when_it_fills_a_wave(sdnn):
     """kernel=auto keeps a TMEM plan beside the row plan (info alt_kernel = 4) and uses it when the
     call is on its fast path and fills one wave; either way the result equals the row kernel's."""
-    p = synth.config_problem("c4_2048x512_s80")  # 32 row blocks × 25 N tiles ≥ 148 SMs / 3
+    p = synth.config_problem("c4_2048x512_s80")  # 35 row blocks × 25 N tiles ≥ 148 SMs / 2
     X = p.x()
     h = sdnn.Handle.from_problem(p)
     assert h.info()["alt_kernel"] == 4 and h.info()["kernel"] == 1
@@ -238,7 +238,7 @@ def test_auto_takes_tmem_plan_when_it_fills_a_wave(sdnn):
     Xs = np.ascontiguousarray(X[:, :100])  # ragged: the row plan
     Ya, _ = run_gpu(sdnn, p, Xs, p.bias, 1, handle=h)
     np.testing.assert_array_equal(Ya, Yr[:, :100])
-    assert h.kernel_for(p.N) == 4 and h.kernel_for(102) == -1 and h.kernel_for(128) == 1  # 32·1·3 < 148
+    assert h.kernel_for(p.N) == 4 and h.kernel_for(102) == -1 and h.kernel_for(128) == 1  # 35·1·2 < 148
 
 
 def test_get_permutation_and_info(sdnn, oracle_mod):
