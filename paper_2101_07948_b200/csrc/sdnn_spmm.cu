@@ -877,7 +877,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
 }
 
 // The TMEM kernel runs one CTA per SM and pays once the call has at least half a wave of CTAs
-// (measured per config, profiles/r01_configs_v5.jsonl: it wins from ~100 CTAs up — c2 3072×768,
+// (measured per config, profiles/r01_configs_v5.log: it wins from ~100 CTAs up — c2 3072×768,
 // c3 512² — while the row kernel, several CTAs per SM, wins on c3 256×128 (65 TMEM CTAs) and below).
 static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const float* Y) {
   return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 &&
