@@ -26,6 +26,10 @@
 #include "sdnn_internal.h"
 #include "group_entry.inc"
 
+#ifndef SDNN_DIAG
+#define SDNN_DIAG 0  // diagnostics builds only (1: no TMEM loads, 2: no FFMA2); never set in the product
+#endif
+
 namespace sdnn {
 void plan_fill_info(const Plan& p, int32_t device, sdnn_info* info);
 }
@@ -501,6 +505,15 @@ __device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, u
 #pragma unroll
         for (int t = 0; t < U / 2; ++t) ee[t] = e[(i >> 1) + t];
         float4 x[U][G];
+#if SDNN_DIAG == 1  // diagnostics build: no TMEM loads (operands from the metadata)
+#pragma unroll
+        for (int t = 0; t < U; ++t)
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float v = (t & 1) ? ee[t >> 1].z : ee[t >> 1].x;
+            x[t][g] = make_float4(v, v, v, v);
+          }
+#else
 #pragma unroll
         for (int t = 0; t < U / 2; ++t) {
           TmemLd<V>::ld(tl + __float_as_uint(ee[t].x), x[2 * t]);
@@ -508,12 +521,18 @@ __device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, u
         }
         if constexpr (U == 4 && G == 1) tmem_wait_ld(x[0][0], x[1][0], x[2][0], x[3][0]);
         else tmem_wait_ld(x[0][0], x[0][1], x[1][0], x[1][1]);
+#endif
+#if SDNN_DIAG == 2  // diagnostics build: no FFMA2 (one FADD per load keeps it live)
+#pragma unroll
+        for (int t = 0; t < U; ++t) acc[r][0].x += x[t][0].x;
+#else
 #pragma unroll
         for (int t = 0; t < U; ++t) {
           const float w = (t & 1) ? ee[t >> 1].w : ee[t >> 1].y;
 #pragma unroll
           for (int g = 0; g < G; ++g) fma4(*reinterpret_cast<float2(*)[2]>(&acc[r][2 * g]), w, x[t][g]);
         }
+#endif
       }
     }
     tc_fence_before();
