@@ -259,3 +259,44 @@ def test_errors(sdnn):
     assert st == 1
     st = sdnn._lib.sdnn_spmm(h._h, X.data_ptr(), 8, None, 1, X.data_ptr(), None)  # Y aliases X
     assert st == 1
+
+
+# ------------------------------------------------------------------ property-based shapes (hypothesis)
+try:
+    from hypothesis import given, settings, HealthCheck
+    from hypothesis import strategies as st
+except ImportError:  # pragma: no cover
+    given = None
+
+if given is not None:
+    @pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "tmem8"])
+    @settings(max_examples=12, deadline=None, suppress_health_check=list(HealthCheck))
+    @given(M=st.integers(1, 300), K=st.integers(1, 300), nq=st.integers(1, 6), ragged=st.booleans(),
+           dens=st.sampled_from([0.0, 0.02, 0.1, 0.3, 1.0]), seed=st.integers(0, 2**31 - 1),
+           mask=st.sampled_from(["uniform", "blocks4"]))
+    def test_random_shapes(sdnn, oracle_mod, kernel, M, K, nq, ragged, dens, seed, mask):
+        """Random M, K, density, N (multiples of 128 — the TMEM fast path — or ragged), uniform or
+        aligned-1×4-run masks, every kernel: |Y − oracle| ≤ 1e-4·S."""
+        rng = np.random.default_rng(seed)
+        N = 128 * nq + (int(rng.integers(1, 128)) if ragged else 0)
+        if mask == "blocks4":
+            blk = rng.random((M, (K + 3) // 4)) < dens
+            m = np.repeat(blk, 4, axis=1)[:, :K]
+        else:
+            m = rng.random((M, K)) < dens
+        rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum(m.sum(1))
+        ci = np.nonzero(m)[1].astype(np.int32)
+        v = (0.05 * rng.standard_normal(ci.size)).astype(np.float32)
+        v[v == 0] = 0.01
+        b = (0.1 * rng.standard_normal(M)).astype(np.float32)
+        p = synth.Problem("rand", M, K, N, 0, "x", rp, ci, v, b, 1, seed)
+        X = rng.standard_normal((K, N)).astype(np.float32)
+        check(sdnn, oracle_mod, p, X=X, act=int(seed % 2), kernel=kernel)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "row", "tmem"])
+def test_large_k_and_large_m(sdnn, oracle_mod, kernel):
+    """K = 40 000 (625 TMEM chunks) and M = 20 000 (334 TMEM row blocks) at small N."""
+    for M, K, N, dens in [(96, 40000, 256, 0.01), (20000, 64, 128, 0.05)]:
+        p = synth.make_problem(f"big_{M}x{K}", M, K, N, 1 - dens, seed=M + K)
+        check(sdnn, oracle_mod, p, kernel=kernel)
