@@ -182,6 +182,14 @@ SDNN_API const char* sdnn_status_string(sdnn_status s);
 SDNN_API const char* sdnn_last_error_message(void); /* thread-local; "" if none */
 SDNN_API int32_t sdnn_abi_version(void);
 
+/* Environment knobs read by libsdnn (diagnostics and experiments only; unset = the product path):
+ *   SDNN_TMEM_FILL   TMEM kernels' fill path: 1 = filler warps with tcgen05.st (default), 0 = one
+ *                    producer thread with tcgen05.cp, 2 = both (odd/even pieces)
+ *   SDNN_DEBUG_TMEM  bit mask, TMEM kernels: 1 skip the X loads (TMA), 2 skip the FMA loop, 4 skip the
+ *                    smem -> TMEM fill — results are WRONG with any bit set (timing decomposition)
+ *   SDNN_ROW_STAGES  upper bound on the row kernel's stage-ring depth
+ * (and, at build time, -DSDNN_DIAG=1|2: TMEM consumer without tcgen05.ld / without FFMA2). */
+
 #ifdef __cplusplus
 }
 #endif
