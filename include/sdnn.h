@@ -74,7 +74,7 @@ typedef struct {
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
                                multiple of 8                                                        */
   int32_t group_sb;         /* group kernel sub-block rows: 0 = auto (cost model), 1, 2 or 4         */
-  uint32_t flags;           /* reserved, must be 0                                                   */
+  uint32_t flags;           /* SDNN_FLAG_NO_ROW_SPLIT or 0                                            */
 } sdnn_perm_opts;
 
 /* Read-only description of a prepared handle (or a host plan). */
@@ -98,7 +98,14 @@ typedef struct {
   int32_t max_block_bytes;  /* largest (row block, chunk) metadata block, bytes                       */
   int32_t alt_kernel;       /* auto handles: kernel of the second (TMEM) plan, else 0                 */
   int64_t max_panel_nnz;
+  int32_t num_split_rows;   /* row plan: rows split into pieces (their pieces are summed by a second
+                               small kernel, in piece order, before the bias: deterministic, but not
+                               bitwise equal to the unsplit summation order)                          */
+  int32_t num_pieces;       /* total pieces of the split rows                                         */
 } sdnn_info;
+
+/* sdnn_perm_opts.flags */
+#define SDNN_FLAG_NO_ROW_SPLIT 1u  /* row plan: never split a row across warps                         */
 
 typedef struct sdnn_handle_s* sdnn_handle; /* opaque; owns its device memory; immutable after prepare */
 typedef struct sdnn_plan_s* sdnn_plan;     /* opaque host-only plan (no device needed)               */
@@ -169,6 +176,10 @@ SDNN_API sdnn_status sdnn_plan_create(const int32_t* csr_ptr, const int32_t* col
                              int32_t K, const sdnn_perm_opts* perm_opts, sdnn_plan* out);
 SDNN_API sdnn_status sdnn_plan_get_info(sdnn_plan p, sdnn_info* info);
 SDNN_API sdnn_status sdnn_plan_export(sdnn_plan p, int32_t* row_orig, int64_t* blk_off, uint8_t* meta);
+/* Split rows of a row plan (info.num_pieces entries each; NULL arrays are skipped): piece i of original
+ * row row[i] covers the CSR entries begin[i], begin[i] + P, begin[i] + 2P, … < end[i], P being the
+ * number of pieces of that row (interleaved pieces); slots whose row_orig is −2 − i hold piece i. */
+SDNN_API sdnn_status sdnn_plan_export_pieces(sdnn_plan p, int32_t* row, int32_t* begin, int32_t* end);
 SDNN_API sdnn_status sdnn_plan_destroy(sdnn_plan p);
 
 /* sdnn_plan_codegen_ptx: the generated PTX of codegen panel `panel` of a plan created with

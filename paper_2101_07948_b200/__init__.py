@@ -27,7 +27,8 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
 EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_host", "sdnn_spmm_kernel", "sdnn_get_permutation",
            "sdnn_get_info",
-           "sdnn_permutation", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_destroy",
+           "sdnn_permutation", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_export_pieces",
+           "sdnn_plan_destroy",
            "sdnn_plan_codegen_ptx", "sdnn_status_string", "sdnn_last_error_message", "sdnn_abi_version"]
 
 
@@ -53,7 +54,7 @@ class Info(ctypes.Structure):
                 ("panel_rows", ctypes.c_int32), ("cta_panels", ctypes.c_int32), ("num_panels", ctypes.c_int32),
                 ("num_row_blocks", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("meta_bytes", ctypes.c_int64), ("max_block_bytes", ctypes.c_int32), ("alt_kernel", ctypes.c_int32),
-                ("max_panel_nnz", ctypes.c_int64)]
+                ("max_panel_nnz", ctypes.c_int64), ("num_split_rows", ctypes.c_int32), ("num_pieces", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "struct_size"}
@@ -71,6 +72,7 @@ _lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
 _lib.sdnn_plan_create.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts), ctypes.POINTER(_vp)]
 _lib.sdnn_plan_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_plan_export.argtypes = [_vp, _vp, _vp, _vp]
+_lib.sdnn_plan_export_pieces.argtypes = [_vp, _vp, _vp, _vp]
 _lib.sdnn_plan_destroy.argtypes = [_vp]
 _lib.sdnn_plan_codegen_ptx.argtypes = [_vp, _vp, _vp, _vp, _i32, _vp, ctypes.POINTER(_i64)]
 _lib.sdnn_status_string.restype = ctypes.c_char_p
@@ -100,10 +102,13 @@ def _csr(row_ptr, col_idx, vals):
 KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4, "tmem8": 5}
 
 
-def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0):
+FLAG_NO_ROW_SPLIT = 1
+
+
+def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0, split_rows=True):
     k = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
     return PermOpts(ctypes.sizeof(PermOpts), int(bool(permute)), k, int(panel_rows), int(cta_panels), int(k_chunk),
-                    int(group_sb), 0)
+                    int(group_sb), 0 if split_rows else FLAG_NO_ROW_SPLIT)
 
 
 def _act(act) -> int:
@@ -147,6 +152,13 @@ class Plan:
         _check(_lib.sdnn_plan_codegen_ptx(self._h, _np_ptr(rp), _np_ptr(ci), _np_ptr(v), panel, buf, ctypes.byref(n)),
                "sdnn_plan_codegen_ptx")
         return buf.value.decode()
+
+    def export_pieces(self):
+        """Split rows of a row plan: (row, begin, end) per piece (CSR entry ranges)."""
+        n = self.info()["num_pieces"]
+        row, begin, end = (np.empty(n, np.int32) for _ in range(3))
+        _check(_lib.sdnn_plan_export_pieces(self._h, _np_ptr(row), _np_ptr(begin), _np_ptr(end)), "sdnn_plan_export_pieces")
+        return row, begin, end
 
     def export(self):
         i = self.info()

@@ -39,6 +39,11 @@ struct Plan {
   std::vector<std::vector<int32_t>> cg_panels;
   int32_t cg_warps = 0, cg_prefetch = 0;
   int32_t tmem_fill = 1;       // TMEM kernels: 1 = filler warps (tcgen05.st), 0 = tcgen05.cp
+  // row plan: heavy rows split into pieces (contiguous CSR entry ranges) that the LPT places like
+  // rows; a piece's slot has row_orig = −2 − piece id and its partial sums go to a workspace row
+  // that split_reduce_kernel adds up (piece order) before the bias and activation.
+  std::vector<int32_t> piece_row, piece_begin, piece_end;
+  std::vector<int32_t> split_row, split_first, split_count;
 };
 
 sdnn_status validate_csr(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K);

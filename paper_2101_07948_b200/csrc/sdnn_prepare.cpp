@@ -102,9 +102,26 @@ struct EmitStats {
   int64_t subblocks = 0;  // group kernel: nonzero sub-blocks over all entries
 };
 
+struct Pieces {  // split rows of a row plan (see Plan::piece_*)
+  std::vector<int32_t> row, begin, end, stride;
+};
+
 static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals,
                         const std::vector<int32_t>& row_orig, const Geometry& g, std::vector<int64_t>& sizes,
-                        uint8_t* out, const std::vector<int64_t>* offs, EmitStats* stats) {
+                        uint8_t* out, const std::vector<int64_t>* offs, EmitStats* stats,
+                        const Pieces* pieces = nullptr) {
+  // CSR entry range of a slot: a whole row, a piece of a split row (row_orig = −2 − piece), or empty
+  struct Range {
+    int32_t begin, end, stride;
+  };
+  auto range_of = [&](int32_t orow) -> Range {
+    if (orow >= 0) return {csr_ptr[orow], csr_ptr[orow + 1], 1};
+    if (orow <= -2 && pieces) {
+      const size_t i = size_t(-2 - orow);
+      return {pieces->begin[i], pieces->end[i], pieces->stride[i]};
+    }
+    return {0, 0, 1};
+  };
   const int32_t rcta = g.rw * g.wc;
   sizes.assign(size_t(g.nrb) * g.nch, 0);
   std::vector<int32_t> cur(rcta);
@@ -113,9 +130,12 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
   std::vector<uint16_t> mask(g.kc);
   std::vector<float> wv(size_t(g.kc) * 16);
   for (int32_t b = 0; b < g.nrb; ++b) {
+    std::vector<int32_t> stop(rcta), step(rcta);
     for (int32_t s = 0; s < rcta; ++s) {
-      const int32_t orow = row_orig[size_t(b) * rcta + s];
-      cur[s] = orow >= 0 ? csr_ptr[orow] : 0;
+      const Range rg = range_of(row_orig[size_t(b) * rcta + s]);
+      cur[s] = rg.begin;
+      stop[s] = rg.end;
+      step[s] = rg.stride;
     }
     for (int32_t j = 0; j < g.nch; ++j) {
       const int32_t lo = j * g.kc, hi = lo + g.kc;
@@ -145,12 +165,13 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
             }
             ++c;
           };
-          if (orow >= 0) {
+          if (orow != -1) {
             int32_t& p = cur[s];
-            const int32_t end = csr_ptr[orow + 1];
+            const int32_t end = stop[s];
+            const int32_t stp = step[s];
             while (p < end && col_idx[p] < hi) {
               const int32_t col = col_idx[p];
-              if (g.tmem == 4 && leading && col % 4 == 0 && p + 3 < end && col_idx[p + 3] == col + 3 &&
+              if (stp == 1 && g.tmem == 4 && leading && col % 4 == 0 && p + 3 < end && col_idx[p + 3] == col + 3 &&
                   col + 3 < hi) {
                 for (int32_t t = 0; t < 4; ++t) put(uint32_t(col + t - lo) * 4u + half, vals[p + t]);
                 p += 4;
@@ -159,7 +180,7 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
               }
               leading = false;
               put(g.tmem ? uint32_t(col - lo) * uint32_t(g.tmem) + half : uint32_t(col - lo), vals[p]);
-              ++p;
+              p += stp;
             }
           }
           const int32_t cpad = g.tmem ? int32_t(align_up(c, tmem_pad(g.tmem))) : c;
@@ -252,7 +273,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     if (opts->struct_size != sizeof(sdnn_perm_opts))
       return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.struct_size mismatch");
     o = *opts;
-    if (o.flags != 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.flags must be 0");
+    if (o.flags & ~SDNN_FLAG_NO_ROW_SPLIT) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown sdnn_perm_opts.flags bits");
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
     if (o.kernel < 0 || o.kernel > 5) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..5");
     if (o.kernel == 4 || o.kernel == 5) {
@@ -362,17 +383,55 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     // time first onto the least-loaded warp with a free slot — which keeps the heavy rows of a
     // skewed (log-normal) matrix from piling into one warp.  Within a warp the rows keep their
     // Algorithm 1 order.
-    auto row_orig_for = [&](const Geometry& g) {
-      const int32_t nw = g.nrb * g.wc;
-      std::vector<int32_t> ro(size_t(nw) * g.rw, -1);
+    //
+    // Heavy rows (row plan only; not with SDNN_FLAG_NO_ROW_SPLIT): a row with more nonzeros than the
+    // mean load of a warp, T = ⌈nnz / warps⌉ (at least 64), would make its warp the critical path of
+    // the whole launch (log-normal rows: up to K nonzeros) — and, since the warps of a CTA advance
+    // through the K chunks together, of every chunk.  It is dealt out in P = ⌈nnz_row / T⌉
+    // interleaved pieces (piece q: entries q, q + P, … of the row, ascending columns) so each piece
+    // has ~1/P of every chunk, and the pieces are placed by the LPT like rows.
+    Pieces pcs;
+    auto row_orig_for = [&](Geometry& g, Pieces* out) {
+      if (out) *out = Pieces{};
       if (g.kernel == 2) {
+        std::vector<int32_t> ro(size_t(g.nrb) * g.wc * g.rw, -1);
         for (int32_t p = 0; p < M; ++p) ro[p] = plan.perm[p];
         return ro;
       }
-      std::vector<int32_t> pos(M), order(M);
-      for (int32_t i = 0; i < M; ++i) { pos[plan.perm[i]] = i; order[i] = i; }
+      std::vector<int32_t> pos(M);
+      for (int32_t i = 0; i < M; ++i) pos[plan.perm[i]] = i;
       auto nz = [&](int32_t r) { return csr_ptr[r + 1] - csr_ptr[r]; };
-      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return nz(a) > nz(b); });
+      // items: whole rows (id = row) and pieces (id = −2 − piece); weight = nonzeros
+      std::vector<std::pair<int64_t, int32_t>> items;
+      items.reserve(size_t(M));
+      const bool split = out && g.kernel == 1 && g.tmem == 0 && !(o.flags & SDNN_FLAG_NO_ROW_SPLIT);
+      const int32_t nw0 = g.nrb * g.wc;
+      const int64_t T = std::max<int64_t>(64, (nnz + nw0 - 1) / std::max(nw0, 1));
+      for (int32_t r = 0; r < M; ++r) {
+        const int64_t n = nz(r);
+        if (split && n > T) {
+          const int32_t P = int32_t((n + T - 1) / T);
+          for (int32_t q = 0; q < P; ++q) {  // piece q: entries q, q + P, q + 2P, … of the row
+            items.push_back({(n - q + P - 1) / P, -2 - int32_t(out->row.size())});
+            out->row.push_back(r);
+            out->begin.push_back(csr_ptr[r] + q);
+            out->end.push_back(csr_ptr[r + 1]);
+            out->stride.push_back(P);
+          }
+        } else {
+          items.push_back({n, r});
+        }
+      }
+      auto orig_of = [&](int32_t id) { return id >= 0 ? id : out->row[size_t(-2 - id)]; };
+      // pieces need slots: more row blocks if the rows already fill them
+      const int64_t per_block = int64_t(g.rw) * g.wc;
+      g.nrb = int32_t(std::max<int64_t>(g.nrb, (int64_t(items.size()) + per_block - 1) / per_block));
+      const int32_t nw = g.nrb * g.wc;
+      std::vector<int32_t> ro(size_t(nw) * g.rw, -1);
+      std::stable_sort(items.begin(), items.end(),
+                       [&](const std::pair<int64_t, int32_t>& a, const std::pair<int64_t, int32_t>& b) {
+                         return a.first > b.first;
+                       });
       // min-heap of (load, warp); warps with full slots leave the heap
       std::vector<std::pair<int64_t, int32_t>> heap;
       heap.reserve(nw);
@@ -380,18 +439,21 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       std::vector<int32_t> fill(nw, 0);
       std::vector<std::vector<int32_t>> rows(nw);
       auto cmp = [](const std::pair<int64_t, int32_t>& a, const std::pair<int64_t, int32_t>& b) { return a > b; };
-      for (int32_t r : order) {
+      for (const auto& it : items) {
         std::pop_heap(heap.begin(), heap.end(), cmp);
         auto [load, w] = heap.back();
         heap.pop_back();
-        rows[w].push_back(r);
+        rows[w].push_back(it.second);
         if (++fill[w] < g.rw) {
-          heap.push_back({load + nz(r) + 1, w});
+          heap.push_back({load + it.first + 1, w});
           std::push_heap(heap.begin(), heap.end(), cmp);
         }
       }
       for (int32_t w = 0; w < nw; ++w) {
-        std::sort(rows[w].begin(), rows[w].end(), [&](int32_t a, int32_t b) { return pos[a] < pos[b]; });
+        std::sort(rows[w].begin(), rows[w].end(), [&](int32_t a, int32_t b) {
+          const int32_t pa = pos[orig_of(a)], pb = pos[orig_of(b)];
+          return pa != pb ? pa < pb : a > b;  // pieces of one row: in piece order (ids −2, −3, …)
+        });
         for (size_t i = 0; i < rows[w].size(); ++i) ro[size_t(w) * g.rw + i] = rows[w][i];
       }
       return ro;
@@ -405,14 +467,14 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
         if (o.k_chunk && c != o.k_chunk) continue;
         g.kc = c;
         g.nch = (K + c - 1) / c;
-        emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries);
+        emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries, &pcs);
         const int32_t s = stages_for(c, max_of(sizes));
         if (s >= 3 || (s >= 2 && (o.k_chunk || c == 8))) return true;
       }
       if (o.k_chunk) {  // explicit KC not in the candidate list
         g.kc = o.k_chunk;
         g.nch = (K + g.kc - 1) / g.kc;
-        emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries);
+        emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries, &pcs);
         return stages_for(g.kc, max_of(sizes)) >= 2;
       }
       return false;
@@ -446,13 +508,15 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
           if (!o.group_sb || o.group_sb == sb) cands.push_back(make_geo(2, sb));
       double best = 0;
       bool found = false;
+      Pieces best_pcs;
       for (Geometry c : cands) {
-        std::vector<int32_t> r = row_orig_for(c);
+        std::vector<int32_t> r = row_orig_for(c, &pcs);
         EmitStats st;
         if (!choose_kc(c, r, &st)) continue;
         const double cc = cost(c, st);
-        if (!found || cc < best) { best = cc; g = c; ro.swap(r); stats = st; found = true; }
+        if (!found || cc < best) { best = cc; g = c; ro.swap(r); stats = st; found = true; best_pcs = pcs; }
       }
+      pcs = best_pcs;
       if (!found) return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
     }
     plan.kernel = (o.kernel == 4 || o.kernel == 5) ? o.kernel : g.kernel;
@@ -468,11 +532,27 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       for (int32_t r = 0; r < g.rw; ++r) {
         const int32_t orow = plan.row_orig[size_t(pn) * g.rw + r];
         if (orow >= 0) s += csr_ptr[orow + 1] - csr_ptr[orow];
+        if (orow <= -2) {
+          const size_t i = size_t(-2 - orow);
+          s += (pcs.end[i] - pcs.begin[i] + pcs.stride[i] - 1) / pcs.stride[i];
+        }
       }
       plan.max_panel_nnz = std::max(plan.max_panel_nnz, s);
     }
+    // split-row table for the reduction kernel (pieces of a row have consecutive ids)
+    plan.piece_row = pcs.row;
+    plan.piece_begin = pcs.begin;
+    plan.piece_end = pcs.end;
+    for (size_t i = 0; i < pcs.row.size(); ++i) {
+      if (i == 0 || pcs.row[i] != pcs.row[i - 1]) {
+        plan.split_row.push_back(pcs.row[i]);
+        plan.split_first.push_back(int32_t(i));
+        plan.split_count.push_back(0);
+      }
+      plan.split_count.back()++;
+    }
     std::vector<int64_t> sizes;
-    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, nullptr, nullptr, &stats);
+    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, nullptr, nullptr, &stats, &pcs);
     plan.group_entries = g.kernel == 2 ? stats.entries : 0;
     plan.group_sb = g.kernel == 2 ? g.sb : 0;
     plan.group_subblocks = g.kernel == 2 ? stats.subblocks : 0;
@@ -480,7 +560,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     plan.blk_off.assign(sizes.size() + 1, 0);
     for (size_t i = 0; i < sizes.size(); ++i) plan.blk_off[i + 1] = plan.blk_off[i] + sizes[i];
     plan.meta.assign(size_t(plan.blk_off.back()), 0);
-    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, plan.meta.data(), &plan.blk_off, nullptr);
+    emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, plan.meta.data(), &plan.blk_off, nullptr, &pcs);
   } catch (const std::bad_alloc&) {
     return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed during planning");
   }
@@ -515,6 +595,8 @@ static void fill_info(const Plan& p, int32_t device, sdnn_info* info) {
   info->max_block_bytes = p.max_block_bytes;
   info->alt_kernel = 0;
   info->max_panel_nnz = p.max_panel_nnz;
+  info->num_split_rows = int32_t(p.split_row.size());
+  info->num_pieces = int32_t(p.piece_row.size());
 }
 
 namespace sdnn {
@@ -580,6 +662,16 @@ sdnn_status sdnn_plan_export(sdnn_plan p, int32_t* row_orig, int64_t* blk_off, u
   if (row_orig) std::memcpy(row_orig, pl.row_orig.data(), pl.row_orig.size() * 4);
   if (blk_off) std::memcpy(blk_off, pl.blk_off.data(), pl.blk_off.size() * 8);
   if (meta && !pl.meta.empty()) std::memcpy(meta, pl.meta.data(), pl.meta.size());
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_plan_export_pieces(sdnn_plan p, int32_t* row, int32_t* begin, int32_t* end) {
+  if (!p) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL plan");
+  const Plan& pl = p->plan;
+  const size_t n = pl.piece_row.size() * 4;
+  if (row && n) std::memcpy(row, pl.piece_row.data(), n);
+  if (begin && n) std::memcpy(begin, pl.piece_begin.data(), n);
+  if (end && n) std::memcpy(end, pl.piece_end.data(), n);
   return SDNN_OK;
 }
 

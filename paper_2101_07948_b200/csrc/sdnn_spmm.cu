@@ -52,6 +52,8 @@ struct sdnn_handle_s {
   uint8_t* d_meta = nullptr;
   int64_t* d_blk_off = nullptr;
   int32_t* d_row_orig = nullptr;
+  int32_t* d_split = nullptr;  // split-row table {rows, first piece, count} (row plan)
+  cudaMemPool_t ws_pool = nullptr;  // split-row workspaces: stream-ordered, memory kept between calls
   // codegen kernel: one JIT module per panel, one stream per panel (all panels run concurrently)
   std::vector<CUmodule> cg_mods;
   std::vector<CUfunction> cg_funcs;
@@ -128,6 +130,7 @@ struct KParams {
   int32_t K, nch, kc, wc, nrb, stages;
   int32_t x_stage_bytes, m_stage_bytes, hdr_bytes;
   int32_t act;
+  float* ws;    // split-row workspace (pieces × N), row plans only
   int32_t dbg;  // TMEM kernels, diagnostics only (SDNN_DEBUG_TMEM): bit 0 skip the X loads, bit 1 skip the FMAs,
                // bit 2 skip the smem → TMEM fill
 };
@@ -222,17 +225,24 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
     const int32_t orow = p.row_orig[panel * RW + r];
-    if (orow < 0) continue;
-    const float b = p.bias ? p.bias[orow] : 0.f;
-    float* yrow = p.Y + int64_t(orow) * p.N;
+    if (orow == -1) continue;
+    // a piece of a split row (row_orig = −2 − piece): its raw partial sums go to workspace row
+    // `piece`; split_reduce_kernel adds the pieces, the bias and the activation
+    const bool piece = orow <= -2;
+    const float b = (piece || !p.bias) ? 0.f : p.bias[orow];
+    float* yrow = piece ? p.ws + int64_t(-2 - orow) * p.N : p.Y + int64_t(orow) * p.N;
 #pragma unroll
     for (int h = 0; h < V / 4; ++h) {
       const int64_t n = n0 + h * 128 + lane * 4;
       const float2 a0 = as_f2(acc[r][2 * h]), a1 = as_f2(acc[r][2 * h + 1]);
-      float v[4] = {a0.x + b, a0.y + b, a1.x + b, a1.y + b};
-      if (p.act == SDNN_ACT_RELU) {
+      float v[4] = {a0.x, a0.y, a1.x, a1.y};
+      if (!piece) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = v[q] > 0.f ? v[q] : 0.f;
+        for (int q = 0; q < 4; ++q) v[q] += b;
+        if (p.act == SDNN_ACT_RELU) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = v[q] > 0.f ? v[q] : 0.f;
+        }
       }
       if (VEC) {
         if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
@@ -243,6 +253,21 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
       }
     }
   }
+}
+
+// Split rows (row plan): Y[row] = act(Σ_pieces ws[piece] (in piece order) + b[row]).  One thread per
+// column; blockIdx.y = split row.  split = {rows[ns], first piece[ns], piece count[ns]}.
+__global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t* __restrict__ split, int32_t ns,
+                                    const float* __restrict__ bias, int32_t act, float* __restrict__ Y, int64_t N) {
+  const int32_t sr = int32_t(blockIdx.y);
+  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int32_t row = split[sr], first = split[ns + sr], cnt = split[2 * ns + sr];
+  float v = ws[int64_t(first) * N + n];
+  for (int32_t k = 1; k < cnt; ++k) v += ws[int64_t(first + k) * N + n];
+  if (bias) v += bias[row];
+  if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
+  Y[int64_t(row) * N + n] = v;
 }
 
 // Fast path: TMA producer warp + W_c consumer warps, mbarrier stage ring.
@@ -904,6 +929,9 @@ static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const 
              a->sms;
 }
 
+static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                               float* Y, float* ws, cudaStream_t stream);
+
 static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
                           cudaStream_t stream) {
   if (tmem_worth(h->alt, X, N, Y)) return launch_tmem(h->alt, X, N, bias, act, Y, stream);
@@ -912,6 +940,31 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
   if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(Y) % 16 == 0)
     return launch_tmem(h, X, N, bias, act, Y, stream);
+  // split rows (row plan): a stream-ordered workspace for the pieces' partial sums, reduced after
+  // the main kernel (no host synchronisation; allocation nodes under CUDA-graph capture)
+  float* ws = nullptr;
+  const int32_t ns = int32_t(pl.split_row.size());
+  if (ns > 0) {
+    SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ws), pl.piece_row.size() * size_t(N) * 4,
+                                          h->ws_pool, stream));
+  }
+  sdnn_status st = launch_main(h, X, N, bias, act, Y, ws, stream);
+  if (ns > 0) {
+    if (st == SDNN_OK) {
+      const dim3 grid{unsigned((N + 255) / 256), unsigned(ns)};
+      split_reduce_kernel<<<grid, 256, 0, stream>>>(ws, h->d_split, ns, bias, act, Y, N);
+      const cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("split_reduce_kernel: ") + cudaGetErrorString(le));
+    }
+    cudaFreeAsync(ws, stream);
+  }
+  return st;
+}
+
+// The row / group / generic kernels of a plan (everything but TMEM and codegen).
+static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
+                               float* ws, cudaStream_t stream) {
+  const Plan& pl = h->plan;
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
   int V = 8;
@@ -939,6 +992,7 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
   p.m_stage_bytes = int32_t(align_up(pl.max_block_bytes, 128));
   p.hdr_bytes = int32_t(align_up(int64_t(rw) * wc * 4, 16));
   p.act = act;
+  p.ws = ws;
 
   const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(Y) % 16 == 0) && pl.kernel < 4;
@@ -1095,6 +1149,8 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     cudaFree(h->d_meta);
     cudaFree(h->d_blk_off);
     cudaFree(h->d_row_orig);
+    cudaFree(h->d_split);
+    if (h->ws_pool) cudaMemPoolDestroy(h->ws_pool);
     delete h;
     return fail(s, m);
   };
@@ -1111,6 +1167,22 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
   if (e == cudaSuccess) e = cudaMemcpy(h->d_blk_off, pl.blk_off.data(), pl.blk_off.size() * 8, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(h->d_row_orig, pl.row_orig.data(), pl.row_orig.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !pl.split_row.empty()) {
+    std::vector<int32_t> tab(pl.split_row);
+    tab.insert(tab.end(), pl.split_first.begin(), pl.split_first.end());
+    tab.insert(tab.end(), pl.split_count.begin(), pl.split_count.end());
+    e = cudaMalloc(&h->d_split, tab.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_split, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&h->ws_pool, &props);
+      uint64_t keep = ~uint64_t(0);
+      if (e == cudaSuccess) e = cudaMemPoolSetAttribute(h->ws_pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (e != cudaSuccess) return cleanup(SDNN_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
   pl.meta_size_uploaded = int64_t(pl.meta.size());
   std::vector<uint8_t>().swap(pl.meta);
@@ -1188,6 +1260,11 @@ sdnn_status sdnn_destroy(sdnn_handle h) {
   cudaFree(h->d_meta);
   cudaFree(h->d_blk_off);
   cudaFree(h->d_row_orig);
+  cudaFree(h->d_split);
+  if (h->ws_pool) {
+    cudaDeviceSynchronize();
+    cudaMemPoolDestroy(h->ws_pool);
+  }
   for (cudaStream_t st : h->cg_streams)
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t ev : h->cg_join)

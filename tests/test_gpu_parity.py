@@ -162,9 +162,11 @@ def test_n_zero_is_noop(sdnn):
 
 # ------------------------------------------------------------------ invariants (bitwise)
 def test_permute_on_off_and_tilings_bitwise(sdnn):
+    """Every kernel and tiling accumulates each row in ascending column order → identical Y (rows
+    are not split here: split rows sum fixed pieces, see test_split_rows)."""
     p = synth.config_problem("c2_768x3072")
     X = p.x()
-    ref, _ = run_gpu(sdnn, p, X, p.bias, 1)
+    ref, _ = run_gpu(sdnn, p, X, p.bias, 1, split_rows=False)
     for opts in [dict(permute=False), dict(panel_rows=8), dict(cta_panels=1), dict(k_chunk=8),
                  dict(k_chunk=96, panel_rows=4, cta_panels=2), dict(kernel="group"), dict(kernel="row"),
                  dict(kernel="group", permute=False), dict(kernel="group", cta_panels=3, k_chunk=16),
@@ -172,8 +174,38 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
                  dict(kernel="codegen"), dict(kernel="codegen", permute=False), dict(kernel="codegen", panel_rows=7),
                  dict(kernel="tmem"), dict(kernel="tmem", permute=False), dict(kernel="tmem8"),
                  dict(kernel="tmem8", permute=False)]:
-        Y, _ = run_gpu(sdnn, p, X, p.bias, 1, **opts)
+        Y, _ = run_gpu(sdnn, p, X, p.bias, 1, split_rows=False, **opts)
         np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
+
+
+@pytest.mark.parametrize("key", ["c2_768x768", "c2_768x3072", "c2_3072x768"])
+def test_split_rows(sdnn, oracle_mod, key):
+    """Heavy log-normal rows split into pieces (row plan): parity with the oracle, deterministic,
+    invariant to column shards and to the permutation (the pieces depend on the row only), close to
+    the unsplit result, and capturable in a CUDA graph (stream-ordered workspace)."""
+    p = synth.config_problem(key)
+    X = p.x()
+    worst, Y, h = check(sdnn, oracle_mod, p, kernel="row")
+    assert h.info()["num_pieces"] > 0
+    Y2, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Y, Y2)
+    Ys, _ = run_gpu(sdnn, p, np.ascontiguousarray(X[:, 100:612]), p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Ys, Y[:, 100:612])
+    Yp, _ = run_gpu(sdnn, p, X, p.bias, 1, kernel="row", permute=False)
+    np.testing.assert_array_equal(Yp, Y)
+    Yu, _ = run_gpu(sdnn, p, X, p.bias, 1, kernel="row", split_rows=False)
+    Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, want_scale=True)[:2]
+    assert_parity(Yu, Yo, S, "unsplit")
+    Xd = torch.from_numpy(X).cuda()
+    b = torch.from_numpy(p.bias).cuda()
+    Yg = torch.empty((p.M, p.N), device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        h.spmm(Xd, b, act=1, out=Yg)
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(Yg.cpu().numpy(), Y)
 
 
 def test_column_shards_bitwise(sdnn):

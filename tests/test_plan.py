@@ -25,6 +25,7 @@ def decode(p, plan):
     triples = []
     last_col = {}
     runs = []
+    prow, pbeg, pend = plan.export_pieces() if info["num_pieces"] else ([], [], [])
     for b in range(nrb):
         for j in range(nch):
             blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]]
@@ -41,6 +42,10 @@ def decode(p, plan):
                         runs.append((b, j, start + 4 * u))
                 assert start % 2 == 0
                 orow = int(row_orig[b * rcta + s])
+                key = orow
+                if orow <= -2:  # a piece of a split row (row plan): CSR entries [pbeg, pend) of prow
+                    pid = -2 - orow
+                    orow, key = int(prow[pid]), (int(prow[pid]), pid)
                 if orow < 0:
                     assert cnt == 0
                     continue
@@ -59,14 +64,23 @@ def decode(p, plan):
                         cl = (cl - half) // V
                     assert 0 <= cl < kc
                     col = j * kc + cl
-                    assert col > last_col.get(orow, -1)  # ascending column order per row
-                    last_col[orow] = col
+                    assert col > last_col.get(key, -1)  # ascending column order per row (per piece)
+                    last_col[key] = col
                     triples.append((orow, col, w))
     for b, j, at in runs:  # a run is 4 consecutive columns k..k+3, k % 4 == 0
         blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]]
         cols = [int(blk[hdr_bytes + (at + t) * 8:hdr_bytes + (at + t) * 8 + 4].view(np.uint32)[0]) for t in range(4)]
         assert cols == [cols[0] + 4 * t for t in range(4)] and (cols[0] % 256) % 16 == 0
     decode.runs = len(runs)
+    # pieces of a row: consecutive ids q = 0..P-1, piece q = entries row_ptr[r] + q, + P, … (interleaved)
+    pid = 0
+    while pid < len(prow):
+        r = int(prow[pid])
+        P = int(np.sum(prow == r))
+        assert list(prow[pid:pid + P]) == [r] * P and P >= 2
+        for q in range(P):
+            assert pbeg[pid + q] == p.row_ptr[r] + q and pend[pid + q] == p.row_ptr[r + 1]
+        pid += P
     return info, row_orig, triples
 
 
@@ -159,12 +173,17 @@ def test_packing_invariants(oracle_mod, key, opts):
         np.testing.assert_array_equal(row_orig[:p.M], perm)
         assert np.all(row_orig[p.M:] == -1)
     else:
-        # row kernel: every row in exactly one slot; rows of a warp keep their Algorithm 1 order
-        assert sorted(row_orig[row_orig >= 0].tolist()) == list(range(p.M))
+        # row kernel: every row in exactly one slot (or split into pieces); rows of a warp keep their
+        # Algorithm 1 order
+        prow = plan.export_pieces()[0] if info["num_pieces"] else np.zeros(0, np.int32)
+        assert sorted(row_orig[row_orig >= 0].tolist() + sorted(set(prow.tolist()))) == list(range(p.M))
+        assert sorted((-2 - row_orig[row_orig <= -2]).tolist()) == list(range(len(prow)))
         pos = np.empty(p.M, int); pos[perm] = np.arange(p.M)
         for w in range(info["num_panels"]):
             rs = [r for r in row_orig[w * info["panel_rows"]:(w + 1) * info["panel_rows"]] if r >= 0]
             assert list(pos[rs]) == sorted(pos[rs])
+        if info["num_pieces"]:
+            return  # load balance of split plans: test_split_rows_balance
         # LPT balance: max warp load <= mean load + heaviest row
         loads = [sum(int(np.diff(p.row_ptr)[r]) for r in row_orig[w * info["panel_rows"]:(w + 1) * info["panel_rows"]] if r >= 0)
                  for w in range(info["num_panels"])]
@@ -172,6 +191,26 @@ def test_packing_invariants(oracle_mod, key, opts):
     assert info["num_row_blocks"] * info["panel_rows"] * info["cta_panels"] >= p.M
     cnt = np.diff(p.row_ptr)
     assert info["max_panel_nnz"] >= cnt.max()
+
+
+def test_split_rows_balance():
+    """Log-normal rows (c2, up to K nonzeros): heavy rows are cut into pieces so that no warp's load
+    exceeds the mean by more than one piece; uniform masks (c3-c5) are never split; the flag turns
+    it off."""
+    for key in ("c2_768x768", "c2_768x3072", "c2_3072x768"):
+        p = synth.config_problem(key, N=4)
+        plan = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="row")
+        info = plan.info()
+        assert info["num_split_rows"] > 0 and info["num_pieces"] > info["num_split_rows"]
+        mean = p.nnz / info["num_panels"]
+        T = max(64, -(-p.nnz // (info["num_panels"])))
+        assert info["max_panel_nnz"] <= 1.2 * mean + T, key
+        off = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="row", split_rows=False).info()
+        assert off["num_pieces"] == 0 and off["max_panel_nnz"] >= np.diff(p.row_ptr).max()
+        decode(p, plan)
+    for key in ("c3_512x512", "c4_2048x512_s80"):
+        p = synth.config_problem(key, N=4)
+        assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="row").info()["num_pieces"] == 0
 
 
 def test_auto_kernel_choice_and_alg1_benefit():
