@@ -141,6 +141,18 @@ SDNN_API sdnn_status sdnn_destroy(sdnn_handle h);
 SDNN_API sdnn_status sdnn_spmm(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
                       void* stream);
 
+/* sdnn_spmm_multi: the same operation, Y written to n_dst (1..8) device buffers at once — the fused
+ * form of "SpMM, then all-gather of Y" (BASELINE north_star): each destination is an
+ * M×ldy row-major buffer (ldy ≥ col0 + N) that receives Y in columns [col0, col0 + N), e.g. every
+ * rank's symmetric-memory Y buffer mapped into this device (peer or multicast addresses), with col0
+ * the rank's column offset; the epilogue stores each output element to every destination, so the
+ * transfer overlaps the kernel.  Visibility on the peers follows the caller's barrier (e.g. the
+ * symmetric-memory barrier after the call).  Same errors as sdnn_spmm, plus INVALID_ARGUMENT for
+ * n_dst outside 1..8, a NULL destination, col0 < 0 or ldy < col0 + N.  The vector fast paths need
+ * ldy, col0 multiples of 4 and 16-byte-aligned destinations; the codegen kernel is UNSUPPORTED. */
+SDNN_API sdnn_status sdnn_spmm_multi(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act,
+                                     float* const* Y_dsts, int32_t n_dst, int64_t ldy, int64_t col0, void* stream);
+
 /* sdnn_spmm_host: the same operation on HOST buffers (X host K×N, bias host fp32[M] or NULL, Y host
  * M×N).  Columns are processed in blocks of `block_cols` (0 = auto), with host→device copy, kernel
  * and device→host copy of successive blocks overlapped on internal streams; pinned (page-locked)

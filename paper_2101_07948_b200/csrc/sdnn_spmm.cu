@@ -19,6 +19,7 @@
 #include <cstring>
 #include <mutex>
 #include <thread>
+#include <type_traits>
 #include <new>
 #include <string>
 #include <vector>
@@ -119,13 +120,37 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
+// Output destinations of a launch: Y is written to every y[d] (d < n), row-major with leading
+// dimension ld, at columns col0 .. col0 + N − 1 (sdnn_spmm: one destination, ld = N, col0 = 0;
+// sdnn_spmm_multi: e.g. the symmetric buffers of all ranks for a fused all-gather).
+constexpr int kMaxDst = 8;
+struct YOut {
+  float* y[kMaxDst];
+  int32_t n;
+  int64_t ld, col0;
+};
+static YOut y_single(float* Y, int64_t N) {
+  YOut o{};
+  o.y[0] = Y;
+  o.n = 1;
+  o.ld = N;
+  o.col0 = 0;
+  return o;
+}
+static bool y_aligned16(const YOut& o) {
+  if (o.ld % 4 || o.col0 % 4) return false;
+  for (int d = 0; d < o.n; ++d)
+    if (reinterpret_cast<uintptr_t>(o.y[d]) % 16) return false;
+  return true;
+}
+
 struct KParams {
   const uint8_t* meta;
   const int64_t* blk_off;
   const int32_t* row_orig;
   const float* X;  // fallback kernel only
   const float* bias;
-  float* Y;
+  float* Y;  // the single destination (ld = N, col0 = 0); yo.y[0] as well
   int64_t N;
   int32_t K, nch, kc, wc, nrb, stages;
   int32_t x_stage_bytes, m_stage_bytes, hdr_bytes;
@@ -134,6 +159,13 @@ struct KParams {
   int32_t dbg;  // TMEM kernels, diagnostics only (SDNN_DEBUG_TMEM): bit 0 skip the X loads, bit 1 skip the FMAs,
                // bit 2 skip the smem → TMEM fill
 };
+// Row/group/generic kernels and the multi-destination TMEM kernel: KParams + every destination.  The
+// single-destination TMEM kernel takes plain KParams — its register allocation (72 regs, bound by
+// __launch_bounds__) shifts with the parameter block size and a larger block measured 8 % slower on c5.
+struct KParamsY : KParams {
+  YOut yo;  // every destination (sdnn_spmm_multi); p.Y = yo.y[0] when there is just one of ld = N, col0 = 0
+};
+template <bool MULTI> using TmemParams = std::conditional_t<MULTI, KParamsY, KParams>;
 
 // Consume one chunk: for each of the warp's RW rows, every (col, w) entry of the chunk:
 // acc[r] += w · X_stage[col][lane·4 .. +4] (and +128 for V = 8), ascending column order.
@@ -220,7 +252,7 @@ template <> struct AccSel<2> { using type = uint64_t; };
 template <int KIND> using AccT = typename AccSel<KIND>::type;
 
 template <int RW, int V, bool VEC, typename A>
-__device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParams& p, int panel, int lane,
+__device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParamsY& p, int panel, int lane,
                                          int64_t n0) {
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
@@ -230,7 +262,6 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
     // `piece`; split_reduce_kernel adds the pieces, the bias and the activation
     const bool piece = orow <= -2;
     const float b = (piece || !p.bias) ? 0.f : p.bias[orow];
-    float* yrow = piece ? p.ws + int64_t(-2 - orow) * p.N : p.Y + int64_t(orow) * p.N;
 #pragma unroll
     for (int h = 0; h < V / 4; ++h) {
       const int64_t n = n0 + h * 128 + lane * 4;
@@ -244,12 +275,19 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
           for (int q = 0; q < 4; ++q) v[q] = v[q] > 0.f ? v[q] : 0.f;
         }
       }
-      if (VEC) {
-        if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
-      } else {
+      // p.Y set: one destination of leading dimension N (sdnn_spmm); else every yo.y[d] (sdnn_spmm_multi)
+      const bool single = piece || p.Y;
+      for (int d = 0; d < (single ? 1 : p.yo.n); ++d) {
+        float* yrow = piece    ? p.ws + int64_t(-2 - orow) * p.N
+                      : single ? p.Y + int64_t(orow) * p.N
+                               : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
+        if (VEC) {
+          if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (n + q < p.N) yrow[n + q] = v[q];
+          for (int q = 0; q < 4; ++q)
+            if (n + q < p.N) yrow[n + q] = v[q];
+        }
       }
     }
   }
@@ -258,7 +296,7 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
 // Split rows (row plan): Y[row] = act(Σ_pieces ws[piece] (in piece order) + b[row]).  One thread per
 // column; blockIdx.y = split row.  split = {rows[ns], first piece[ns], piece count[ns]}.
 __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t* __restrict__ split, int32_t ns,
-                                    const float* __restrict__ bias, int32_t act, float* __restrict__ Y, int64_t N) {
+                                    const float* __restrict__ bias, int32_t act, const YOut yo, int64_t N) {
   const int32_t sr = int32_t(blockIdx.y);
   const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (n >= N) return;
@@ -267,14 +305,14 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t*
   for (int32_t k = 1; k < cnt; ++k) v += ws[int64_t(first + k) * N + n];
   if (bias) v += bias[row];
   if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
-  Y[int64_t(row) * N + n] = v;
+  for (int d = 0; d < yo.n; ++d) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
 }
 
 // Fast path: TMA producer warp + W_c consumer warps, mbarrier stage ring.
 // KIND 1 = row kernel (RW rows per warp), KIND 2 = group kernel (RW = 16).
 template <int KIND, int RW, int V, int SB = 0>
 __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 32, 1)
-    spmm_tma_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+    spmm_tma_kernel(const __grid_constant__ CUtensorMap tmap, const KParamsY p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -334,7 +372,7 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
 // Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
 // threads using bounds-checked loads (zero fill) and a block barrier instead of TMA/mbarriers.
 template <int KIND, int RW, int V, int SB = 0>
-__global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) spmm_generic_kernel(const KParams p) {
+__global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) spmm_generic_kernel(const KParamsY p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -481,8 +519,8 @@ template <> struct TmemLd<8> {
 
 // Consumer warp of TMEM lane quarter q, warp slot wi: the chunk loop (wait for the chunk's
 // metadata and TMEM half, 4 / 2 nonzeros per step: tcgen05.ld → FFMA2) and the fused epilogue.
-template <int V>
-__device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, uint64_t* mfull, uint64_t* mempty,
+template <int V, bool MULTI>
+__device__ __forceinline__ void tmem_consume(const TmemParams<MULTI>& p, uint8_t* mring, uint64_t* mfull, uint64_t* mempty,
                                              uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0, int q, int wi,
                                              int lane) {
   constexpr int RW = tmem_rows(V);
@@ -573,7 +611,7 @@ __device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, u
     const int32_t orow = p.row_orig[(rb * kTmemPanels + wi) * RW + r];
     if (orow < 0) continue;
     const float b = p.bias ? p.bias[orow] : 0.f;
-    float* yrow = p.Y + int64_t(orow) * p.N;
+    float* yrow = MULTI ? nullptr : p.Y + int64_t(orow) * p.N;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int64_t n = n0 + g * 512 + q * 128 + lane * 4;
@@ -582,7 +620,14 @@ __device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, u
 #pragma unroll
         for (int t = 0; t < 4; ++t) v[t] = v[t] > 0.f ? v[t] : 0.f;
       }
-      if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
+      if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
+        if (n < p.N)
+          for (int d = 0; d < p.yo.n; ++d)
+            __stcs(reinterpret_cast<float4*>(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n),
+                   make_float4(v[0], v[1], v[2], v[3]));
+      } else {
+        if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
+      }
     }
   }
 }
@@ -597,9 +642,9 @@ __device__ __forceinline__ void tmem_consume(const KParams& p, uint8_t* mring, u
 template <int FILL> __host__ __device__ constexpr int tmem_side_warps() { return FILL ? 4 : 1; }
 // FILL 2: odd pieces of a chunk by tcgen05.cp (issued by filler 0 lane 0), even pieces by the four
 // filler warps with tcgen05.st — the two fill paths run side by side.
-template <int V, int FILL>
+template <int V, int FILL, bool MULTI = false>
 __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 32, 1)
-    spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+    spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI> p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 128 * V;
   constexpr int KC = tmem_kc(V);
@@ -772,7 +817,7 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
     // one code copy for all four lane quarters (four specialised copies exceed the SM's
     // instruction cache: profiles/r01_tmem_fill_diag.log)
     if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0
-    tmem_consume<V>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp & 3, warp >> 2, lane);
+    tmem_consume<V, MULTI>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp & 3, warp >> 2, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -831,9 +876,12 @@ static int occupancy(const void* fn, int threads, size_t smem) {
 }
 
 static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                                  float* Y, cudaStream_t stream) {
+                                  const YOut& yo, cudaStream_t stream) {
   const Plan& pl = h->plan;
   if (N >= (int64_t(1) << 30)) return fail(SDNN_ERR_UNSUPPORTED, "codegen kernel needs N < 2^30");
+  if (yo.n != 1 || yo.ld != N || yo.col0 != 0)
+    return fail(SDNN_ERR_UNSUPPORTED, "the codegen kernel writes one dense M×N output");
+  float* Y = yo.y[0];
   const int32_t tile = 32 * pl.cg_warps;
   uint32_t ntiles = uint32_t((N + tile - 1) / tile);
   uint64_t px = reinterpret_cast<uint64_t>(X), py = reinterpret_cast<uint64_t>(Y),
@@ -859,19 +907,20 @@ static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, c
 }
 
 static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                               float* Y, cudaStream_t stream) {
+                               const YOut& yo, cudaStream_t stream) {
   const Plan& pl = h->plan;
   const int V = tmem_v(pl.kernel), TN = 128 * V;
   const int64_t ntiles = (N + TN - 1) / TN;
   const int64_t nblocks = ntiles * pl.num_row_blocks;
   if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "N too large for one launch");
-  KParams p{};
+  KParamsY p{};
   p.meta = h->d_meta;
   p.blk_off = h->d_blk_off;
   p.row_orig = h->d_row_orig;
   p.X = X;
   p.bias = bias;
-  p.Y = Y;
+  p.yo = yo;
+  p.Y = (yo.n == 1 && yo.ld == N && yo.col0 == 0) ? yo.y[0] : nullptr;
   p.N = N;
   p.K = pl.K;
   p.nch = pl.num_chunks;
@@ -910,9 +959,13 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   const int fill = fill_env >= 0 ? fill_env : pl.tmem_fill;
   const unsigned threads = unsigned(kTmemConsumers + (fill ? 4 : 1)) * 32;
   const unsigned grid = unsigned(nblocks);
-  if (V == 8 && fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
+  const bool multi = !(yo.n == 1 && yo.ld == N && yo.col0 == 0);
+  if (multi && fill != 1) return fail(SDNN_ERR_UNSUPPORTED, "multi-destination TMEM launch needs the filler-warp fill");
+  if (V == 8 && multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (V == 8 && fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
   else if (V == 8 && fill == 1) spmm_tmem_kernel<8, 1><<<grid, threads, smem, stream>>>(tmap, p);
   else if (V == 8) spmm_tmem_kernel<8, 0><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (multi) spmm_tmem_kernel<4, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
   else if (fill == 2) spmm_tmem_kernel<4, 2><<<grid, threads, smem, stream>>>(tmap, p);
   else if (fill == 1) spmm_tmem_kernel<4, 1><<<grid, threads, smem, stream>>>(tmap, p);
   else spmm_tmem_kernel<4, 0><<<grid, threads, smem, stream>>>(tmap, p);
@@ -923,23 +976,22 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
 // The TMEM kernel runs one CTA per SM and pays once the call has at least half a wave of CTAs
 // (measured per config, profiles/r01_configs_v5.log: it wins from ~100 CTAs up — c2 3072×768,
 // c3 512² — while the row kernel, several CTAs per SM, wins on c3 256×128 (65 TMEM CTAs) and below).
-static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const float* Y) {
-  return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 &&
+static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const YOut& yo) {
+  return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo) &&
          2 * int64_t(a->plan.num_row_blocks) * ((N + 128 * tmem_v(a->plan.kernel) - 1) / (128 * tmem_v(a->plan.kernel))) >=
              a->sms;
 }
 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                               float* Y, float* ws, cudaStream_t stream);
+                               const YOut& yo, float* ws, cudaStream_t stream);
 
-static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
+static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, const YOut& yo,
                           cudaStream_t stream) {
-  if (tmem_worth(h->alt, X, N, Y)) return launch_tmem(h->alt, X, N, bias, act, Y, stream);
+  if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
-  if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, Y, stream);
-  if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
-      reinterpret_cast<uintptr_t>(Y) % 16 == 0)
-    return launch_tmem(h, X, N, bias, act, Y, stream);
+  if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
+  if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))
+    return launch_tmem(h, X, N, bias, act, yo, stream);
   // split rows (row plan): a stream-ordered workspace for the pieces' partial sums, reduced after
   // the main kernel (no host synchronisation; allocation nodes under CUDA-graph capture)
   float* ws = nullptr;
@@ -948,11 +1000,11 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
     SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ws), pl.piece_row.size() * size_t(N) * 4,
                                           h->ws_pool, stream));
   }
-  sdnn_status st = launch_main(h, X, N, bias, act, Y, ws, stream);
+  sdnn_status st = launch_main(h, X, N, bias, act, yo, ws, stream);
   if (ns > 0) {
     if (st == SDNN_OK) {
       const dim3 grid{unsigned((N + 255) / 256), unsigned(ns)};
-      split_reduce_kernel<<<grid, 256, 0, stream>>>(ws, h->d_split, ns, bias, act, Y, N);
+      split_reduce_kernel<<<grid, 256, 0, stream>>>(ws, h->d_split, ns, bias, act, yo, N);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("split_reduce_kernel: ") + cudaGetErrorString(le));
     }
@@ -962,8 +1014,8 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
 }
 
 // The row / group / generic kernels of a plan (everything but TMEM and codegen).
-static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, float* Y,
-                               float* ws, cudaStream_t stream) {
+static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                               const YOut& yo, float* ws, cudaStream_t stream) {
   const Plan& pl = h->plan;
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
@@ -975,13 +1027,14 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   const int64_t nblocks = ntiles * pl.num_row_blocks;
   if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "N too large for one launch");
 
-  KParams p{};
+  KParamsY p{};
   p.meta = h->d_meta;
   p.blk_off = h->d_blk_off;
   p.row_orig = h->d_row_orig;
   p.X = X;
   p.bias = bias;
-  p.Y = Y;
+  p.yo = yo;
+  p.Y = (yo.n == 1 && yo.ld == N && yo.col0 == 0) ? yo.y[0] : nullptr;
   p.N = N;
   p.K = pl.K;
   p.nch = pl.num_chunks;
@@ -994,8 +1047,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   p.act = act;
   p.ws = ws;
 
-  const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
-                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0) && pl.kernel < 4;
+  const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) && y_aligned16(yo) && pl.kernel < 4;
   if (fast) {
     const int sb = pl.group_sb;
     const void* fn = nullptr;
@@ -1144,6 +1196,12 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
   });
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     cudaFree(h->d_meta);
@@ -1289,7 +1347,32 @@ sdnn_status sdnn_spmm(sdnn_handle h, const float* X, int64_t N, const float* bia
     return fail(SDNN_ERR_INVALID_ARGUMENT, "Y overlaps X or bias");
   sdnn_status st = check_device(h);
   if (st != SDNN_OK) return st;
-  return launch(h, X, N, bias, act, Y, static_cast<cudaStream_t>(stream));
+  return launch(h, X, N, bias, act, y_single(Y, N), static_cast<cudaStream_t>(stream));
+}
+
+sdnn_status sdnn_spmm_multi(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act,
+                            float* const* Y_dsts, int32_t n_dst, int64_t ldy, int64_t col0, void* stream) {
+  if (!h) return fail(SDNN_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (N < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "N < 0");
+  if (act != SDNN_ACT_NONE && act != SDNN_ACT_RELU) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown act");
+  if (!Y_dsts || n_dst < 1 || n_dst > kMaxDst) return fail(SDNN_ERR_INVALID_ARGUMENT, "need 1..8 destinations");
+  if (col0 < 0 || ldy < col0 + N) return fail(SDNN_ERR_INVALID_ARGUMENT, "need col0 >= 0 and ldy >= col0 + N");
+  if (N == 0) return SDNN_OK;
+  if (!X) return fail(SDNN_ERR_INVALID_ARGUMENT, "X is NULL");
+  YOut yo{};
+  yo.n = n_dst;
+  yo.ld = ldy;
+  yo.col0 = col0;
+  const size_t span = (size_t(h->plan.M - 1) * size_t(ldy) + size_t(col0 + N)) * 4;
+  for (int32_t d = 0; d < n_dst; ++d) {
+    if (!Y_dsts[d]) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL destination");
+    yo.y[d] = Y_dsts[d];
+    if (overlaps(Y_dsts[d], span, X, size_t(h->plan.K) * size_t(N) * 4) || overlaps(Y_dsts[d], span, bias, size_t(h->plan.M) * 4))
+      return fail(SDNN_ERR_INVALID_ARGUMENT, "a destination overlaps X or bias");
+  }
+  sdnn_status st = check_device(h);
+  if (st != SDNN_OK) return st;
+  return launch(h, X, N, bias, act, yo, static_cast<cudaStream_t>(stream));
 }
 
 sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const float* bias_host, int32_t act,
@@ -1366,7 +1449,7 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
       ck(cudaStreamWaitEvent(s[1], hs.ev[0][b], 0), "cudaStreamWaitEvent");
       ck(cudaStreamWaitEvent(s[1], hs.ev[2][b], 0), "cudaStreamWaitEvent");
       if (rs == SDNN_OK) {
-        sdnn_status ls = launch(h, hs.x[b], w, bd, act, hs.y[b], s[1]);
+        sdnn_status ls = launch(h, hs.x[b], w, bd, act, y_single(hs.y[b], w), s[1]);
         if (ls != SDNN_OK) { rs = ls; msg = sdnn_last_error_message(); }
       }
       ck(cudaEventRecord(hs.ev[1][b], s[1]), "cudaEventRecord");
@@ -1384,12 +1467,13 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
 
 sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const float* Y, int32_t* kernel) {
   if (!h || !kernel || N < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle / kernel or N < 0");
-  if (tmem_worth(h->alt, X, N, Y)) {
+  const YOut yo = y_single(const_cast<float*>(Y), N);
+  if (tmem_worth(h->alt, X, N, yo)) {
     *kernel = h->alt->plan.kernel;
     return SDNN_OK;
   }
   const int k = h->plan.kernel;
-  const bool tma = N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0;
+  const bool tma = N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo);
   *kernel = (k == 4 || k == 5) ? (N % 128 == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
   return SDNN_OK;
 }

@@ -332,3 +332,36 @@ def test_large_k_and_large_m(sdnn, oracle_mod, kernel):
     for M, K, N, dens in [(96, 40000, 256, 0.01), (20000, 64, 128, 0.05)]:
         p = synth.make_problem(f"big_{M}x{K}", M, K, N, 1 - dens, seed=M + K)
         check(sdnn, oracle_mod, p, kernel=kernel)
+
+
+# ------------------------------------------------------------------ fused all-gather form (sdnn_spmm_multi)
+@pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "tmem8"])
+@pytest.mark.parametrize("key,N", [("c3_512x512", 1024), ("c3_512x512", 1000), ("c2_768x768", 512), ("c1", 128)])
+def test_spmm_multi_destinations(sdnn, key, N, kernel):
+    """Y written to 3 buffers of leading dimension ldy at column offset col0 (the all-gather layout a
+    rank writes into every peer's symmetric buffer): each equals the plain result, untouched elsewhere."""
+    p = synth.config_problem(key, N=N)
+    h = sdnn.Handle.from_problem(p, kernel=kernel)
+    X = torch.from_numpy(p.x()).cuda()
+    b = torch.from_numpy(p.bias).cuda()
+    ref = h.spmm(X, b, act=1).clone()
+    col0, ldy = 256, N + 512
+    bufs = [torch.full((p.M, ldy), -7.0, device="cuda") for _ in range(3)]
+    h.spmm_multi(X, [t.data_ptr() for t in bufs], ldy, col0, bias=b, act=1)
+    torch.cuda.synchronize()
+    for t in bufs:
+        assert torch.equal(t[:, col0:col0 + N], ref)
+        assert bool((t[:, :col0] == -7.0).all()) and bool((t[:, col0 + N:] == -7.0).all())
+
+
+def test_spmm_multi_errors(sdnn):
+    p = synth.config_problem("c1")
+    h = sdnn.Handle.from_problem(p)
+    X = torch.zeros((p.K, 8), device="cuda")
+    Y = torch.zeros((p.M, 8), device="cuda")
+    with pytest.raises(sdnn.SdnnError):
+        h.spmm_multi(X, [], 8, 0)
+    with pytest.raises(sdnn.SdnnError):
+        h.spmm_multi(X, [Y.data_ptr()] * 9, 8, 0)
+    with pytest.raises(sdnn.SdnnError):
+        h.spmm_multi(X, [Y.data_ptr()], 7, 0)  # ldy < col0 + N
