@@ -39,11 +39,9 @@ KERNEL = "spmm_tma_kernel"
 
 # ----------------------------------------------------------------------------- sharding / reductions
 def shard_range(N: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous column block of rank r: [r·N/g, (r+1)·N/g) with the remainder spread over the
-    first ranks, rounded so every shard but the last starts at a multiple of 4 (TMA alignment)."""
-    base = (N // world) // 4 * 4
-    starts = [r * base for r in range(world)] + [N]
-    return starts[rank], starts[rank + 1]
+    """Contiguous column block of rank r (paper_2101_07948_b200.gather.column_bounds)."""
+    from paper_2101_07948_b200.gather import column_bounds
+    return column_bounds(N, world)[rank]
 
 
 def max_over_ranks(x: float, dist=None) -> float:
@@ -277,8 +275,12 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
         err = np.abs(Ys.astype(np.float64) - Yo) / np.where(S > 0, S, 1.0)
         parity = max_over_ranks(float(err.max()), dist)
 
-    # ---- optional Y all-gather over NVLink (NCCL), reported separately
-    ag_ms = None
+    # ---- optional Y all-gather, reported separately from the SpMM step:
+    # nccl = all_gather_into_tensor of the shards after the step (collective alone);
+    # fused = the whole step with the gather in the epilogue (sdnn_spmm_multi into every rank's
+    # symmetric-memory Y + barrier), to set beside ms_per_step
+    ag_ms = fused_ms = None
+    fused_ok = None
     if args.allgather and world > 1:
         Yall = torch.empty((world, p.M, Nr), dtype=torch.float32, device=dev)
         for _ in range(2):
@@ -293,6 +295,36 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
         torch.cuda.synchronize()
         ag_ms = max_over_ranks(a0.elapsed_time(a1) / 3, dist)
         del Yall
+        try:
+            from paper_2101_07948_b200.gather import FusedGather, column_bounds
+            # strong: the shards tile n_total; weak: every rank's Nr columns side by side
+            gb = ([(r * Nr, (r + 1) * Nr) for r in range(world)] if args.scaling == "weak"
+                  else column_bounds(args.n_total, world))
+            fg = FusedGather(p.M, gb[-1][1], gb, device=dev)
+        except Exception as e:  # no symmetric memory / multicast on this box: NCCL number only
+            print(f"fused all-gather unavailable: {e}", file=sys.stderr)
+            fg = None
+        if fg is not None:
+            for _ in range(2):
+                fg.spmm(h, X, bias, act=1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a0.record(stream)
+            for _ in range(3):
+                fg.spmm(h, X, bias, act=1)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            fused_ms = max_over_ranks(a0.elapsed_time(a1) / 3, dist)
+            # every rank's columns arrived intact (bitwise: same kernel, same per-column order)
+            ok = bool(torch.equal(fg.Y[:, gb[rank][0]:gb[rank][1]], Y))
+            # peers' blocks: fp64 checksum of each rank's own shard against its block in our Y
+            sums = torch.zeros(world, dtype=torch.float64, device=dev)
+            sums[rank] = Y.sum(dtype=torch.float64)
+            dist.all_reduce(sums)
+            got = torch.stack([fg.Y[:, a:b].sum(dtype=torch.float64) for a, b in gb])
+            ok = ok and bool(torch.allclose(got, sums, rtol=1e-9, atol=1e-6))
+            fused_ok = max_over_ranks(0.0 if ok else 1.0, dist) == 0.0
+            del fg
 
     # ---- e2e through the public host-buffer API (H2D of X + bias, D2H of Y inside the timed region)
     Yh = torch.empty((p.M, Nr), dtype=torch.float32, pin_memory=True)
@@ -361,6 +393,8 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
         "clocks": clk.summary(),
         "parity_max_err_over_scale": parity,
         "allgather_ms": None if ag_ms is None else round(ag_ms, 3),
+        "fused_allgather_step_ms": None if fused_ms is None else round(fused_ms, 3),
+        "fused_allgather_ok": fused_ok,
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -36,9 +36,46 @@ def _worker(rank, world, port, q):
         Y, _ = oracle.spmm(p.row_ptr, p.col_idx, p.vals, p.M, p.K, p.x_cols(c0, c1), p.bias, act=1, want_scale=False)
         parts = [None] * world
         dist.all_gather_object(parts, (c0, c1, Y))
+        # unfused Y all-gather (gather.nccl_gather; gloo here): every rank gets the full M×N Y
+        from paper_2101_07948_b200.gather import column_bounds, nccl_gather
+        import torch
+        Yg = nccl_gather(torch.from_numpy(Y), column_bounds(p.N, world)).numpy()
+        Yfull, _ = oracle.spmm(p.row_ptr, p.col_idx, p.vals, p.M, p.K, p.x(), p.bias, act=1, want_scale=False)
+        assert np.array_equal(Yg, Yfull)
         q.put((rank, c0, c1, t, same, differ, parts if rank == 0 else None))
     finally:
         dist.destroy_process_group()
+
+
+def _gather_worker(rank, world, port, N, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from paper_2101_07948_b200.gather import column_bounds, nccl_gather
+        bounds = column_bounds(N, world)
+        c0, c1 = bounds[rank]
+        full = torch.arange(5 * N, dtype=torch.float32).reshape(5, N)
+        got = nccl_gather(full[:, c0:c1].contiguous(), bounds)
+        q.put((rank, bool(torch.equal(got, full))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,world", [(10, 3), (9, 2)])
+def test_nccl_gather_ragged_shards(N, world):
+    """Unequal (and empty) column blocks are padded for the collective and trimmed after."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, N, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(ok for _, ok in res)
 
 
 def test_two_rank_gloo(oracle_mod):
