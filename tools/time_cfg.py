@@ -21,8 +21,15 @@ def main():
     ap.add_argument("--kernel", default="tmem")
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--shape", default="", help="MxK:sparsity, e.g. 4096x2048:0.9 (uniform mask; overrides --config)")
     a = ap.parse_args()
-    p = synth.config_problem(a.config)
+    if a.shape:
+        mk, sp = a.shape.split(":")
+        M, K = (int(v) for v in mk.split("x"))
+        p = synth.make_problem(a.shape, M, K, a.n or 65536, float(sp))
+        a.config = a.shape
+    else:
+        p = synth.config_problem(a.config)
     N = a.n or p.N
     X = torch.randn((p.K, N), device="cuda")
     b = torch.from_numpy(p.bias).cuda()
