@@ -102,6 +102,8 @@ typedef struct {
                                small kernel, in piece order, before the bias: deterministic, but not
                                bitwise equal to the unsplit summation order)                          */
   int32_t num_pieces;       /* total pieces of the split rows                                         */
+  int32_t narrow_row_blocks; /* auto handles: row blocks of the narrow row plan (4-row panels) taken by
+                               row-plan calls whose grid is under one wave; 0 = none                 */
 } sdnn_info;
 
 /* sdnn_perm_opts.flags */

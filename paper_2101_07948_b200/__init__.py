@@ -55,7 +55,8 @@ class Info(ctypes.Structure):
                 ("panel_rows", ctypes.c_int32), ("cta_panels", ctypes.c_int32), ("num_panels", ctypes.c_int32),
                 ("num_row_blocks", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("meta_bytes", ctypes.c_int64), ("max_block_bytes", ctypes.c_int32), ("alt_kernel", ctypes.c_int32),
-                ("max_panel_nnz", ctypes.c_int64), ("num_split_rows", ctypes.c_int32), ("num_pieces", ctypes.c_int32)]
+                ("max_panel_nnz", ctypes.c_int64), ("num_split_rows", ctypes.c_int32), ("num_pieces", ctypes.c_int32),
+                ("narrow_row_blocks", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "struct_size"}

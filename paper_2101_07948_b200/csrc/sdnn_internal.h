@@ -72,8 +72,10 @@ const DriverApi& driver();
 sdnn_status codegen_build(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t K,
                           const std::vector<std::vector<int32_t>>& panels, int32_t warps, int32_t D,
                           std::vector<CUmodule>& mods, std::vector<CUfunction>& funcs, int32_t threads);
+// perm: a permutation already computed for this matrix (another plan of the same handle), so
+// Algorithm 1 runs once per handle; nullptr → computed here (or identity when opts->permute = 0).
 sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
-                       const sdnn_perm_opts* opts, Plan& plan);
+                       const sdnn_perm_opts* opts, Plan& plan, const std::vector<int32_t>* perm = nullptr);
 
 // Shared-memory budget used for the X/metadata stage ring (bytes) and the fixed CTA layout.
 constexpr int kSmemBudget = 220 * 1024;

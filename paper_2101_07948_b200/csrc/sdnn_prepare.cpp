@@ -265,7 +265,7 @@ static int32_t stages_for(int32_t kc, int64_t max_block) {
 }
 
 sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M, int32_t K,
-                       const sdnn_perm_opts* opts, Plan& plan) {
+                       const sdnn_perm_opts* opts, Plan& plan, const std::vector<int32_t>* perm) {
   sdnn_perm_opts o{};
   o.struct_size = sizeof(o);
   o.permute = 1;
@@ -307,7 +307,9 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     plan.nnz = nnz;
     plan.permuted = o.permute;
     plan.perm.resize(M);
-    if (o.permute)
+    if (o.permute && perm && perm->size() == size_t(M))
+      plan.perm = *perm;
+    else if (o.permute)
       algorithm1(csr_ptr, col_idx, M, K, plan.perm.data());
     else
       for (int32_t i = 0; i < M; ++i) plan.perm[i] = i;
@@ -597,6 +599,7 @@ static void fill_info(const Plan& p, int32_t device, sdnn_info* info) {
   info->max_panel_nnz = p.max_panel_nnz;
   info->num_split_rows = int32_t(p.split_row.size());
   info->num_pieces = int32_t(p.piece_row.size());
+  info->narrow_row_blocks = 0;
 }
 
 namespace sdnn {

@@ -66,6 +66,9 @@ struct sdnn_handle_s {
   // auto handles (kernel = 0): the TMEM plan prepared beside the row plan; sdnn_spmm takes it when
   // the call fits its fast path and fills at least one wave of CTAs (tmem_worth)
   sdnn_handle_s* alt = nullptr;
+  // auto handles: a row plan with more, smaller row blocks, for row-plan calls whose grid on the
+  // main row plan is under one wave (small N: one or two N tiles)
+  sdnn_handle_s* narrow = nullptr;
   int32_t sms = 148;
   HostStage hs;         // sdnn_spmm_host staging (created on first use)
   std::mutex host_mu;
@@ -177,11 +180,23 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
   constexpr int TN = 32 * V;
   const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + warp * RW;
   const float4* ent = reinterpret_cast<const float4*>(ms + hdr_bytes);
-  const float* xl = xs + lane * 4;
+  const float* xl = xs + lane * (V == 2 ? 2 : 4);
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
     const uint32_t h = hdr[r];
-    const int cnt = int(TF ? (h & 0xffu) : (h & 0xffffu));  // TMEM format: bits 8..15 count leading runs
+    const int cnt = int(TF ? (h & 0xffu) : (h & 0xffffu));
+    if constexpr (V == 2) {  // 2 columns of N per lane (TN = 64): small-N calls, twice the warps
+      const float4* e2 = ent + (h >> 16) / 2;
+      for (int i = 0; i < cnt; i += 2) {
+        const float4 ee = e2[i >> 1];
+        acc[r][0] = __ffma2_rn(make_float2(ee.y, ee.y), *reinterpret_cast<const float2*>(xl + __float_as_int(ee.x) * TN),
+                               acc[r][0]);
+        if (i + 1 < cnt)
+          acc[r][0] = __ffma2_rn(make_float2(ee.w, ee.w),
+                                 *reinterpret_cast<const float2*>(xl + __float_as_int(ee.z) * TN), acc[r][0]);
+      }
+      continue;
+    }  // TMEM format: bits 8..15 count leading runs
     const float4* e = ent + (h >> 16) / 2;
     for (int i = 0; i < cnt; i += 2) {
       const float4 ee = e[i >> 1];
@@ -262,6 +277,32 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
     // `piece`; split_reduce_kernel adds the pieces, the bias and the activation
     const bool piece = orow <= -2;
     const float b = (piece || !p.bias) ? 0.f : p.bias[orow];
+    if constexpr (V == 2) {
+      const int64_t n = n0 + lane * 2;
+      const float2 a0 = as_f2(acc[r][0]);
+      float v[2] = {a0.x, a0.y};
+      if (!piece) {
+        v[0] += b;
+        v[1] += b;
+        if (p.act == SDNN_ACT_RELU) {
+          v[0] = v[0] > 0.f ? v[0] : 0.f;
+          v[1] = v[1] > 0.f ? v[1] : 0.f;
+        }
+      }
+      const bool single = piece || p.Y;
+      for (int d = 0; d < (single ? 1 : p.yo.n); ++d) {
+        float* yrow = piece    ? p.ws + int64_t(-2 - orow) * p.N
+                      : single ? p.Y + int64_t(orow) * p.N
+                               : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
+        if (VEC) {
+          if (n < p.N) __stcs(reinterpret_cast<float2*>(yrow + n), make_float2(v[0], v[1]));
+        } else {
+          if (n < p.N) yrow[n] = v[0];
+          if (n + 1 < p.N) yrow[n + 1] = v[1];
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int h = 0; h < V / 4; ++h) {
       const int64_t n = n0 + h * 128 + lane * 4;
@@ -985,9 +1026,33 @@ static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                const YOut& yo, float* ws, cudaStream_t stream);
 
+// N-tile width of the row / group kernels for a call: V = 8 floats per lane (TN = 256) when that
+// still gives ≥ 2 CTAs per SM worth of work units, else V = 4 (TN = 128).
+static int row_tile_v(const Plan& pl, int64_t N) {
+  return int64_t(pl.num_row_blocks) * ((N + 255) / 256) < 2 * 148 ? 4 : 8;
+}
+// Row kernel only: V = 2 (TN = 64, twice the warps and CTAs) when the V = 4 grid is under half a
+// wave, or under one wave with CTAs of ≤ 8 warps (profiles/r01_row_small_n.log: 1024², 70 %,
+// N = 128: 44 → 26 µs; with 16-warp CTAs a 1.7-wave V = 2 grid lost: 4096², N = 256, 91 → 121 µs).
+static int row_tile_v_small(const Plan& pl, int64_t N, int sms) {
+  const int v = row_tile_v(pl, N);
+  if (pl.kernel != 1 || v != 4) return v;
+  const int64_t g4 = int64_t(pl.num_row_blocks) * ((N + 127) / 128);
+  return (2 * g4 <= sms || (g4 < sms && pl.cta_panels <= 8)) ? 2 : 4;
+}
+// Row-plan call whose grid (row blocks × N tiles) is under one wave: the narrow plan (more row
+// blocks of 4-row panels) fills the GPU instead (profiles/r01_row_geometry.log: 4096², N = 128:
+// 166 → 90 µs; 2048², N = 512: 70 → 50 µs).
+static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
+  if (!h->narrow) return false;
+  const int64_t tn = 32 * row_tile_v(h->plan, N);
+  return int64_t(h->plan.num_row_blocks) * ((N + tn - 1) / tn) < h->sms;
+}
+
 static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, const YOut& yo,
                           cudaStream_t stream) {
   if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
+  if (narrow_worth(h, N)) return launch(h->narrow, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
   if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))
@@ -1019,8 +1084,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   const Plan& pl = h->plan;
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
-  int V = 8;
-  if (int64_t(pl.num_row_blocks) * ((N + 255) / 256) < 2 * 148) V = 4;
+  int V = row_tile_v_small(pl, N, h->sms);
   if (pl.kernel == 4 || pl.kernel == 5) V = 4;  // TMEM plan, ragged / unaligned call: generic kernel
   const int TN = 32 * V;
   const int64_t ntiles = (N + TN - 1) / TN;
@@ -1059,8 +1123,10 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
     else if (pl.kernel == 2) fn = reinterpret_cast<const void*>(spmm_tma_kernel<2, 16, 4, 4>);
     else if (rw == 8 && V == 8) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 8, 8>);
     else if (rw == 8 && V == 4) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 8, 4>);
+    else if (rw == 8) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 8, 2>);
     else if (rw == 4 && V == 8) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 4, 8>);
-    else fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 4, 4>);
+    else if (V == 4) fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 4, 4>);
+    else fn = reinterpret_cast<const void*>(spmm_tma_kernel<1, 4, 2>);
     const int threads = (wc + 1) * 32;
     auto smem_for = [&](int S) { return size_t(S) * (p.x_stage_bytes + p.m_stage_bytes) + size_t(2 * S) * 8; };
     int S = int(kSmemBudget / (p.x_stage_bytes + p.m_stage_bytes));
@@ -1121,8 +1187,10 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
     else if (pl.kernel == 5) spmm_generic_kernel<5, tmem_rows(8), 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 8) spmm_generic_kernel<1, 8, 8><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 4) spmm_generic_kernel<1, 8, 4><<<grid, block, smem, stream>>>(p);
+    else if (rw == 8) spmm_generic_kernel<1, 8, 2><<<grid, block, smem, stream>>>(p);
     else if (rw == 4 && V == 8) spmm_generic_kernel<1, 4, 8><<<grid, block, smem, stream>>>(p);
-    else spmm_generic_kernel<1, 4, 4><<<grid, block, smem, stream>>>(p);
+    else if (V == 4) spmm_generic_kernel<1, 4, 4><<<grid, block, smem, stream>>>(p);
+    else spmm_generic_kernel<1, 4, 2><<<grid, block, smem, stream>>>(p);
   }
   SDNN_CUDA_TRY(cudaGetLastError());
   return SDNN_OK;
@@ -1146,7 +1214,8 @@ static sdnn_status check_device(const sdnn_handle_s* h) {
 extern "C" {
 
 static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M,
-                               int32_t K, const sdnn_perm_opts* perm_opts, sdnn_handle* out) {
+                               int32_t K, const sdnn_perm_opts* perm_opts, sdnn_handle* out,
+                               const std::vector<int32_t>* perm = nullptr) {
   if (!out) return fail(SDNN_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   int dev = -1;
@@ -1158,7 +1227,7 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
                                           std::to_string(prop.major) + std::to_string(prop.minor));
   sdnn_handle_s* h = new (std::nothrow) sdnn_handle_s;
   if (!h) return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
-  sdnn_status st = build_plan(csr_ptr, col_idx, vals, M, K, perm_opts, h->plan);
+  sdnn_status st = build_plan(csr_ptr, col_idx, vals, M, K, perm_opts, h->plan, perm);
   if (st != SDNN_OK) {
     delete h;
     return st;
@@ -1172,6 +1241,8 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     if (ae == cudaSuccess) ae = set_smem_attrs<1, 8, 4>();
     if (ae == cudaSuccess) ae = set_smem_attrs<1, 4, 8>();
     if (ae == cudaSuccess) ae = set_smem_attrs<1, 4, 4>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<1, 8, 2>();
+    if (ae == cudaSuccess) ae = set_smem_attrs<1, 4, 2>();
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8, 1>();
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8, 2>();
     if (ae == cudaSuccess) ae = set_smem_attrs<2, 16, 8, 4>();
@@ -1283,8 +1354,9 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
   o.struct_size = sizeof(o);
   o.permute = perm_opts ? perm_opts->permute : 1;
   o.kernel = 4;
+  const std::vector<int32_t>* perm = &(*out)->plan.perm;  // Algorithm 1 once per handle
   sdnn_handle alt = nullptr;
-  st = prepare_one(csr_ptr, col_idx, vals, M, K, &o, &alt);
+  st = prepare_one(csr_ptr, col_idx, vals, M, K, &o, &alt, perm);
   if (st != SDNN_OK) {
     std::string m = sdnn_last_error_message();
     sdnn_destroy(*out);
@@ -1292,12 +1364,37 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
     return fail(st, m);
   }
   (*out)->alt = alt;
+  // and, when the row plan has few row blocks, a row plan of 4-row panels with ≥ 64 row blocks for
+  // the calls whose grid would not fill the GPU (launch: narrow_worth)
+  const Plan& wide = (*out)->plan;
+  if (wide.kernel == 1 && !(perm_opts && (perm_opts->panel_rows_max || perm_opts->cta_panels))) {
+    int32_t wc = 16;
+    while (wc > 4 && (M + 4 * wc - 1) / (4 * wc) < 64) wc /= 2;
+    if ((M + 4 * wc - 1) / (4 * wc) > wide.num_row_blocks) {
+      sdnn_perm_opts n = perm_opts ? *perm_opts : sdnn_perm_opts{};
+      n.struct_size = sizeof(n);
+      if (!perm_opts) n.permute = 1;
+      n.kernel = 1;
+      n.panel_rows_max = 4;
+      n.cta_panels = wc;
+      sdnn_handle nar = nullptr;
+      st = prepare_one(csr_ptr, col_idx, vals, M, K, &n, &nar, perm);
+      if (st != SDNN_OK) {
+        std::string m = sdnn_last_error_message();
+        sdnn_destroy(*out);
+        *out = nullptr;
+        return fail(st, m);
+      }
+      (*out)->narrow = nar;
+    }
+  }
   return SDNN_OK;
 }
 
 sdnn_status sdnn_destroy(sdnn_handle h) {
   if (!h) return SDNN_OK;
   if (h->alt) sdnn_destroy(h->alt);
+  if (h->narrow) sdnn_destroy(h->narrow);
   int cur = -1;
   cudaGetDevice(&cur);
   if (cur != h->device) cudaSetDevice(h->device);
@@ -1472,6 +1569,7 @@ sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const flo
     *kernel = h->alt->plan.kernel;
     return SDNN_OK;
   }
+  if (narrow_worth(h, N)) return sdnn_spmm_kernel(h->narrow, N, X, Y, kernel);
   const int k = h->plan.kernel;
   const bool tma = N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo);
   *kernel = (k == 4 || k == 5) ? (N % 128 == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
@@ -1490,6 +1588,7 @@ sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info) {
   plan_fill_info(h->plan, h->device, info);
   info->meta_bytes = h->plan.meta_size_uploaded;
   info->alt_kernel = h->alt ? h->alt->plan.kernel : 0;
+  info->narrow_row_blocks = h->narrow ? h->narrow->plan.num_row_blocks : 0;
   return SDNN_OK;
 }
 

@@ -273,6 +273,26 @@ def test_auto_takes_tmem_plan_when_it_fills_a_wave(sdnn):
     assert h.kernel_for(p.N) == 4 and h.kernel_for(102) == -1 and h.kernel_for(128) == 1  # 35·1·2 < 148
 
 
+@pytest.mark.parametrize("M,K,sp", [(2048, 2048, 0.9), (4096, 1024, 0.7)])
+def test_auto_narrow_row_plan_for_small_grids(sdnn, oracle_mod, M, K, sp):
+    """An auto handle whose row plan has few row blocks also keeps a narrow row plan (4-row panels,
+    ≥ 64 row blocks, same permutation) for row-plan calls under one wave of CTAs (small N).  Same
+    per-row accumulation order → bitwise equal to the row plan; oracle parity."""
+    p = synth.make_problem(f"narrow{M}", M, K, 256, sp)
+    h = sdnn.Handle.from_problem(p)
+    info = h.info()
+    assert info["narrow_row_blocks"] >= 64 and info["narrow_row_blocks"] > info["num_row_blocks"]
+    hr = sdnn.Handle.from_problem(p, kernel="row")
+    assert hr.info()["narrow_row_blocks"] == 0
+    for N in (128, 256, 100):
+        X = np.ascontiguousarray(p.x()[:, :N])
+        Ya, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+        Yr, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=hr)
+        np.testing.assert_array_equal(Ya, Yr)
+        Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, want_scale=True)[:2]
+        assert_parity(Ya, Yo, S, f"narrow N={N}")
+
+
 def test_get_permutation_and_info(sdnn, oracle_mod):
     p = synth.config_problem("c2_768x768")
     h = sdnn.Handle.from_problem(p)

@@ -1,0 +1,4 @@
+for v in A B; do SDNN_PKG_DIR=ab/$v timeout 900 python tools/bench_configs.py --variants auto --graph > gpurun_out/geom_cfg_$v.jsonl 2> gpurun_out/geom_cfg_$v.err; done
+for v in A B; do for shape in 4096x4096:0.9 2048x2048:0.9 1024x1024:0.9 4096x4096:0.7 2048x2048:0.7; do for n in 128 256 512 1000 2048; do
+  SDNN_PKG_DIR=ab/$v timeout 120 python tools/time_cfg.py --shape $shape --n $n --kernel auto --iters 20 | sed "s/^/$v /"
+done; done; done

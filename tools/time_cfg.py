@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--kernel", default="tmem")
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--opts", default="", help="handle options, e.g. panel_rows=4,cta_panels=4")
     ap.add_argument("--shape", default="", help="MxK:sparsity, e.g. 4096x2048:0.9 (uniform mask; overrides --config)")
     a = ap.parse_args()
     if a.shape:
@@ -35,7 +36,8 @@ def main():
     b = torch.from_numpy(p.bias).cuda()
     Y = torch.empty((p.M, N), device="cuda")
     for k in a.kernel.split(","):
-        h = sdnn.Handle.from_problem(p, kernel=k)
+        opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opts.split(",") if kv}
+        h = sdnn.Handle.from_problem(p, kernel=k, **opts)
         for _ in range(2):
             h.spmm(X, b, act=1, out=Y)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -45,7 +47,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
-        print(f"{a.config} N={N} {k:8s} lib={sdnn.LIB_PATH.split('/')[-3]} dbg={os.environ.get('SDNN_DEBUG_TMEM', '0')} {ms:9.3f} ms "
+        print(f"{a.config} N={N} {k:8s} {a.opts:24s} lib={sdnn.LIB_PATH.split('/')[-3]} dbg={os.environ.get('SDNN_DEBUG_TMEM', '0')} {ms:9.3f} ms "
               f"{2 * p.nnz * N / ms / 1e9:8.2f} TF", flush=True)
         h.close()
 
