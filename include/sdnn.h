@@ -74,7 +74,7 @@ typedef struct {
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
                                multiple of 8                                                        */
   int32_t group_sb;         /* group kernel sub-block rows: 0 = auto (cost model), 1, 2 or 4         */
-  uint32_t flags;           /* SDNN_FLAG_NO_ROW_SPLIT or 0                                            */
+  uint32_t flags;           /* SDNN_FLAG_NO_ROW_SPLIT | SDNN_FLAG_PERMUTED_OUTPUT, or 0               */
 } sdnn_perm_opts;
 
 /* Read-only description of a prepared handle (or a host plan). */
@@ -108,6 +108,12 @@ typedef struct {
 
 /* sdnn_perm_opts.flags */
 #define SDNN_FLAG_NO_ROW_SPLIT 1u  /* row plan: never split a row across warps                         */
+/* Y rows (and bias entries) in the plan's row order instead of the original order: sdnn_spmm writes
+ * Y_perm[i] = act(W[order[i]]·X + b_perm[i]) with order = sdnn_get_permutation and the caller's bias
+ * given as b_perm[i] = b[order[i]].  The paper's cross-layer form: the next layer consumes
+ * Y_perm after its columns are relabelled the same way (sdnn_csr_permute_columns), so no layer
+ * un-permutes.  Not with the codegen kernel (kernel = 3: SDNN_ERR_UNSUPPORTED). */
+#define SDNN_FLAG_PERMUTED_OUTPUT 2u
 
 typedef struct sdnn_handle_s* sdnn_handle; /* opaque; owns its device memory; immutable after prepare */
 typedef struct sdnn_plan_s* sdnn_plan;     /* opaque host-only plan (no device needed)               */
@@ -179,6 +185,17 @@ SDNN_API sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info);
  * Validates the CSR like sdnn_prepare. */
 SDNN_API sdnn_status sdnn_permutation(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K,
                              int32_t* order);
+
+/* sdnn_csr_permute_columns: the CSR of W·P, P the permutation matrix of `order` (HOST, K entries,
+ * order[i] = the original column that moves to position i; a bijection of 0..K−1): every entry
+ * (r, c, w) becomes (r, pos(c), w) with order[pos(c)] = c, each row re-sorted by its new columns.
+ * out_col_idx / out_vals: HOST, nnz = csr_ptr[M] entries each (row pointers are unchanged).  For
+ * the next layer of a chain whose previous layer ran with SDNN_FLAG_PERMUTED_OUTPUT.
+ * Errors: SDNN_ERR_INVALID_CSR (as sdnn_prepare), SDNN_ERR_INVALID_ARGUMENT (NULL, not a
+ * permutation). */
+SDNN_API sdnn_status sdnn_csr_permute_columns(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals,
+                                              int32_t M, int32_t K, const int32_t* order, int32_t* out_col_idx,
+                                              float* out_vals);
 
 /* sdnn_plan_create: everything sdnn_prepare does except the upload, on host.  sdnn_plan_export
  * copies the plan's arrays into caller HOST buffers sized from sdnn_plan_get_info:

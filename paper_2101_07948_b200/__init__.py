@@ -28,7 +28,7 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
 EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_spmm_host", "sdnn_spmm_kernel",
            "sdnn_get_permutation",
            "sdnn_get_info",
-           "sdnn_permutation", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_export_pieces",
+           "sdnn_permutation", "sdnn_csr_permute_columns", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_export_pieces",
            "sdnn_plan_destroy",
            "sdnn_plan_codegen_ptx", "sdnn_status_string", "sdnn_last_error_message", "sdnn_abi_version"]
 
@@ -72,6 +72,7 @@ _lib.sdnn_get_permutation.argtypes = [_vp, _vp]
 _lib.sdnn_spmm_kernel.argtypes = [_vp, _i64, _vp, _vp, ctypes.POINTER(_i32)]
 _lib.sdnn_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
+_lib.sdnn_csr_permute_columns.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
 _lib.sdnn_plan_create.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts), ctypes.POINTER(_vp)]
 _lib.sdnn_plan_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_plan_export.argtypes = [_vp, _vp, _vp, _vp]
@@ -106,12 +107,15 @@ KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4, "tmem8": 5}
 
 
 FLAG_NO_ROW_SPLIT = 1
+FLAG_PERMUTED_OUTPUT = 2
 
 
-def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0, split_rows=True):
+def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0, split_rows=True,
+          permuted_output=False):
     k = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+    flags = (0 if split_rows else FLAG_NO_ROW_SPLIT) | (FLAG_PERMUTED_OUTPUT if permuted_output else 0)
     return PermOpts(ctypes.sizeof(PermOpts), int(bool(permute)), k, int(panel_rows), int(cta_panels), int(k_chunk),
-                    int(group_sb), 0 if split_rows else FLAG_NO_ROW_SPLIT)
+                    int(group_sb), flags)
 
 
 def _act(act) -> int:
@@ -126,6 +130,20 @@ def permutation(row_ptr, col_idx, M: int, K: int) -> np.ndarray:
     order = np.empty(M, dtype=np.int32)
     _check(_lib.sdnn_permutation(_np_ptr(rp), _np_ptr(ci), M, K, _np_ptr(order)), "sdnn_permutation")
     return order
+
+
+def permute_columns(row_ptr, col_idx, vals, M: int, K: int, order) -> tuple[np.ndarray, np.ndarray]:
+    """CSR of W·P (sdnn_csr_permute_columns): column order[i] moves to position i, rows re-sorted.
+    Returns (col_idx', vals'); row_ptr is unchanged."""
+    rp, ci, v = _csr(row_ptr, col_idx, vals)
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    if order.shape != (K,):
+        raise ValueError("order must have K entries")
+    oc = np.empty_like(ci)
+    ov = np.empty_like(v)
+    _check(_lib.sdnn_csr_permute_columns(_np_ptr(rp), _np_ptr(ci), _np_ptr(v), M, K, _np_ptr(order), _np_ptr(oc),
+                                         _np_ptr(ov)), "sdnn_csr_permute_columns")
+    return oc, ov
 
 
 class Plan:
@@ -278,3 +296,55 @@ class Handle:
 
 def abi_version() -> int:
     return _lib.sdnn_abi_version()
+
+
+class Chain:
+    """Layers Y_{l+1} = act_l(W_l·Y_l + b_l) run back to back.
+
+    Every layer but the last is prepared with SDNN_FLAG_PERMUTED_OUTPUT, so its output rows stay in
+    that layer's Algorithm 1 order and nothing is un-permuted between layers; the next layer's
+    columns are relabelled the same way at preparation (sdnn_csr_permute_columns), and its bias is
+    taken in its own plan order.  The last layer writes the original row order.  Intermediates are
+    preallocated per N and reused (the GPU form of the paper's buffer reuse; at the BERT FFN shapes
+    they stay in the 126 MB L2).  layers: [(row_ptr, col_idx, vals, M, K, bias | None, act), ...].
+    """
+
+    def __init__(self, layers, **opts):
+        import torch
+        self.handles, self.biases, self.acts = [], [], []
+        prev_order, prev_M = None, None
+        for i, (rp, ci, v, M, K, bias, act) in enumerate(layers):
+            if prev_M is not None and K != prev_M:
+                raise ValueError(f"layer {i}: K = {K} but the previous layer has M = {prev_M}")
+            if prev_order is not None:
+                ci, v = permute_columns(rp, ci, v, M, K, prev_order)
+            last = i == len(layers) - 1
+            h = Handle(rp, ci, v, M, K, permuted_output=not last, **opts)
+            order = h.permutation()
+            b = None
+            if bias is not None:
+                b = np.ascontiguousarray(np.asarray(bias, np.float32) if last else np.asarray(bias, np.float32)[order])
+                b = torch.from_numpy(b).cuda()
+            self.handles.append(h)
+            self.biases.append(b)
+            self.acts.append(act)
+            prev_order, prev_M = order, M
+        self.K = layers[0][4]
+        self.M = layers[-1][3]
+        self._bufs = {}
+
+    def forward(self, X, out=None, stream=None):
+        """X: CUDA float32 (K_0, N); returns the last layer's (M_L, N) output in original row order."""
+        import torch
+        N = X.shape[1]
+        bufs = self._bufs.get(N)
+        if bufs is None:
+            bufs = [torch.empty((h.M, N), dtype=torch.float32, device=X.device) for h in self.handles[:-1]]
+            self._bufs = {N: bufs}
+        cur = X
+        for i, h in enumerate(self.handles):
+            last = i == len(self.handles) - 1
+            dst = out if last else bufs[i]
+            cur = h.spmm(cur, self.biases[i], act=self.acts[i], out=dst, stream=stream)
+        return cur
+

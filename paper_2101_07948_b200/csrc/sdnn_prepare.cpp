@@ -273,7 +273,10 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     if (opts->struct_size != sizeof(sdnn_perm_opts))
       return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.struct_size mismatch");
     o = *opts;
-    if (o.flags & ~SDNN_FLAG_NO_ROW_SPLIT) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown sdnn_perm_opts.flags bits");
+    if (o.flags & ~(SDNN_FLAG_NO_ROW_SPLIT | SDNN_FLAG_PERMUTED_OUTPUT))
+      return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown sdnn_perm_opts.flags bits");
+    if ((o.flags & SDNN_FLAG_PERMUTED_OUTPUT) && o.kernel == 3)
+      return fail(SDNN_ERR_UNSUPPORTED, "SDNN_FLAG_PERMUTED_OUTPUT is not available with the codegen kernel");
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
     if (o.kernel < 0 || o.kernel > 5) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..5");
     if (o.kernel == 4 || o.kernel == 5) {
@@ -563,6 +566,16 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     for (size_t i = 0; i < sizes.size(); ++i) plan.blk_off[i + 1] = plan.blk_off[i] + sizes[i];
     plan.meta.assign(size_t(plan.blk_off.back()), 0);
     emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, plan.meta.data(), &plan.blk_off, nullptr, &pcs);
+    if (o.flags & SDNN_FLAG_PERMUTED_OUTPUT) {
+      // output rows (and bias entries) by plan position instead of original row; the
+      // metadata above was emitted from the original rows' CSR entries, so this comes last
+      std::vector<int32_t> pos(static_cast<size_t>(M));
+      for (int32_t i = 0; i < M; ++i) pos[size_t(plan.perm[i])] = i;
+      for (auto& r : plan.row_orig)
+        if (r >= 0) r = pos[size_t(r)];
+      for (auto& r : plan.split_row) r = pos[size_t(r)];
+      plan.permuted_output = 1;
+    }
   } catch (const std::bad_alloc&) {
     return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed during planning");
   }
@@ -631,6 +644,35 @@ sdnn_status sdnn_permutation(const int32_t* csr_ptr, const int32_t* col_idx, int
   if (st != SDNN_OK) return st;
   try {
     algorithm1(csr_ptr, col_idx, M, K, order);
+  } catch (const std::bad_alloc&) {
+    return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
+  }
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_csr_permute_columns(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M,
+                                     int32_t K, const int32_t* order, int32_t* out_col_idx, float* out_vals) {
+  if (!order || !out_col_idx || !out_vals) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL order or output");
+  sdnn_status st = validate_csr(csr_ptr, col_idx, M, K);
+  if (st != SDNN_OK) return st;
+  if (csr_ptr[M] > 0 && !vals) return fail(SDNN_ERR_INVALID_ARGUMENT, "vals is NULL with nnz > 0");
+  try {
+    std::vector<int32_t> pos(size_t(K), -1);
+    for (int32_t i = 0; i < K; ++i) {
+      const int32_t c = order[i];
+      if (c < 0 || c >= K || pos[size_t(c)] != -1) return fail(SDNN_ERR_INVALID_ARGUMENT, "order is not a permutation of 0..K-1");
+      pos[size_t(c)] = i;
+    }
+    std::vector<std::pair<int32_t, float>> row;
+    for (int32_t r = 0; r < M; ++r) {
+      row.clear();
+      for (int32_t p = csr_ptr[r]; p < csr_ptr[r + 1]; ++p) row.emplace_back(pos[size_t(col_idx[p])], vals[p]);
+      std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (size_t i = 0; i < row.size(); ++i) {
+        out_col_idx[csr_ptr[r] + int32_t(i)] = row[i].first;
+        out_vals[csr_ptr[r] + int32_t(i)] = row[i].second;
+      }
+    }
   } catch (const std::bad_alloc&) {
     return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
   }

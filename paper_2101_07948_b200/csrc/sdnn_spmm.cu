@@ -1354,6 +1354,7 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
   o.struct_size = sizeof(o);
   o.permute = perm_opts ? perm_opts->permute : 1;
   o.kernel = 4;
+  o.flags = perm_opts ? (perm_opts->flags & SDNN_FLAG_PERMUTED_OUTPUT) : 0u;  // TMEM plans never split rows
   const std::vector<int32_t>* perm = &(*out)->plan.perm;  // Algorithm 1 once per handle
   sdnn_handle alt = nullptr;
   st = prepare_one(csr_ptr, col_idx, vals, M, K, &o, &alt, perm);
