@@ -6,6 +6,8 @@ Plain CPU definitions of what the SparseDNN hot path computes, written from the 
   * spmm_omp(...)        → the OpenMP-over-rows timing variant (bitwise identical).
   * alg1(...)            → liboracle.so `oracle_alg1` (Algorithm 1, bitset brute force).
   * alg1_bruteforce(...) → the same algorithm in pure Python over sets, for tiny inputs.
+  * conv.conv2d(...)     → sparse k×k convolution by its definition (numpy, fp64),
+                           pinned by tests/test_conv_oracle.py.
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference` leg may use
 this package.  It shares no code with paper_2101_07948_b200/ (the CUDA path) and imports nothing

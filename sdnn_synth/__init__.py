@@ -231,3 +231,62 @@ def desk_grid():
             for N in (32, 128):
                 for seed in range(3):
                     yield dict(name=f"desk_{n}_{int(round(s * 100))}_{N}", M=n, K=n, N=N, sparsity=s, seed=seed)
+
+
+# ----------------------------------------------------------------------------- sparse convolution
+@dataclasses.dataclass
+class ConvProblem:
+    """Sparse k×k convolution: filters OC×IC×FY×FX stored as
+    the CSR of the OC × (IC·FY·FX) matrix (column = (ic·FY + fy)·FX + fx), activations in
+    the C×(B·H·W) layout of the 1×1 convs (reading C17): X[ic][b][y][x], Y[oc][b][oy][ox]."""
+    name: str
+    OC: int
+    IC: int
+    H: int
+    W: int
+    B: int
+    FY: int
+    FX: int
+    pad: int
+    stride: int
+    sparsity: float
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    vals: np.ndarray
+    bias: np.ndarray | None
+    act: int
+    seed: int
+
+    @property
+    def K(self) -> int:
+        return self.IC * self.FY * self.FX
+
+    @property
+    def Ho(self) -> int:
+        return (self.H + 2 * self.pad - self.FY) // self.stride + 1
+
+    @property
+    def Wo(self) -> int:
+        return (self.W + 2 * self.pad - self.FX) // self.stride + 1
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    def x(self) -> np.ndarray:
+        """Input activations, float32 [IC][B][H][W], N(0, 1)."""
+        return _rng(self.seed, self.name, T_X).standard_normal((self.IC, self.B, self.H, self.W), dtype=np.float32)
+
+
+def make_conv_problem(name: str, OC: int, IC: int, H: int, W: int, B: int, sparsity: float, FY: int = 3,
+                      FX: int = 3, pad: int = 1, stride: int = 1, bias: bool = True, act: int = ACT_RELU,
+                      seed: int = 0) -> ConvProblem:
+    """The paper's conv suite: random (uniform-mask) sparse filters at 90 / 95 %, IC/OC 32-256,
+    images 7/14/28/56, 3×3, pad 1; values N(0, 0.05) like the SpMM weights."""
+    K = IC * FY * FX
+    nnz = nnz_target(OC, K, sparsity)
+    row_ptr, cols = mask_uniform(OC, K, nnz, _rng(seed, name, T_MASK))
+    vals = weight_values(nnz, _rng(seed, name, T_VALS))
+    b = (0.1 * _rng(seed, name, T_BIAS).standard_normal(OC)).astype(np.float32) if bias else None
+    return ConvProblem(name, OC, IC, H, W, B, FY, FX, pad, stride, float(sparsity), row_ptr.astype(np.int32),
+                       cols.astype(np.int32), vals.astype(np.float32), b, act, seed)
