@@ -169,6 +169,23 @@ SDNN_API sdnn_status sdnn_spmm_multi(sdnn_handle h, const float* X, int64_t N, c
 SDNN_API sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const float* bias_host, int32_t act,
                            float* Y_host, int64_t block_cols);
 
+/* sdnn_conv2d: sparse k×k convolution (§3.2.3, "treated as an SpMM where the sparse
+ * matrix is the filters treated as an OC by IC × Fx × Fy matrix ... the dense matrix is a virtual
+ * matrix that is realized on the fly from the input dense activations with the proper offsets").
+ *   h       a handle prepared from the filters as the CSR of the OC × (IC·FY·FX) matrix, column
+ *           (ic·FY + fy)·FX + fx, with a row plan without split rows (kernel 0 or 1 and
+ *           SDNN_FLAG_NO_ROW_SPLIT); else SDNN_ERR_UNSUPPORTED.  K must equal IC·FY·FX.
+ *   X       DEVICE fp32 [IC][B][H][W] (the C×(B·H·W) activation layout of the 1×1 convs).
+ *   Y       DEVICE fp32 [OC][B][Ho][Wo], Ho = (H + 2·pad − FY)/stride + 1 (same for Wo), written in
+ *           original output-channel order; bias fp32[OC] or NULL; act as sdnn_spmm.
+ *   Y[oc][b][oy][ox] = act(Σ W[oc][ic][fy][fx] · X[ic][b][oy·stride + fy − pad][ox·stride + fx − pad]
+ *                          + bias[oc]), taps outside the image contribute 0.
+ * Enqueued on `stream`, no host sync.  B = 0 → SDNN_OK, nothing done.  Errors as sdnn_spmm, plus
+ * SDNN_ERR_INVALID_ARGUMENT for an empty output or K ≠ IC·FY·FX. */
+SDNN_API sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, int32_t H, int32_t W,
+                                 int32_t FY, int32_t FX, int32_t pad, int32_t stride, const float* bias, int32_t act,
+                                 float* Y, void* stream);
+
 /* ------------------------------------------------------------------ introspection
  * sdnn_get_permutation: out_perm (HOST, M entries) receives order[i] = original row at permuted
  * position i (Algorithm 1 output, SPEC S:295 convention).  sdnn_get_info fills *info. */

@@ -25,7 +25,7 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
           4: "SDNN_ERR_OUT_OF_MEMORY", 5: "SDNN_ERR_CUDA", 6: "SDNN_ERR_DEVICE_MISMATCH", 7: "SDNN_ERR_INTERNAL"}
 
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
-EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_spmm_host", "sdnn_spmm_kernel",
+EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_spmm_host", "sdnn_spmm_kernel",
            "sdnn_get_permutation",
            "sdnn_get_info",
            "sdnn_permutation", "sdnn_csr_permute_columns", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_export_pieces",
@@ -73,6 +73,7 @@ _lib.sdnn_spmm_kernel.argtypes = [_vp, _i64, _vp, _vp, ctypes.POINTER(_i32)]
 _lib.sdnn_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
 _lib.sdnn_csr_permute_columns.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
+_lib.sdnn_conv2d.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]
 _lib.sdnn_plan_create.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts), ctypes.POINTER(_vp)]
 _lib.sdnn_plan_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_plan_export.argtypes = [_vp, _vp, _vp, _vp]
@@ -246,6 +247,27 @@ class Handle:
         s = torch.cuda.current_stream(X.device) if stream is None else stream
         _check(_lib.sdnn_spmm(self._h, X.data_ptr(), N, None if bias is None else bias.data_ptr(), _act(act),
                               out.data_ptr(), s.cuda_stream), "sdnn_spmm")
+        return out
+
+    def conv2d(self, X, FY: int = 3, FX: int = 3, pad: int = 1, stride: int = 1, bias=None, act="relu", out=None,
+               stream=None):
+        """Sparse convolution (sdnn_conv2d): X CUDA float32 [IC][B][H][W] → [OC][B][Ho][Wo]; the handle
+        holds the filters as the OC × (IC·FY·FX) CSR (prepare with split_rows=False)."""
+        import torch
+        if X.dim() != 4 or X.dtype != torch.float32 or not X.is_cuda or not X.is_contiguous():
+            raise ValueError("X must be a contiguous CUDA float32 [IC][B][H][W] tensor")
+        IC, B, H, W = X.shape
+        Ho, Wo = (H + 2 * pad - FY) // stride + 1, (W + 2 * pad - FX) // stride + 1
+        if out is None:
+            out = torch.empty((self.M, B, Ho, Wo), dtype=torch.float32, device=X.device)
+        elif out.shape != (self.M, B, Ho, Wo) or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float32 [OC][B][Ho][Wo] tensor")
+        if bias is not None and (bias.numel() != self.M or bias.dtype != torch.float32 or not bias.is_cuda):
+            raise ValueError("bias must be a CUDA float32 tensor of OC elements")
+        s = torch.cuda.current_stream(X.device) if stream is None else stream
+        _check(_lib.sdnn_conv2d(self._h, X.data_ptr(), B, IC, H, W, FY, FX, pad, stride,
+                                None if bias is None else bias.data_ptr(), _act(act), out.data_ptr(), s.cuda_stream),
+               "sdnn_conv2d")
         return out
 
     def spmm_multi(self, X, dst_ptrs, ldy: int, col0: int, bias=None, act="relu", stream=None):

@@ -450,6 +450,91 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) 
   epilogue<RW, V, false>(acc, p, rb * p.wc + warp, lane, n0);
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// Sparse k×k convolution (§3.2.3): the filters are the OC × (IC·FY·FX)
+// sparse matrix of a row plan (column k = (ic·FY + fy)·FX + fx), and the dense operand is the
+// virtual matrix X_v[k][n] = X[ic][b][oy·s + fy − pad][ox·s + fx − pad] (0 outside the image),
+// n = (b·Ho + oy)·Wo + ox, "realized on the fly from the input dense activations with the proper
+// offsets".  Same consumption and fused epilogue as the row kernel; the X stage is gathered by every
+// thread with 4-byte cp.async (src-size 0 → zero fill for the padding taps), double-buffered so the
+// gather of chunk j + 1 overlaps the FMAs of chunk j.  Y is OC × (B·Ho·Wo) = [OC][B][Ho][Wo].
+struct ConvGeom {
+  int32_t B, IC, H, W, Ho, Wo, FY, FX, pad, stride;
+};
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int RW, bool VEC>
+__global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p, const ConvGeom c) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int V = 4, TN = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = blockIdx.x % p.nrb;
+  const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
+  float* xs[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + p.x_stage_bytes)};
+  uint8_t* ms[2] = {smem + 2 * size_t(p.x_stage_bytes), smem + 2 * size_t(p.x_stage_bytes) + p.m_stage_bytes};
+  const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
+  // this thread's column of the stage (blockDim.x is a multiple of TN) and its output pixel
+  const int nn = int(threadIdx.x) % TN, kk0 = int(threadIdx.x) / TN, kstep = int(blockDim.x) / TN;
+  const int64_t n = n0 + nn;
+  const bool col_ok = n < p.N;
+  const int HWo = c.Ho * c.Wo, FYX = c.FY * c.FX;
+  const int bimg = col_ok ? int(n / HWo) : 0;
+  const int rem = col_ok ? int(n - int64_t(bimg) * HWo) : 0;
+  const int iy0 = (rem / c.Wo) * c.stride - c.pad, ix0 = (rem % c.Wo) * c.stride - c.pad;
+  const float* xb = p.X + int64_t(bimg) * c.H * c.W;  // + ic·B·H·W + iy·W + ix
+  const int64_t icstride = int64_t(c.B) * c.H * c.W;
+  auto gather = [&](int j, int buf) {
+    int k = j * p.kc + kk0;
+    int ic = k / FYX, t = k - ic * FYX;
+    for (int kk = kk0; kk < p.kc; kk += kstep) {
+      const int fy = t / c.FX, fx = t - fy * c.FX;
+      const int iy = iy0 + fy, ix = ix0 + fx;
+      const bool ok = col_ok && k < p.K && iy >= 0 && iy < c.H && ix >= 0 && ix < c.W;
+      const float* src = ok ? xb + ic * icstride + int64_t(iy) * c.W + ix : p.X;
+      cp_async4(xs[buf] + kk * TN + nn, src, ok);
+      k += kstep;
+      t += kstep;
+      while (t >= FYX) {
+        t -= FYX;
+        ++ic;
+      }
+    }
+    const int mbytes = int(off[j + 1] - off[j]);
+    const uint8_t* msrc = p.meta + off[j];
+    for (int i = int(threadIdx.x); i < mbytes / 16; i += int(blockDim.x)) cp_async16(ms[buf] + 16 * i, msrc + 16 * i);
+    cp_async_commit();
+  };
+  float2 acc[RW][V / 2];
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) acc[r][q] = make_float2(0.f, 0.f);
+  gather(0, 0);
+  for (int j = 0; j < p.nch; ++j) {
+    if (j + 1 < p.nch) {
+      gather(j + 1, (j + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    consume_chunk<RW, V>(acc, xs[j & 1], ms[j & 1], warp, lane, p.hdr_bytes);
+    __syncthreads();
+  }
+  epilogue<RW, V, VEC>(acc, p, rb * p.wc + warp, lane, n0);
+}
+
 // ------------------------------------------------------------------------------------------------
 // TMEM kernel (DESIGN.md §6 "TMEM kernel").  The row kernel reads one 4-byte X operand per FMA from
 // shared memory, and shared memory delivers 128 B/clk/SM — a 25 % ceiling on the FMA pipe.  Tensor
@@ -1471,6 +1556,68 @@ sdnn_status sdnn_spmm_multi(sdnn_handle h, const float* X, int64_t N, const floa
   sdnn_status st = check_device(h);
   if (st != SDNN_OK) return st;
   return launch(h, X, N, bias, act, yo, static_cast<cudaStream_t>(stream));
+}
+
+sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, int32_t H, int32_t W, int32_t FY,
+                        int32_t FX, int32_t pad, int32_t stride, const float* bias, int32_t act, float* Y,
+                        void* stream) {
+  if (!h) return fail(SDNN_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (B < 0 || IC < 1 || H < 1 || W < 1 || FY < 1 || FX < 1 || pad < 0 || stride < 1)
+    return fail(SDNN_ERR_INVALID_ARGUMENT, "need B >= 0, IC, H, W, FY, FX, stride >= 1 and pad >= 0");
+  if (act != SDNN_ACT_NONE && act != SDNN_ACT_RELU) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown act");
+  const Plan& pl = h->plan;
+  if (int64_t(IC) * FY * FX != pl.K)
+    return fail(SDNN_ERR_INVALID_ARGUMENT, "handle K = " + std::to_string(pl.K) + " != IC·FY·FX");
+  if (pl.kernel != 1 || !pl.split_row.empty())
+    return fail(SDNN_ERR_UNSUPPORTED, "sdnn_conv2d needs a row plan without split rows (kernel 0 or 1, "
+                                      "SDNN_FLAG_NO_ROW_SPLIT)");
+  const int32_t Ho = (H + 2 * pad - FY) / stride + 1, Wo = (W + 2 * pad - FX) / stride + 1;
+  if (H + 2 * pad < FY || W + 2 * pad < FX || Ho < 1 || Wo < 1)
+    return fail(SDNN_ERR_INVALID_ARGUMENT, "empty output (filter larger than the padded image)");
+  const int64_t N = int64_t(B) * Ho * Wo;
+  if (N == 0) return SDNN_OK;
+  if (!X || !Y) return fail(SDNN_ERR_INVALID_ARGUMENT, "X or Y is NULL");
+  if (overlaps(Y, size_t(pl.M) * size_t(N) * 4, X, size_t(IC) * B * H * W * 4) ||
+      overlaps(Y, size_t(pl.M) * size_t(N) * 4, bias, size_t(pl.M) * 4))
+    return fail(SDNN_ERR_INVALID_ARGUMENT, "Y overlaps X or bias");
+  sdnn_status st = check_device(h);
+  if (st != SDNN_OK) return st;
+  constexpr int TN = 128;
+  const int rw = pl.panel_rows, wc = pl.cta_panels;
+  if (wc < 4) return fail(SDNN_ERR_UNSUPPORTED, "sdnn_conv2d needs >= 4 panels per CTA");
+  const int64_t nblocks = int64_t(pl.num_row_blocks) * ((N + TN - 1) / TN);
+  if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "output too large for one launch");
+  KParamsY p{};
+  p.meta = h->d_meta;
+  p.blk_off = h->d_blk_off;
+  p.row_orig = h->d_row_orig;
+  p.X = X;
+  p.bias = bias;
+  p.yo = y_single(Y, N);
+  p.Y = Y;
+  p.N = N;
+  p.K = pl.K;
+  p.nch = pl.num_chunks;
+  p.kc = pl.k_chunk;
+  p.wc = wc;
+  p.nrb = pl.num_row_blocks;
+  p.x_stage_bytes = int32_t(align_up(int64_t(pl.k_chunk) * TN * 4, 128));
+  p.m_stage_bytes = int32_t(align_up(pl.max_block_bytes, 128));
+  p.hdr_bytes = int32_t(align_up(int64_t(rw) * wc * 4, 16));
+  p.act = act;
+  const ConvGeom cg{B, IC, H, W, Ho, Wo, FY, FX, pad, stride};
+  const size_t smem = 2 * size_t(p.x_stage_bytes) + 2 * size_t(p.m_stage_bytes);
+  if (smem > size_t(kSmemBudget)) return fail(SDNN_ERR_INTERNAL, "conv stage does not fit shared memory");
+  const bool vec = N % 4 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0;
+  const void* fn = rw == 8 ? (vec ? reinterpret_cast<const void*>(spmm_conv_kernel<8, true>)
+                                  : reinterpret_cast<const void*>(spmm_conv_kernel<8, false>))
+                           : (vec ? reinterpret_cast<const void*>(spmm_conv_kernel<4, true>)
+                                  : reinterpret_cast<const void*>(spmm_conv_kernel<4, false>));
+  SDNN_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  void* args[] = {&p, const_cast<ConvGeom*>(&cg)};
+  SDNN_CUDA_TRY(cudaLaunchKernel(fn, dim3(unsigned(nblocks)), dim3(unsigned(wc * 32)), args, smem,
+                                 static_cast<cudaStream_t>(stream)));
+  return SDNN_OK;
 }
 
 sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const float* bias_host, int32_t act,
