@@ -535,6 +535,126 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
   epilogue<RW, V, VEC>(acc, p, rb * p.wc + warp, lane, n0);
 }
 
+// Patch form (the default): per K chunk the CTA stages the *input* rows its tile needs — the window
+// of the zero-padded input P[ic][b·Hp + y + pad][x + pad] (Hp = H + 2·pad, Wp = W + 2·pad) covering
+// the tile's output rows and the filter halo, for the chunk's input channels — instead of the FY·FX
+// shifted copies of the virtual matrix (≈ 4-9× fewer staged elements, one coalesced row per warp
+// step).  X_v[k][n] = patch[tab[k − k0] + pos(n)], tab = (ic − ic_lo)·PS + fy·Wp + fx per chunk
+// column, pos(n) = (b·Hp + oy·stride − vr0)·Wp + ox·stride per output pixel.  A lane owns the
+// pixels n0 + lane + 32q (q < 4), so each of its four loads per nonzero is a conflict-free
+// warp-contiguous read and the epilogue stores are coalesced.
+template <int RW>
+__global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p, const ConvGeom c, int32_t PSrows,
+                                                               int32_t ICC) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int TN = 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = int(blockDim.x) >> 5;
+  const int rb = blockIdx.x % p.nrb;
+  const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
+  const int Hp = c.H + 2 * c.pad, Wp = c.W + 2 * c.pad, PS = PSrows * Wp, FYX = c.FY * c.FX;
+  const int HWo = c.Ho * c.Wo;
+  const size_t stage = ((size_t(ICC) * PS * 4 + size_t(p.kc) * 4 + 127) & ~size_t(127)) + size_t(p.m_stage_bytes);
+  // srcoff[e], e < PS: offset of patch element e (row e / Wp, column e mod Wp) within one input
+  // channel, −1 for padding; the same for every channel and chunk of this tile (after both stages)
+  int32_t* srcoff = reinterpret_cast<int32_t*>(smem + 2 * stage);
+  float* patch[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + stage)};
+  int32_t* tab[2] = {reinterpret_cast<int32_t*>(patch[0] + size_t(ICC) * PS),
+                     reinterpret_cast<int32_t*>(patch[1] + size_t(ICC) * PS)};
+  uint8_t* ms[2] = {smem + stage - p.m_stage_bytes, smem + 2 * stage - p.m_stage_bytes};
+  const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
+  // the tile's first virtual input row, and each lane's four pixels
+  const int b0 = int(n0 / HWo), oy0 = int((n0 - int64_t(b0) * HWo) / c.Wo);
+  const int vr0 = b0 * Hp + oy0 * c.stride;
+  int po[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t n = n0 + lane + 32 * q;
+    const int b = int(n / HWo), rem = int(n - int64_t(b) * HWo), oy = rem / c.Wo, ox = rem - oy * c.Wo;
+    po[q] = n < p.N ? (b * Hp + oy * c.stride - vr0) * Wp + ox * c.stride : 0;
+  }
+  const int64_t icstride = int64_t(c.B) * c.H * c.W;
+  for (int e = int(threadIdx.x); e < PS; e += int(blockDim.x)) {
+    const int r = e / Wp, xp = e - r * Wp, vr = vr0 + r, b = vr / Hp, iy = vr - b * Hp - c.pad, ix = xp - c.pad;
+    srcoff[e] = (b < c.B && iy >= 0 && iy < c.H && ix >= 0 && ix < c.W) ? (b * c.H + iy) * c.W + ix : -1;
+  }
+  __syncthreads();
+  auto gather = [&](int j, int buf) {
+    const int k0 = j * p.kc, ic_lo = k0 / FYX;
+    for (int icl = 0; icl < ICC; ++icl) {  // the chunk's input channels, element-parallel over the patch
+      const int ic = ic_lo + icl;
+      const float* src = p.X + int64_t(ic < c.IC ? ic : 0) * icstride;
+      float* dst = patch[buf] + icl * PS;
+      for (int e = int(threadIdx.x); e < PS; e += int(blockDim.x)) {
+        const int so = srcoff[e];
+        const bool ok = so >= 0 && ic < c.IC;
+        cp_async4(dst + e, ok ? src + so : p.X, ok);
+      }
+    }
+    for (int cl = int(threadIdx.x); cl < p.kc; cl += int(blockDim.x)) {
+      const int k = k0 + cl, ic = k / FYX, t = k - ic * FYX, fy = t / c.FX, fx = t - fy * c.FX;
+      tab[buf][cl] = (ic - ic_lo) * PS + fy * Wp + fx;
+    }
+    const int mbytes = int(off[j + 1] - off[j]);
+    const uint8_t* msrc = p.meta + off[j];
+    for (int i = int(threadIdx.x); i < mbytes / 16; i += int(blockDim.x)) cp_async16(ms[buf] + 16 * i, msrc + 16 * i);
+    cp_async_commit();
+  };
+  float2 acc[RW][2];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+  gather(0, 0);
+  for (int j = 0; j < p.nch; ++j) {
+    if (j + 1 < p.nch) {
+      gather(j + 1, (j + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* xs = patch[j & 1];
+    const int32_t* tb = tab[j & 1];
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms[j & 1]) + warp * RW;
+    const float4* ent = reinterpret_cast<const float4*>(ms[j & 1] + p.hdr_bytes);
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const uint32_t h = hdr[r];
+      const int cnt = int(h & 0xffffu);
+      const float4* e = ent + (h >> 16) / 2;
+      for (int i = 0; i < cnt; i += 2) {
+        const float4 ee = e[i >> 1];
+        {
+          const float* xp = xs + tb[__float_as_int(ee.x)];
+          const float2 w2 = make_float2(ee.y, ee.y);
+          acc[r][0] = __ffma2_rn(w2, make_float2(xp[po[0]], xp[po[1]]), acc[r][0]);
+          acc[r][1] = __ffma2_rn(w2, make_float2(xp[po[2]], xp[po[3]]), acc[r][1]);
+        }
+        if (i + 1 < cnt) {
+          const float* xp = xs + tb[__float_as_int(ee.z)];
+          const float2 w2 = make_float2(ee.w, ee.w);
+          acc[r][0] = __ffma2_rn(w2, make_float2(xp[po[0]], xp[po[1]]), acc[r][0]);
+          acc[r][1] = __ffma2_rn(w2, make_float2(xp[po[2]], xp[po[3]]), acc[r][1]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // epilogue: + bias[orig], act, coalesced stores of pixels n0 + lane + 32q
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int32_t orow = p.row_orig[(rb * p.wc + warp) * RW + r];
+    if (orow < 0) continue;
+    const float bv = p.bias ? p.bias[orow] : 0.f;
+    float v[4] = {acc[r][0].x + bv, acc[r][0].y + bv, acc[r][1].x + bv, acc[r][1].y + bv};
+    float* yrow = p.Y + int64_t(orow) * p.N;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t n = n0 + lane + 32 * q;
+      const float y = p.act == SDNN_ACT_RELU ? (v[q] > 0.f ? v[q] : 0.f) : v[q];
+      if (n < p.N) __stcs(yrow + n, y);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------------
 // TMEM kernel (DESIGN.md §6 "TMEM kernel").  The row kernel reads one 4-byte X operand per FMA from
 // shared memory, and shared memory delivers 128 B/clk/SM — a 25 % ceiling on the FMA pipe.  Tensor
@@ -1584,7 +1704,6 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
   if (st != SDNN_OK) return st;
   constexpr int TN = 128;
   const int rw = pl.panel_rows, wc = pl.cta_panels;
-  if (wc < 4) return fail(SDNN_ERR_UNSUPPORTED, "sdnn_conv2d needs >= 4 panels per CTA");
   const int64_t nblocks = int64_t(pl.num_row_blocks) * ((N + TN - 1) / TN);
   if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "output too large for one launch");
   KParamsY p{};
@@ -1606,6 +1725,37 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
   p.hdr_bytes = int32_t(align_up(int64_t(rw) * wc * 4, 16));
   p.act = act;
   const ConvGeom cg{B, IC, H, W, Ho, Wo, FY, FX, pad, stride};
+  // patch form: the largest input window a tile needs (rows of the padded input, all images laid
+  // end to end) and the channels a K chunk can touch
+  {
+    const int64_t Hp = int64_t(H) + 2 * pad, HWo = int64_t(Ho) * Wo;
+    int64_t rows = 0;
+    for (int64_t n0 = 0; n0 < N; n0 += TN) {
+      const int64_t n1 = std::min<int64_t>(n0 + TN, N) - 1;
+      const int64_t b0 = n0 / HWo, oy0 = (n0 - b0 * HWo) / Wo, b1 = n1 / HWo, oy1 = (n1 - b1 * HWo) / Wo;
+      rows = std::max<int64_t>(rows, (b1 * Hp + oy1 * stride + FY - 1) - (b0 * Hp + oy0 * stride) + 1);
+    }
+    const int64_t FYX = int64_t(FY) * FX, ICC = (pl.k_chunk - 1) / FYX + 2;
+    const int64_t Wp = int64_t(W) + 2 * pad;
+    const size_t stage = align_up(int64_t(ICC * rows * Wp * 4 + int64_t(pl.k_chunk) * 4), 128) + size_t(p.m_stage_bytes);
+    static const int conv_env = [] {
+      const char* e = getenv("SDNN_CONV_GATHER");
+      return e ? atoi(e) : 0;
+    }();
+    const size_t smem2 = 2 * stage + size_t(rows * Wp) * 4;
+    if (conv_env == 0 && smem2 <= size_t(kSmemBudget) && rows * Wp < (int64_t(1) << 30)) {
+      const void* fn2 = rw == 8 ? reinterpret_cast<const void*>(spmm_conv2_kernel<8>)
+                                : reinterpret_cast<const void*>(spmm_conv2_kernel<4>);
+      SDNN_CUDA_TRY(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      int32_t psr = int32_t(rows), icc = int32_t(ICC);
+      void* args2[] = {&p, const_cast<ConvGeom*>(&cg), &psr, &icc};
+      SDNN_CUDA_TRY(cudaLaunchKernel(fn2, dim3(unsigned(nblocks)), dim3(unsigned(wc * 32)), args2, smem2,
+                                     static_cast<cudaStream_t>(stream)));
+      return SDNN_OK;
+    }
+  }
+  // gather form (very wide images, or SDNN_CONV_GATHER=1): the virtual matrix itself is staged
+  if (wc < 4) return fail(SDNN_ERR_UNSUPPORTED, "the gather form of sdnn_conv2d needs >= 4 panels per CTA");
   const size_t smem = 2 * size_t(p.x_stage_bytes) + 2 * size_t(p.m_stage_bytes);
   if (smem > size_t(kSmemBudget)) return fail(SDNN_ERR_INTERNAL, "conv stage does not fit shared memory");
   const bool vec = N % 4 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0;

@@ -24,16 +24,19 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
+    ap.add_argument("--cta-panels", type=int, default=0, help="row-plan warps per CTA (0 = auto)")
+    ap.add_argument("--sizes", default="32,64,128,256")
+    ap.add_argument("--images", default="7,14,28,56")
     a = ap.parse_args()
     torch.backends.cudnn.allow_tf32 = False
     torch.backends.cuda.matmul.allow_tf32 = False
     out = open(a.out, "w") if a.out else None
     sp_all = {0.9: [], 0.95: []}
-    for ch in (32, 64, 128, 256):
-        for hw in (7, 14, 28, 56):
+    for ch in (int(v) for v in a.sizes.split(",")):
+        for hw in (int(v) for v in a.images.split(",")):
             for sp in (0.9, 0.95):
                 p = synth.make_conv_problem(f"cb{ch}_{hw}_{sp}", ch, ch, hw, hw, a.batch, sp)
-                h = sdnn.Handle(p.row_ptr, p.col_idx, p.vals, p.OC, p.K, split_rows=False)
+                h = sdnn.Handle(p.row_ptr, p.col_idx, p.vals, p.OC, p.K, split_rows=False, cta_panels=a.cta_panels)
                 X = torch.from_numpy(p.x()).cuda()
                 b = torch.from_numpy(p.bias).cuda()
                 Y = torch.empty((p.OC, p.B, p.Ho, p.Wo), device="cuda")
