@@ -74,7 +74,7 @@ typedef struct {
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
                                multiple of 8                                                        */
   int32_t group_sb;         /* group kernel sub-block rows: 0 = auto (cost model), 1, 2 or 4         */
-  uint32_t flags;           /* SDNN_FLAG_NO_ROW_SPLIT | SDNN_FLAG_PERMUTED_OUTPUT, or 0               */
+  uint32_t flags;           /* SDNN_FLAG_NO_ROW_SPLIT | SDNN_FLAG_PERMUTED_OUTPUT | SDNN_FLAG_NO_SPLIT_K */
 } sdnn_perm_opts;
 
 /* Read-only description of a prepared handle (or a host plan). */
@@ -114,6 +114,11 @@ typedef struct {
  * Y_perm after its columns are relabelled the same way (sdnn_csr_permute_columns), so no layer
  * un-permutes.  Not with the codegen kernel (kernel = 3: SDNN_ERR_UNSUPPORTED). */
 #define SDNN_FLAG_PERMUTED_OUTPUT 2u
+/* Row kernel: never split the K range across CTAs.  By default a row-kernel call whose grid is under
+ * two waves runs KS ≤ 8 CTAs per (row block, N tile), each over a range of K chunks, and a second
+ * small kernel sums the KS partial results in slice order before bias and activation: deterministic,
+ * but not bitwise equal to the unsplit (sequential) summation order. */
+#define SDNN_FLAG_NO_SPLIT_K 4u
 
 typedef struct sdnn_handle_s* sdnn_handle; /* opaque; owns its device memory; immutable after prepare */
 typedef struct sdnn_plan_s* sdnn_plan;     /* opaque host-only plan (no device needed)               */

@@ -109,12 +109,14 @@ KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4, "tmem8": 5}
 
 FLAG_NO_ROW_SPLIT = 1
 FLAG_PERMUTED_OUTPUT = 2
+FLAG_NO_SPLIT_K = 4
 
 
 def _opts(permute=True, kernel="auto", panel_rows=0, cta_panels=0, k_chunk=0, group_sb=0, split_rows=True,
-          permuted_output=False):
+          permuted_output=False, split_k=True):
     k = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
-    flags = (0 if split_rows else FLAG_NO_ROW_SPLIT) | (FLAG_PERMUTED_OUTPUT if permuted_output else 0)
+    flags = ((0 if split_rows else FLAG_NO_ROW_SPLIT) | (FLAG_PERMUTED_OUTPUT if permuted_output else 0)
+             | (0 if split_k else FLAG_NO_SPLIT_K))
     return PermOpts(ctypes.sizeof(PermOpts), int(bool(permute)), k, int(panel_rows), int(cta_panels), int(k_chunk),
                     int(group_sb), flags)
 

@@ -273,7 +273,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     if (opts->struct_size != sizeof(sdnn_perm_opts))
       return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_perm_opts.struct_size mismatch");
     o = *opts;
-    if (o.flags & ~(SDNN_FLAG_NO_ROW_SPLIT | SDNN_FLAG_PERMUTED_OUTPUT))
+    if (o.flags & ~(SDNN_FLAG_NO_ROW_SPLIT | SDNN_FLAG_PERMUTED_OUTPUT | SDNN_FLAG_NO_SPLIT_K))
       return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown sdnn_perm_opts.flags bits");
     if ((o.flags & SDNN_FLAG_PERMUTED_OUTPUT) && o.kernel == 3)
       return fail(SDNN_ERR_UNSUPPORTED, "SDNN_FLAG_PERMUTED_OUTPUT is not available with the codegen kernel");
@@ -309,6 +309,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     plan.K = K;
     plan.nnz = nnz;
     plan.permuted = o.permute;
+    plan.no_split_k = (o.flags & SDNN_FLAG_NO_SPLIT_K) ? 1 : 0;
     plan.perm.resize(M);
     if (o.permute && perm && perm->size() == size_t(M))
       plan.perm = *perm;

@@ -166,6 +166,8 @@ struct KParams {
 // single-destination TMEM kernel takes plain KParams — its register allocation (72 regs, bound by
 // __launch_bounds__) shifts with the parameter block size and a larger block measured 8 % slower on c5.
 struct KParamsY : KParams {
+  float* kws;   // split-K (row kernel): raw partial sums, slice blockIdx.y at kws + blockIdx.y·M·N, else NULL
+  int32_t M;
   YOut yo;  // every destination (sdnn_spmm_multi); p.Y = yo.y[0] when there is just one of ld = N, col0 = 0
 };
 template <bool MULTI> using TmemParams = std::conditional_t<MULTI, KParamsY, KParams>;
@@ -275,7 +277,7 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
     if (orow == -1) continue;
     // a piece of a split row (row_orig = −2 − piece): its raw partial sums go to workspace row
     // `piece`; split_reduce_kernel adds the pieces, the bias and the activation
-    const bool piece = orow <= -2;
+    const bool piece = orow <= -2 || p.kws;  // raw partial sums: a split row's piece or a split-K slice
     const float b = (piece || !p.bias) ? 0.f : p.bias[orow];
     if constexpr (V == 2) {
       const int64_t n = n0 + lane * 2;
@@ -291,7 +293,8 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
       }
       const bool single = piece || p.Y;
       for (int d = 0; d < (single ? 1 : p.yo.n); ++d) {
-        float* yrow = piece    ? p.ws + int64_t(-2 - orow) * p.N
+        float* yrow = p.kws    ? p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N
+                      : piece  ? p.ws + int64_t(-2 - orow) * p.N
                       : single ? p.Y + int64_t(orow) * p.N
                                : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
         if (VEC) {
@@ -319,7 +322,8 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
       // p.Y set: one destination of leading dimension N (sdnn_spmm); else every yo.y[d] (sdnn_spmm_multi)
       const bool single = piece || p.Y;
       for (int d = 0; d < (single ? 1 : p.yo.n); ++d) {
-        float* yrow = piece    ? p.ws + int64_t(-2 - orow) * p.N
+        float* yrow = p.kws    ? p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N
+                      : piece  ? p.ws + int64_t(-2 - orow) * p.N
                       : single ? p.Y + int64_t(orow) * p.N
                                : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
         if (VEC) {
@@ -344,6 +348,21 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t*
   const int32_t row = split[sr], first = split[ns + sr], cnt = split[2 * ns + sr];
   float v = ws[int64_t(first) * N + n];
   for (int32_t k = 1; k < cnt; ++k) v += ws[int64_t(first + k) * N + n];
+  if (bias) v += bias[row];
+  if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
+  for (int d = 0; d < yo.n; ++d) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+}
+
+// Split-K (row kernel): Y[row] = act(Σ_{s < KS} kws[s][row] (slice order) + b[row]).  One thread per
+// column; blockIdx.y = row.
+__global__ void splitk_reduce_kernel(const float* __restrict__ kws, int32_t KS, int32_t M, const float* __restrict__ bias,
+                                     int32_t act, const YOut yo, int64_t N) {
+  const int32_t row = int32_t(blockIdx.y);
+  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int64_t slice = int64_t(M) * N;
+  float v = kws[int64_t(row) * N + n];
+  for (int32_t s = 1; s < KS; ++s) v += kws[s * slice + int64_t(row) * N + n];
   if (bias) v += bias[row];
   if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
   for (int d = 0; d < yo.n; ++d) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
@@ -374,12 +393,14 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
   }
   __syncthreads();
 
+  // split-K (gridDim.y > 1): this CTA's K chunks [j0, j1)
+  const int j0 = int(blockIdx.y) * p.nch / int(gridDim.y), j1 = (int(blockIdx.y) + 1) * p.nch / int(gridDim.y);
   if (warp == p.wc) {  // producer
     if (lane == 0) {
       const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
-      for (int j = 0; j < p.nch; ++j) {
-        const int s = j % S;
-        if (j >= S) mbar_wait(&empty[s], ((j / S) - 1) & 1);
+      for (int j = j0; j < j1; ++j) {
+        const int s = (j - j0) % S;
+        if (j - j0 >= S) mbar_wait(&empty[s], (((j - j0) / S) - 1) & 1);
         const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
         mbar_expect_tx(&full[s], uint32_t(p.x_stage_bytes) + mbytes);
         tma_load_2d(xstage + size_t(s) * p.x_stage_bytes, &tmap, int32_t(n0), j * p.kc, &full[s]);
@@ -395,9 +416,9 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
 #pragma unroll
     for (int q = 0; q < V / 2; ++q) acc[r][q] = AccT<KIND>{};
 
-  for (int j = 0; j < p.nch; ++j) {
-    const int s = j % S;
-    mbar_wait(&full[s], (j / S) & 1);
+  for (int j = j0; j < j1; ++j) {
+    const int s = (j - j0) % S;
+    mbar_wait(&full[s], ((j - j0) / S) & 1);
     const float* xs = reinterpret_cast<const float*>(xstage + size_t(s) * p.x_stage_bytes);
     if constexpr (KIND == 2)
       consume_group<V, SB>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane);
@@ -1229,7 +1250,7 @@ static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const 
 }
 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                               const YOut& yo, float* ws, cudaStream_t stream);
+                               const YOut& yo, float* ws, cudaStream_t stream, float* kws = nullptr, int KS = 1);
 
 // N-tile width of the row / group kernels for a call: V = 8 floats per lane (TN = 256) when that
 // still gives ≥ 2 CTAs per SM worth of work units, else V = 4 (TN = 128).
@@ -1248,6 +1269,28 @@ static int row_tile_v_small(const Plan& pl, int64_t N, int sms) {
 // Row-plan call whose grid (row blocks × N tiles) is under one wave: the narrow plan (more row
 // blocks of 4-row panels) fills the GPU instead (profiles/r01_row_geometry.log: 4096², N = 128:
 // 166 → 90 µs; 2048², N = 512: 70 → 50 µs).
+// Split-K factor for a row-kernel call (fast path, no split rows): only when the call puts fewer
+// than 8 warps on an SM and the K range is long (≥ 32 chunks): KS ≤ 8 slices of ≥ 4 chunks each,
+// up to ~16 warps per SM.
+// The partial-sum round trip and the reduction kernel cost more than the shorter chains save on
+// larger grids (profiles/r01_split_k.log: 768×3072, N = 128: 44 → 27 µs, 512×4096: 55 → 24 µs; an
+// earlier looser rule lost on 2048², N = 512, 256 CTAs: 50 → 69 µs).  SDNN_SPLIT_K=n forces n (1 = off) for experiments.
+static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const YOut& yo) {
+  const Plan& pl = h->plan;
+  if (pl.kernel != 1 || !pl.split_row.empty() || pl.no_split_k) return 1;
+  if (!(N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))) return 1;
+  static const int env = [] {
+    const char* e = getenv("SDNN_SPLIT_K");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 0) return std::max(1, std::min(env, pl.num_chunks));
+  const int64_t tn = 32 * row_tile_v_small(pl, N, h->sms);
+  const int64_t ctas = int64_t(pl.num_row_blocks) * ((N + tn - 1) / tn);
+  const int64_t warps = ctas * (pl.cta_panels + 1);
+  if (warps > 8 * int64_t(h->sms) || pl.num_chunks < 32) return 1;  // only clearly under-filled GPUs
+  const int64_t ks = std::min<int64_t>({8, pl.num_chunks / 4, 16 * int64_t(h->sms) / warps});
+  return ks >= 2 ? int(ks) : 1;
+}
 static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
   if (!h->narrow) return false;
   const int64_t tn = 32 * row_tile_v(h->plan, N);
@@ -1270,7 +1313,23 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
     SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ws), pl.piece_row.size() * size_t(N) * 4,
                                           h->ws_pool, stream));
   }
-  sdnn_status st = launch_main(h, X, N, bias, act, yo, ws, stream);
+  // split-K (row kernel, small grids): KS CTAs per (row block, N tile), each over a K-chunk range,
+  // raw partial sums to a stream-ordered workspace, summed in slice order by splitk_reduce_kernel
+  const int KS = ns > 0 ? 1 : splitk_for(h, N, X, yo);
+  float* kws = nullptr;
+  if (KS > 1)
+    SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws), size_t(KS) * pl.M * size_t(N) * 4,
+                                          h->ws_pool, stream));
+  sdnn_status st = launch_main(h, X, N, bias, act, yo, ws, stream, kws, KS);
+  if (KS > 1) {
+    if (st == SDNN_OK) {
+      const dim3 grid{unsigned((N + 255) / 256), unsigned(pl.M)};
+      splitk_reduce_kernel<<<grid, 256, 0, stream>>>(kws, KS, pl.M, bias, act, yo, N);
+      const cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("splitk_reduce_kernel: ") + cudaGetErrorString(le));
+    }
+    cudaFreeAsync(kws, stream);
+  }
   if (ns > 0) {
     if (st == SDNN_OK) {
       const dim3 grid{unsigned((N + 255) / 256), unsigned(ns)};
@@ -1285,7 +1344,7 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
 
 // The row / group / generic kernels of a plan (everything but TMEM and codegen).
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                               const YOut& yo, float* ws, cudaStream_t stream) {
+                               const YOut& yo, float* ws, cudaStream_t stream, float* kws, int KS) {
   const Plan& pl = h->plan;
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
@@ -1315,6 +1374,8 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   p.hdr_bytes = int32_t(align_up(int64_t(rw) * wc * 4, 16));
   p.act = act;
   p.ws = ws;
+  p.kws = kws;
+  p.M = pl.M;
 
   const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) && y_aligned16(yo) && pl.kernel < 4;
   if (fast) {
@@ -1344,7 +1405,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
     {
       auto waves = [&](int s) {
         const int occ = std::max(1, occupancy(fn, threads, smem_for(s)));
-        return double(nblocks) / (double(h->sms) * occ);
+        return double(nblocks) * KS / (double(h->sms) * occ);
       };
       double best = waves(S);
       int best_s = S;
@@ -1376,8 +1437,9 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
     void* args[] = {&tmap, &p};
-    SDNN_CUDA_TRY(cudaLaunchKernel(fn, dim3(unsigned(nblocks)), dim3(unsigned(threads)), args, smem, stream));
+    SDNN_CUDA_TRY(cudaLaunchKernel(fn, dim3(unsigned(nblocks), unsigned(KS)), dim3(unsigned(threads)), args, smem, stream));
   } else {
+    if (KS > 1) return fail(SDNN_ERR_INTERNAL, "split-K outside the row kernel's fast path");
     p.stages = 1;
     const size_t smem = size_t(p.x_stage_bytes) + p.m_stage_bytes;
     const dim3 grid{unsigned(nblocks)}, block{unsigned(wc * 32)};
@@ -1507,15 +1569,16 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     tab.insert(tab.end(), pl.split_count.begin(), pl.split_count.end());
     e = cudaMalloc(&h->d_split, tab.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_split, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) {
-      cudaMemPoolProps props{};
-      props.allocType = cudaMemAllocationTypePinned;
-      props.location.type = cudaMemLocationTypeDevice;
-      props.location.id = dev;
-      e = cudaMemPoolCreate(&h->ws_pool, &props);
-      uint64_t keep = ~uint64_t(0);
-      if (e == cudaSuccess) e = cudaMemPoolSetAttribute(h->ws_pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
+  }
+  // workspace pool of the split-row pieces and the split-K slices (row plans)
+  if (e == cudaSuccess && pl.kernel == 1) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    e = cudaMemPoolCreate(&h->ws_pool, &props);
+    uint64_t keep = ~uint64_t(0);
+    if (e == cudaSuccess) e = cudaMemPoolSetAttribute(h->ws_pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   if (e != cudaSuccess) return cleanup(SDNN_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
   pl.meta_size_uploaded = int64_t(pl.meta.size());

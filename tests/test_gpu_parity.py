@@ -166,7 +166,7 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
     are not split here: split rows sum fixed pieces, see test_split_rows)."""
     p = synth.config_problem("c2_768x3072")
     X = p.x()
-    ref, _ = run_gpu(sdnn, p, X, p.bias, 1, split_rows=False)
+    ref, _ = run_gpu(sdnn, p, X, p.bias, 1, split_rows=False, split_k=False)
     for opts in [dict(permute=False), dict(panel_rows=8), dict(cta_panels=1), dict(k_chunk=8),
                  dict(k_chunk=96, panel_rows=4, cta_panels=2), dict(kernel="group"), dict(kernel="row"),
                  dict(kernel="group", permute=False), dict(kernel="group", cta_panels=3, k_chunk=16),
@@ -174,7 +174,7 @@ def test_permute_on_off_and_tilings_bitwise(sdnn):
                  dict(kernel="codegen"), dict(kernel="codegen", permute=False), dict(kernel="codegen", panel_rows=7),
                  dict(kernel="tmem"), dict(kernel="tmem", permute=False), dict(kernel="tmem8"),
                  dict(kernel="tmem8", permute=False)]:
-        Y, _ = run_gpu(sdnn, p, X, p.bias, 1, split_rows=False, **opts)
+        Y, _ = run_gpu(sdnn, p, X, p.bias, 1, split_rows=False, split_k=False, **opts)
         np.testing.assert_array_equal(Y, ref, err_msg=str(opts))
 
 
@@ -211,7 +211,7 @@ def test_split_rows(sdnn, oracle_mod, key):
 def test_column_shards_bitwise(sdnn):
     p = synth.config_problem("c3_512x512")
     X = p.x()
-    h = sdnn.Handle.from_problem(p)
+    h = sdnn.Handle.from_problem(p, split_k=False)  # split-K slices depend on the grid, hence on N
     ref, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
     for a, b in [(0, 4), (4, 1000), (1000, 1001), (1001, p.N)]:
         Y, _ = run_gpu(sdnn, p, np.ascontiguousarray(X[:, a:b]), p.bias, 1, handle=h)
@@ -233,7 +233,7 @@ def test_repeat_bitwise_and_linearity(sdnn):
 def test_host_entry_point_matches_device(sdnn, kernel):
     p = synth.config_problem("c3_256x128")
     X = p.x()
-    h = sdnn.Handle.from_problem(p, kernel=kernel)
+    h = sdnn.Handle.from_problem(p, kernel=kernel, **({} if kernel == "codegen" else dict(split_k=False)))
     ref, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
     for bc in (0, 512, 1000, 4, 2048):
         Y = h.spmm_host(X, p.bias, act=1, block_cols=bc)
@@ -279,10 +279,10 @@ def test_auto_narrow_row_plan_for_small_grids(sdnn, oracle_mod, M, K, sp):
     ≥ 64 row blocks, same permutation) for row-plan calls under one wave of CTAs (small N).  Same
     per-row accumulation order → bitwise equal to the row plan; oracle parity."""
     p = synth.make_problem(f"narrow{M}", M, K, 256, sp)
-    h = sdnn.Handle.from_problem(p)
+    h = sdnn.Handle.from_problem(p, split_k=False)
     info = h.info()
     assert info["narrow_row_blocks"] >= 64 and info["narrow_row_blocks"] > info["num_row_blocks"]
-    hr = sdnn.Handle.from_problem(p, kernel="row")
+    hr = sdnn.Handle.from_problem(p, kernel="row", split_k=False)
     assert hr.info()["narrow_row_blocks"] == 0
     for N in (128, 256, 100):
         X = np.ascontiguousarray(p.x()[:, :N])
@@ -291,6 +291,34 @@ def test_auto_narrow_row_plan_for_small_grids(sdnn, oracle_mod, M, K, sp):
         np.testing.assert_array_equal(Ya, Yr)
         Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, want_scale=True)[:2]
         assert_parity(Ya, Yo, S, f"narrow N={N}")
+
+
+@pytest.mark.parametrize("M,K,N,sp,mask", [(512, 4096, 128, 0.9, "uniform"), (768, 3072, 128, 0.9, "uniform"),
+                                            (768, 3072, 64, 0.9, "lognormal"), (256, 2048, 96, 0.8, "uniform")])
+def test_split_k(sdnn, oracle_mod, M, K, N, sp, mask):
+    """Row-kernel calls that leave the GPU under-filled split the K range over CTAs (partial sums reduced in slice
+    order): oracle parity, deterministic (bitwise on repeat and in a CUDA graph), within rounding of
+    the unsplit result, and SDNN_FLAG_NO_SPLIT_K turns it off."""
+    p = synth.make_problem(f"sk{M}_{K}", M, K, N, sp, mask=mask)
+    X = p.x()
+    h = sdnn.Handle.from_problem(p, split_rows=False)
+    Y, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    Y2, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Y, Y2)
+    Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, want_scale=True)[:2]
+    assert_parity(Y, Yo, S, "split-K")
+    Yn, _ = run_gpu(sdnn, p, X, p.bias, 1, split_rows=False, split_k=False)
+    assert_parity(Yn, Yo, S, "unsplit")
+    assert not np.array_equal(Y, Yn)  # a different (slice-order) summation actually ran
+    Xd, b = torch.from_numpy(X).cuda(), torch.from_numpy(p.bias).cuda()
+    Yg = torch.empty((p.M, p.N), device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        h.spmm(Xd, b, act=1, out=Yg)
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(Yg.cpu().numpy(), Y)
 
 
 def test_get_permutation_and_info(sdnn, oracle_mod):
