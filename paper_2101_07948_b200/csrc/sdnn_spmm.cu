@@ -623,19 +623,22 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
   float2 acc[RW][2];
 #pragma unroll
   for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
-  gather(0, 0);
-  for (int j = 0; j < p.nch; ++j) {
-    if (j + 1 < p.nch) {
-      gather(j + 1, (j + 1) & 1);
+  // split-K (gridDim.y > 1): this CTA's K chunks [j0, j1); raw partial sums to p.kws
+  const int j0 = int(blockIdx.y) * p.nch / int(gridDim.y), j1 = (int(blockIdx.y) + 1) * p.nch / int(gridDim.y);
+  gather(j0, 0);
+  for (int j = j0; j < j1; ++j) {
+    const int bj = (j - j0) & 1;
+    if (j + 1 < j1) {
+      gather(j + 1, bj ^ 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const float* xs = patch[j & 1];
-    const int32_t* tb = tab[j & 1];
-    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms[j & 1]) + warp * RW;
-    const float4* ent = reinterpret_cast<const float4*>(ms[j & 1] + p.hdr_bytes);
+    const float* xs = patch[bj];
+    const int32_t* tb = tab[bj];
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms[bj]) + warp * RW;
+    const float4* ent = reinterpret_cast<const float4*>(ms[bj] + p.hdr_bytes);
 #pragma unroll
     for (int r = 0; r < RW; ++r) {
       const uint32_t h = hdr[r];
@@ -664,13 +667,13 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
   for (int r = 0; r < RW; ++r) {
     const int32_t orow = p.row_orig[(rb * p.wc + warp) * RW + r];
     if (orow < 0) continue;
-    const float bv = p.bias ? p.bias[orow] : 0.f;
+    const float bv = (p.bias && !p.kws) ? p.bias[orow] : 0.f;
     float v[4] = {acc[r][0].x + bv, acc[r][0].y + bv, acc[r][1].x + bv, acc[r][1].y + bv};
-    float* yrow = p.Y + int64_t(orow) * p.N;
+    float* yrow = p.kws ? p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N : p.Y + int64_t(orow) * p.N;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t n = n0 + lane + 32 * q;
-      const float y = p.act == SDNN_ACT_RELU ? (v[q] > 0.f ? v[q] : 0.f) : v[q];
+      const float y = (p.act == SDNN_ACT_RELU && !p.kws) ? (v[q] > 0.f ? v[q] : 0.f) : v[q];
       if (n < p.N) __stcs(yrow + n, y);
     }
   }
@@ -1810,10 +1813,28 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
       const void* fn2 = rw == 8 ? reinterpret_cast<const void*>(spmm_conv2_kernel<8>)
                                 : reinterpret_cast<const void*>(spmm_conv2_kernel<4>);
       SDNN_CUDA_TRY(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      // split-K as for the row kernel: small images leave the GPU under-filled (few pixel tiles)
+      const int64_t warps = nblocks * wc;
+      int KS = 1;
+      if (!pl.no_split_k && warps <= 8 * int64_t(h->sms) && pl.num_chunks >= 16)
+        KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / 4, 16 * int64_t(h->sms) / warps})));
+      cudaStream_t st_ = static_cast<cudaStream_t>(stream);
+      float* kws = nullptr;
+      if (KS > 1) SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws),
+                                                        size_t(KS) * pl.M * size_t(N) * 4, h->ws_pool, st_));
+      p.kws = kws;
+      p.M = pl.M;
       int32_t psr = int32_t(rows), icc = int32_t(ICC);
       void* args2[] = {&p, const_cast<ConvGeom*>(&cg), &psr, &icc};
-      SDNN_CUDA_TRY(cudaLaunchKernel(fn2, dim3(unsigned(nblocks)), dim3(unsigned(wc * 32)), args2, smem2,
-                                     static_cast<cudaStream_t>(stream)));
+      cudaError_t le = cudaLaunchKernel(fn2, dim3(unsigned(nblocks), unsigned(KS)), dim3(unsigned(wc * 32)), args2,
+                                        smem2, st_);
+      if (le == cudaSuccess && KS > 1) {
+        splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(pl.M)), 256, 0, st_>>>(kws, KS, pl.M, bias, act,
+                                                                                                y_single(Y, N), N);
+        le = cudaGetLastError();
+      }
+      if (KS > 1) cudaFreeAsync(kws, st_);
+      if (le != cudaSuccess) return fail(SDNN_ERR_CUDA, std::string("sdnn_conv2d: ") + cudaGetErrorString(le));
       return SDNN_OK;
     }
   }

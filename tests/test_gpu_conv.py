@@ -70,3 +70,14 @@ def test_conv_errors(sdnn):
     ht = sdnn.Handle(p.row_ptr, p.col_idx, p.vals, p.OC, p.K, kernel="tmem")
     with pytest.raises(sdnn.SdnnError):
         ht.conv2d(X, 3, 3, 1, 1)
+
+
+def test_conv_split_k(sdnn):
+    """Small images with many input channels split the K range over CTAs (partial sums reduced in
+    slice order): oracle parity, deterministic, and SDNN_FLAG_NO_SPLIT_K gives the sequential order."""
+    p = synth.make_conv_problem("csk", 256, 256, 7, 7, 1, 0.9)
+    Y1, h = run(sdnn, p)
+    Y2, _ = run(sdnn, p)
+    np.testing.assert_array_equal(Y1, Y2)
+    Yn, _ = run(sdnn, p, split_k=False)
+    assert not np.array_equal(Y1, Yn)  # the split path actually ran
