@@ -252,6 +252,9 @@ SDNN_API int32_t sdnn_abi_version(void);
  *   SDNN_DEBUG_TMEM  bit mask, TMEM kernels: 1 skip the X loads (TMA), 2 skip the FMA loop, 4 skip the
  *                    smem -> TMEM fill — results are WRONG with any bit set (timing decomposition)
  *   SDNN_ROW_STAGES  upper bound on the row kernel's stage-ring depth
+ *   SDNN_SPLIT_K     row kernel: force this many K slices (1 = never split); default: automatic for
+ *                    under-filled calls (see SDNN_FLAG_NO_SPLIT_K)
+ *   SDNN_CONV_GATHER 1 = sdnn_conv2d stages the virtual matrix itself instead of the input patch
  * (and, at build time, -DSDNN_DIAG=1|2: TMEM consumer without tcgen05.ld / without FFMA2). */
 
 #ifdef __cplusplus
