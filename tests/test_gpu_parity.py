@@ -374,6 +374,26 @@ if given is not None:
         check(sdnn, oracle_mod, p, X=X, act=int(seed % 2), kernel=kernel)
 
 
+if given is not None:
+    @settings(max_examples=10, deadline=None, suppress_health_check=list(HealthCheck))
+    @given(M=st.integers(16, 1500), K=st.integers(1024, 4096), n4=st.integers(1, 50), dens=st.sampled_from([0.02, 0.1, 0.2]),
+           bias=st.booleans(), act=st.integers(0, 1), seed=st.integers(0, 2**31 - 1))
+    def test_random_small_n_long_k(sdnn, oracle_mod, M, K, n4, dens, bias, act, seed):
+        """Small N, long K, auto kernel: the narrow plan, V = 2 tiles and split-K (slice-ordered
+        reduction, with / without bias and ReLU) against the oracle."""
+        rng = np.random.default_rng(seed)
+        N = 4 * n4
+        m = rng.random((M, K)) < dens
+        rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum(m.sum(1))
+        ci = np.nonzero(m)[1].astype(np.int32)
+        v = (0.05 * rng.standard_normal(ci.size)).astype(np.float32)
+        v[v == 0] = 0.01
+        b = (0.1 * rng.standard_normal(M)).astype(np.float32)
+        p = synth.Problem("randk", M, K, N, 0, "x", rp, ci, v, b, act, seed)
+        X = rng.standard_normal((K, N)).astype(np.float32)
+        check(sdnn, oracle_mod, p, X=X, act=act, bias=b if bias else None)
+
+
 @pytest.mark.parametrize("kernel", ["auto", "row", "tmem"])
 def test_large_k_and_large_m(sdnn, oracle_mod, kernel):
     """K = 40 000 (625 TMEM chunks) and M = 20 000 (334 TMEM row blocks) at small N."""
