@@ -191,6 +191,20 @@ SDNN_API sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32
                                  int32_t FY, int32_t FX, int32_t pad, int32_t stride, const float* bias, int32_t act,
                                  float* Y, void* stream);
 
+/* sdnn_serialize / sdnn_deserialize: the prepared handle (every plan it keeps — row, TMEM, narrow —
+ * with its execution-ordered metadata) as a self-contained blob, so another process skips
+ * Algorithm 1 and the packing (the paper's reusable preparation stage).
+ *   sdnn_serialize(h, NULL, &size) stores the blob size; sdnn_serialize(h, buf, &size) writes it to
+ *   the HOST buffer (SDNN_ERR_INVALID_ARGUMENT if *size is too small; *size = bytes written).
+ *   Codegen handles (kernel 3, JIT-compiled from the CSR) → SDNN_ERR_UNSUPPORTED.
+ *   sdnn_deserialize(buf, size, &h) uploads the plans to the current device; a corrupt or
+ *   truncated blob → SDNN_ERR_INVALID_ARGUMENT, another format version → SDNN_ERR_UNSUPPORTED.
+ *   Only the structure is validated (sizes, offsets, row indices); the packed stream itself is
+ *   trusted — load blobs this library wrote.
+ * Results of the deserialized handle are bitwise those of the original. */
+SDNN_API sdnn_status sdnn_serialize(sdnn_handle h, void* buf, size_t* size);
+SDNN_API sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out);
+
 /* ------------------------------------------------------------------ introspection
  * sdnn_get_permutation: out_perm (HOST, M entries) receives order[i] = original row at permuted
  * position i (Algorithm 1 output, SPEC S:295 convention).  sdnn_get_info fills *info. */

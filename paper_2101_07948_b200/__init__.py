@@ -25,7 +25,8 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
           4: "SDNN_ERR_OUT_OF_MEMORY", 5: "SDNN_ERR_CUDA", 6: "SDNN_ERR_DEVICE_MISMATCH", 7: "SDNN_ERR_INTERNAL"}
 
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
-EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_spmm_host", "sdnn_spmm_kernel",
+EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_serialize",
+           "sdnn_deserialize", "sdnn_spmm_host", "sdnn_spmm_kernel",
            "sdnn_get_permutation",
            "sdnn_get_info",
            "sdnn_permutation", "sdnn_csr_permute_columns", "sdnn_plan_create", "sdnn_plan_get_info", "sdnn_plan_export", "sdnn_plan_export_pieces",
@@ -73,6 +74,8 @@ _lib.sdnn_spmm_kernel.argtypes = [_vp, _i64, _vp, _vp, ctypes.POINTER(_i32)]
 _lib.sdnn_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
 _lib.sdnn_csr_permute_columns.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
+_lib.sdnn_serialize.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_size_t)]
+_lib.sdnn_deserialize.argtypes = [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)]
 _lib.sdnn_conv2d.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]
 _lib.sdnn_plan_create.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts), ctypes.POINTER(_vp)]
 _lib.sdnn_plan_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
@@ -213,6 +216,25 @@ class Handle:
     @classmethod
     def from_problem(cls, p, **opts):
         return cls(p.row_ptr, p.col_idx, p.vals, p.M, p.K, **opts)
+
+    def serialize(self) -> bytes:
+        """The prepared handle as a blob (sdnn_serialize): reload with Handle.deserialize."""
+        n = ctypes.c_size_t(0)
+        _check(_lib.sdnn_serialize(self._h, None, ctypes.byref(n)), "sdnn_serialize")
+        buf = ctypes.create_string_buffer(n.value)
+        _check(_lib.sdnn_serialize(self._h, buf, ctypes.byref(n)), "sdnn_serialize")
+        return buf.raw[:n.value]
+
+    @classmethod
+    def deserialize(cls, blob: bytes) -> "Handle":
+        """A handle from sdnn_serialize's blob, on the current CUDA device (no Algorithm 1, no packing)."""
+        h = _vp()
+        _check(_lib.sdnn_deserialize(blob, len(blob), ctypes.byref(h)), "sdnn_deserialize")
+        self = cls.__new__(cls)
+        self._h = h
+        i = self.info()
+        self.M, self.K = i["M"], i["K"]
+        return self
 
     def info(self) -> dict:
         i = Info()

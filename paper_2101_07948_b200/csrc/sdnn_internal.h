@@ -22,8 +22,8 @@ struct Plan {
   int32_t M = 0, K = 0;
   int64_t nnz = 0;
   int32_t permuted = 0;
-  int32_t permuted_output = 0;
-  int32_t no_split_k = 0;       // SDNN_FLAG_NO_SPLIT_K: the row kernel never splits K across CTAs  // SDNN_FLAG_PERMUTED_OUTPUT: row_orig / split_row hold plan positions
+  int32_t permuted_output = 0;  // SDNN_FLAG_PERMUTED_OUTPUT: row_orig / split_row hold plan positions
+  int32_t no_split_k = 0;       // SDNN_FLAG_NO_SPLIT_K: the row kernel never splits K across CTAs
   int32_t kernel = 1;          // 1 = row kernel, 2 = group kernel
   int64_t group_entries = 0;   // union entries of the group format
   int32_t group_sb = 0;        // group kernel sub-block rows (1, 2 or 4)

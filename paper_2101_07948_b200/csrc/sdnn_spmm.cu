@@ -1485,7 +1485,7 @@ extern "C" {
 
 static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, const float* vals, int32_t M,
                                int32_t K, const sdnn_perm_opts* perm_opts, sdnn_handle* out,
-                               const std::vector<int32_t>* perm = nullptr) {
+                               const std::vector<int32_t>* perm = nullptr, Plan* given = nullptr) {
   if (!out) return fail(SDNN_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   int dev = -1;
@@ -1497,7 +1497,9 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
                                           std::to_string(prop.major) + std::to_string(prop.minor));
   sdnn_handle_s* h = new (std::nothrow) sdnn_handle_s;
   if (!h) return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
-  sdnn_status st = build_plan(csr_ptr, col_idx, vals, M, K, perm_opts, h->plan, perm);
+  sdnn_status st = SDNN_OK;
+  if (given) h->plan = std::move(*given);  // sdnn_deserialize: a plan prepared earlier
+  else st = build_plan(csr_ptr, col_idx, vals, M, K, perm_opts, h->plan, perm);
   if (st != SDNN_OK) {
     delete h;
     return st;
@@ -1971,6 +1973,159 @@ sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info) {
   info->meta_bytes = h->plan.meta_size_uploaded;
   info->alt_kernel = h->alt ? h->alt->plan.kernel : 0;
   info->narrow_row_blocks = h->narrow ? h->narrow->plan.num_row_blocks : 0;
+  return SDNN_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------------
+// Serialization of a prepared handle (the paper's reusable preparation): every plan
+// of the handle (main, TMEM, narrow) with its packed metadata, so a process can skip Algorithm 1
+// and the packing.  Blob: "SDNNPLAN", u32 version, u32 plan count, then per plan a u32 role
+// (0 main, 1 TMEM, 2 narrow) and its fields in a fixed order (little-endian, sizes as u64).
+namespace {
+constexpr uint32_t kBlobVersion = 1;
+struct BlobW {
+  std::vector<uint8_t> b;
+  template <class T> void s(const T& v) {
+    const uint8_t* q = reinterpret_cast<const uint8_t*>(&v);
+    b.insert(b.end(), q, q + sizeof(T));
+  }
+  template <class T> void v(const std::vector<T>& x) {
+    s<uint64_t>(x.size());
+    const uint8_t* q = reinterpret_cast<const uint8_t*>(x.data());
+    b.insert(b.end(), q, q + x.size() * sizeof(T));
+  }
+};
+struct BlobR {
+  const uint8_t* p;
+  size_t n, off = 0;
+  bool ok = true;
+  template <class T> void s(T& v) {
+    if (!ok || off + sizeof(T) > n) { ok = false; return; }
+    std::memcpy(&v, p + off, sizeof(T));
+    off += sizeof(T);
+  }
+  template <class T> void v(std::vector<T>& x) {
+    uint64_t m = 0;
+    s(m);
+    if (!ok || m > (n - off) / sizeof(T)) { ok = false; return; }
+    x.resize(size_t(m));
+    std::memcpy(x.data(), p + off, size_t(m) * sizeof(T));
+    off += size_t(m) * sizeof(T);
+  }
+};
+template <class IO> void plan_fields(IO& io, Plan& p) {
+  io.s(p.M); io.s(p.K); io.s(p.nnz); io.s(p.permuted); io.s(p.permuted_output); io.s(p.no_split_k);
+  io.s(p.kernel); io.s(p.group_entries); io.s(p.group_sb); io.s(p.group_subblocks); io.s(p.panel_rows);
+  io.s(p.cta_panels); io.s(p.num_panels); io.s(p.num_row_blocks); io.s(p.k_chunk); io.s(p.num_chunks);
+  io.s(p.max_block_bytes); io.s(p.max_panel_nnz); io.s(p.tmem_fill);
+  io.v(p.perm); io.v(p.row_orig); io.v(p.blk_off); io.v(p.meta);
+  io.v(p.piece_row); io.v(p.piece_begin); io.v(p.piece_end); io.v(p.split_row); io.v(p.split_first);
+  io.v(p.split_count);
+}
+// A handle's plan with its metadata copied back from the device (the host copy is freed at upload).
+sdnn_status plan_with_meta(const sdnn_handle_s* h, Plan& out) {
+  out = h->plan;
+  out.meta.resize(size_t(h->plan.meta_size_uploaded));
+  if (!out.meta.empty()) SDNN_CUDA_TRY(cudaMemcpy(out.meta.data(), h->d_meta, out.meta.size(), cudaMemcpyDeviceToHost));
+  return SDNN_OK;
+}
+// Structural checks of a deserialized plan before it is uploaded and launched.
+bool plan_sane(const Plan& p) {
+  if (p.M < 1 || p.K < 1 || p.kernel < 1 || p.kernel > 5 || p.kernel == 3) return false;
+  if (p.perm.size() != size_t(p.M) || p.num_row_blocks < 1 || p.num_chunks < 1 || p.k_chunk < 1) return false;
+  if (p.blk_off.size() != size_t(p.num_row_blocks) * size_t(p.num_chunks) + 1) return false;
+  if (p.row_orig.size() != size_t(p.num_panels) * size_t(p.panel_rows)) return false;
+  if (p.blk_off.front() != 0 || p.blk_off.back() != int64_t(p.meta.size())) return false;
+  for (size_t i = 1; i < p.blk_off.size(); ++i)
+    if (p.blk_off[i] < p.blk_off[i - 1] || p.blk_off[i] - p.blk_off[i - 1] > p.max_block_bytes) return false;
+  for (int32_t r : p.row_orig)
+    if (r >= p.M || (r <= -2 && size_t(-2 - int64_t(r)) >= p.piece_row.size())) return false;
+  if (p.split_first.size() != p.split_row.size() || p.split_count.size() != p.split_row.size()) return false;
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
+sdnn_status sdnn_serialize(sdnn_handle h, void* buf, size_t* size) {
+  if (!h || !size) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle or size");
+  const sdnn_handle_s* parts[3] = {h, h->alt, h->narrow};
+  for (const sdnn_handle_s* q : parts)
+    if (q && q->plan.kernel == 3)
+      return fail(SDNN_ERR_UNSUPPORTED, "codegen plans are JIT-compiled from the CSR and are not serialized");
+  sdnn_status st = check_device(h);
+  if (st != SDNN_OK) return st;
+  BlobW w;
+  try {
+    const char magic[8] = {'S', 'D', 'N', 'N', 'P', 'L', 'A', 'N'};
+    w.b.insert(w.b.end(), magic, magic + 8);
+    w.s(kBlobVersion);
+    w.s(uint32_t((h->alt ? 1 : 0) + (h->narrow ? 1 : 0) + 1));
+    for (uint32_t role = 0; role < 3; ++role) {
+      if (!parts[role]) continue;
+      Plan pl;
+      st = plan_with_meta(parts[role], pl);
+      if (st != SDNN_OK) return st;
+      w.s(role);
+      plan_fields(w, pl);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
+  }
+  if (!buf) {
+    *size = w.b.size();
+    return SDNN_OK;
+  }
+  if (*size < w.b.size()) {
+    const size_t have = *size;
+    *size = w.b.size();
+    return fail(SDNN_ERR_INVALID_ARGUMENT, "buffer of " + std::to_string(have) + " bytes < " + std::to_string(w.b.size()));
+  }
+  std::memcpy(buf, w.b.data(), w.b.size());
+  *size = w.b.size();
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
+  if (!buf || !out) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL buffer or out");
+  *out = nullptr;
+  BlobR r{static_cast<const uint8_t*>(buf), size};
+  if (size < 16 || std::memcmp(buf, "SDNNPLAN", 8) != 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "not an sdnn blob");
+  r.off = 8;
+  uint32_t ver = 0, count = 0;
+  r.s(ver);
+  r.s(count);
+  if (!r.ok || ver != kBlobVersion) return fail(SDNN_ERR_UNSUPPORTED, "blob version " + std::to_string(ver) + " != 1");
+  if (count < 1 || count > 3) return fail(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan count)");
+  sdnn_handle parts[3] = {nullptr, nullptr, nullptr};
+  auto cleanup = [&](sdnn_status s, const std::string& m) {
+    for (auto& q : parts)
+      if (q) sdnn_destroy(q);
+    return fail(s, m);
+  };
+  try {
+    for (uint32_t i = 0; i < count; ++i) {
+      uint32_t role = 3;
+      r.s(role);
+      Plan pl;
+      plan_fields(r, pl);
+      if (!r.ok || role > 2 || parts[role] || !plan_sane(pl) || (role == 0) != (i == 0))
+        return cleanup(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan " + std::to_string(i) + ")");
+      sdnn_status st = prepare_one(nullptr, nullptr, nullptr, pl.M, pl.K, nullptr, &parts[role], nullptr, &pl);
+      if (st != SDNN_OK) {
+        std::string m = sdnn_last_error_message();
+        return cleanup(st, m);
+      }
+    }
+  } catch (const std::bad_alloc&) {
+    return cleanup(SDNN_ERR_OUT_OF_MEMORY, "host allocation failed");
+  }
+  if (r.off != size) return cleanup(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (trailing bytes)");
+  parts[0]->alt = parts[1];
+  parts[0]->narrow = parts[2];
+  *out = parts[0];
   return SDNN_OK;
 }
 
