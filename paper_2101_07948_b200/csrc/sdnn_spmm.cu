@@ -1803,7 +1803,9 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
       const int64_t b0 = n0 / HWo, oy0 = (n0 - b0 * HWo) / Wo, b1 = n1 / HWo, oy1 = (n1 - b1 * HWo) / Wo;
       rows = std::max<int64_t>(rows, (b1 * Hp + oy1 * stride + FY - 1) - (b0 * Hp + oy0 * stride) + 1);
     }
-    const int64_t FYX = int64_t(FY) * FX, ICC = (pl.k_chunk - 1) / FYX + 2;
+    // input channels a K chunk touches: kc / (FY·FX) when chunks start on channel boundaries
+    // (k_chunk a multiple of FY·FX, e.g. 72 for 3×3), else up to two partial channels more
+    const int64_t FYX = int64_t(FY) * FX, ICC = pl.k_chunk % FYX == 0 ? pl.k_chunk / FYX : (pl.k_chunk - 1) / FYX + 2;
     const int64_t Wp = int64_t(W) + 2 * pad;
     const size_t stage = align_up(int64_t(ICC * rows * Wp * 4 + int64_t(pl.k_chunk) * 4), 128) + size_t(p.m_stage_bytes);
     static const int conv_env = [] {

@@ -21,7 +21,7 @@ def sdnn():
 
 
 def run(sdnn, p, **hopts):
-    h = sdnn.Handle(p.row_ptr, p.col_idx, p.vals, p.OC, p.K, split_rows=False, **hopts)
+    h = sdnn.Handle.for_conv(p.row_ptr, p.col_idx, p.vals, p.OC, p.IC, p.FY, p.FX, **hopts)
     X = p.x()
     b = None if p.bias is None else torch.from_numpy(p.bias).cuda()
     Y = h.conv2d(torch.from_numpy(X).cuda(), p.FY, p.FX, p.pad, p.stride, b, act=p.act).cpu().numpy()

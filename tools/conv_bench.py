@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
     ap.add_argument("--cta-panels", type=int, default=0, help="row-plan warps per CTA (0 = auto)")
+    ap.add_argument("--k-chunk", type=int, default=-1, help="row-plan K chunk (-1 = Handle.for_conv's choice, 0 = auto)")
     ap.add_argument("--sizes", default="32,64,128,256")
     ap.add_argument("--images", default="7,14,28,56")
     a = ap.parse_args()
@@ -36,7 +37,8 @@ def main():
         for hw in (int(v) for v in a.images.split(",")):
             for sp in (0.9, 0.95):
                 p = synth.make_conv_problem(f"cb{ch}_{hw}_{sp}", ch, ch, hw, hw, a.batch, sp)
-                h = sdnn.Handle(p.row_ptr, p.col_idx, p.vals, p.OC, p.K, split_rows=False, cta_panels=a.cta_panels)
+                h = sdnn.Handle.for_conv(p.row_ptr, p.col_idx, p.vals, p.OC, p.IC, 3, 3, cta_panels=a.cta_panels,
+                                         **({"k_chunk": a.k_chunk} if a.k_chunk >= 0 else {}))
                 X = torch.from_numpy(p.x()).cuda()
                 b = torch.from_numpy(p.bias).cuda()
                 Y = torch.empty((p.OC, p.B, p.Ho, p.Wo), device="cuda")
