@@ -578,10 +578,11 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
   // srcoff[e], e < PS: offset of patch element e (row e / Wp, column e mod Wp) within one input
   // channel, −1 for padding; the same for every channel and chunk of this tile (after both stages)
   int32_t* srcoff = reinterpret_cast<int32_t*>(smem + 2 * stage);
-  float* patch[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + stage)};
-  int32_t* tab[2] = {reinterpret_cast<int32_t*>(patch[0] + size_t(ICC) * PS),
-                     reinterpret_cast<int32_t*>(patch[1] + size_t(ICC) * PS)};
-  uint8_t* ms[2] = {smem + stage - p.m_stage_bytes, smem + 2 * stage - p.m_stage_bytes};
+  // stage b: patch floats at smem + b·stage, then the tap table, then the metadata block (addresses
+  // recomputed from smem — no pointer arrays, so every access stays an LDS/STS)
+  auto patch_of = [&](int b) { return reinterpret_cast<float*>(smem + size_t(b) * stage); };
+  auto tab_of = [&](int b) { return reinterpret_cast<int32_t*>(smem + size_t(b) * stage + size_t(ICC) * PS * 4); };
+  auto ms_of = [&](int b) { return smem + size_t(b + 1) * stage - p.m_stage_bytes; };
   const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
   // the tile's first virtual input row, and each lane's four pixels
   const int b0 = int(n0 / HWo), oy0 = int((n0 - int64_t(b0) * HWo) / c.Wo);
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
     for (int icl = 0; icl < ICC; ++icl) {  // the chunk's input channels, element-parallel over the patch
       const int ic = ic_lo + icl;
       const float* src = p.X + int64_t(ic < c.IC ? ic : 0) * icstride;
-      float* dst = patch[buf] + icl * PS;
+      float* dst = patch_of(buf) + icl * PS;
       for (int e = int(threadIdx.x); e < PS; e += int(blockDim.x)) {
         const int so = srcoff[e];
         const bool ok = so >= 0 && ic < c.IC;
@@ -613,11 +614,11 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
     }
     for (int cl = int(threadIdx.x); cl < p.kc; cl += int(blockDim.x)) {
       const int k = k0 + cl, ic = k / FYX, t = k - ic * FYX, fy = t / c.FX, fx = t - fy * c.FX;
-      tab[buf][cl] = (ic - ic_lo) * PS + fy * Wp + fx;
+      tab_of(buf)[cl] = (ic - ic_lo) * PS + fy * Wp + fx;
     }
     const int mbytes = int(off[j + 1] - off[j]);
     const uint8_t* msrc = p.meta + off[j];
-    for (int i = int(threadIdx.x); i < mbytes / 16; i += int(blockDim.x)) cp_async16(ms[buf] + 16 * i, msrc + 16 * i);
+    for (int i = int(threadIdx.x); i < mbytes / 16; i += int(blockDim.x)) cp_async16(ms_of(buf) + 16 * i, msrc + 16 * i);
     cp_async_commit();
   };
   float2 acc[RW][2];
@@ -635,10 +636,11 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
       cp_async_wait<0>();
     }
     __syncthreads();
-    const float* xs = patch[bj];
-    const int32_t* tb = tab[bj];
-    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms[bj]) + warp * RW;
-    const float4* ent = reinterpret_cast<const float4*>(ms[bj] + p.hdr_bytes);
+    const float* xs = patch_of(bj);
+    const int32_t* tb = tab_of(bj);
+    const uint8_t* msb = ms_of(bj);
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(msb) + warp * RW;
+    const float4* ent = reinterpret_cast<const float4*>(msb + p.hdr_bytes);
 #pragma unroll
     for (int r = 0; r < RW; ++r) {
       const uint32_t h = hdr[r];

@@ -11,7 +11,7 @@ import sdnn_synth as synth  # noqa: E402
 
 C, HW, B, sp = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), float(sys.argv[4])
 p = synth.make_conv_problem("pc", C, C, HW, HW, B, sp)
-h = sdnn.Handle(p.row_ptr, p.col_idx, p.vals, p.OC, p.K, split_rows=False)
+h = sdnn.Handle.for_conv(p.row_ptr, p.col_idx, p.vals, p.OC, p.IC, 3, 3)
 print(h.info())
 X = torch.from_numpy(p.x()).cuda()
 b = torch.from_numpy(p.bias).cuda()
