@@ -350,7 +350,9 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t*
   for (int32_t k = 1; k < cnt; ++k) v += ws[int64_t(first + k) * N + n];
   if (bias) v += bias[row];
   if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
-  for (int d = 0; d < yo.n; ++d) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+#pragma unroll
+  for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
+    if (d < yo.n) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
 }
 
 // Split-K (row kernel): Y[row] = act(Σ_{s < KS} kws[s][row] (slice order) + b[row]).  One thread per
@@ -365,7 +367,9 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ kws, int32_t KS, 
   for (int32_t s = 1; s < KS; ++s) v += kws[s * slice + int64_t(row) * N + n];
   if (bias) v += bias[row];
   if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
-  for (int d = 0; d < yo.n; ++d) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+#pragma unroll
+  for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
+    if (d < yo.n) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
 }
 
 // Fast path: TMA producer warp + W_c consumer warps, mbarrier stage ring.
@@ -502,8 +506,9 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = blockIdx.x % p.nrb;
   const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
-  float* xs[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + p.x_stage_bytes)};
-  uint8_t* ms[2] = {smem + 2 * size_t(p.x_stage_bytes), smem + 2 * size_t(p.x_stage_bytes) + p.m_stage_bytes};
+  // stage addresses from the shared-memory base (pointer arrays would become generic loads)
+  auto xs_of = [&](int b) { return reinterpret_cast<float*>(smem + size_t(b) * p.x_stage_bytes); };
+  auto ms_of = [&](int b) { return smem + 2 * size_t(p.x_stage_bytes) + size_t(b) * p.m_stage_bytes; };
   const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
   // this thread's column of the stage (blockDim.x is a multiple of TN) and its output pixel
   const int nn = int(threadIdx.x) % TN, kk0 = int(threadIdx.x) / TN, kstep = int(blockDim.x) / TN;
@@ -523,7 +528,7 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
       const int iy = iy0 + fy, ix = ix0 + fx;
       const bool ok = col_ok && k < p.K && iy >= 0 && iy < c.H && ix >= 0 && ix < c.W;
       const float* src = ok ? xb + ic * icstride + int64_t(iy) * c.W + ix : p.X;
-      cp_async4(xs[buf] + kk * TN + nn, src, ok);
+      cp_async4(xs_of(buf) + kk * TN + nn, src, ok);
       k += kstep;
       t += kstep;
       while (t >= FYX) {
@@ -533,7 +538,7 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
     }
     const int mbytes = int(off[j + 1] - off[j]);
     const uint8_t* msrc = p.meta + off[j];
-    for (int i = int(threadIdx.x); i < mbytes / 16; i += int(blockDim.x)) cp_async16(ms[buf] + 16 * i, msrc + 16 * i);
+    for (int i = int(threadIdx.x); i < mbytes / 16; i += int(blockDim.x)) cp_async16(ms_of(buf) + 16 * i, msrc + 16 * i);
     cp_async_commit();
   };
   float2 acc[RW][V / 2];
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
       cp_async_wait<0>();
     }
     __syncthreads();
-    consume_chunk<RW, V>(acc, xs[j & 1], ms[j & 1], warp, lane, p.hdr_bytes);
+    consume_chunk<RW, V>(acc, xs_of(j & 1), ms_of(j & 1), warp, lane, p.hdr_bytes);
     __syncthreads();
   }
   epilogue<RW, V, VEC>(acc, p, rb * p.wc + warp, lane, n0);
