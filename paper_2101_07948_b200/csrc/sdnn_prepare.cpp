@@ -565,6 +565,8 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     plan.max_block_bytes = int32_t(max_of(sizes));
     plan.blk_off.assign(sizes.size() + 1, 0);
     for (size_t i = 0; i < sizes.size(); ++i) plan.blk_off[i + 1] = plan.blk_off[i] + sizes[i];
+    // zero-filled: the partner slot of an odd row segment stays (column 0, weight 0.0), which the
+    // row kernel and the conv kernels read unconditionally as an entry pair
     plan.meta.assign(size_t(plan.blk_off.back()), 0);
     emit_blocks(csr_ptr, col_idx, vals, plan.row_orig, g, sizes, plan.meta.data(), &plan.blk_off, nullptr, &pcs);
     if (o.flags & SDNN_FLAG_PERMUTED_OUTPUT) {

@@ -51,6 +51,8 @@ def decode(p, plan):
                     continue
                 if V:  # TMEM format: segments padded to multiples of 4 (V = 4) / 2 (V = 8)
                     assert cnt % (4 if V == 4 else 2) == 0
+                elif cnt % 2:  # row format: an odd segment's partner slot is the zero entry the kernels read
+                    assert not np.any(ent[(start + cnt) * 8:(start + cnt) * 8 + 8])
                 for i in range(cnt):
                     e = ent[(start + i) * 8:(start + i) * 8 + 8]
                     cl = int(e[:4].view(np.uint32)[0])
