@@ -571,11 +571,11 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
 // column, pos(n) = (b·Hp + oy·stride − vr0)·Wp + ox·stride per output pixel.  A lane owns the
 // pixels n0 + lane + 32q (q < 4), so each of its four loads per nonzero is a conflict-free
 // warp-contiguous read and the epilogue stores are coalesced.
-template <int RW>
+template <int RW, int PX>
 __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p, const ConvGeom c, int32_t PSrows,
                                                                int32_t ICC) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int TN = 128;
+  constexpr int TN = 32 * PX;  // PX pixels per lane: 4, or 2 for small grids (twice the CTAs)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = int(blockDim.x) >> 5;
   const int rb = blockIdx.x % p.nrb;
   const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
@@ -594,9 +594,9 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
   // the tile's first virtual input row, and each lane's four pixels
   const int b0 = int(n0 / HWo), oy0 = int((n0 - int64_t(b0) * HWo) / c.Wo);
   const int vr0 = b0 * Hp + oy0 * c.stride;
-  int po[4];
+  int po[PX];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < PX; ++q) {
     const int64_t n = n0 + lane + 32 * q;
     const int b = int(n / HWo), rem = int(n - int64_t(b) * HWo), oy = rem / c.Wo, ox = rem - oy * c.Wo;
     po[q] = n < p.N ? (b * Hp + oy * c.stride - vr0) * Wp + ox * c.stride : 0;
@@ -628,9 +628,11 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
     for (int i = int(threadIdx.x); i < mbytes / 16; i += int(blockDim.x)) cp_async16(ms_of(buf) + 16 * i, msrc + 16 * i);
     cp_async_commit();
   };
-  float2 acc[RW][2];
+  float2 acc[RW][PX / 2];
 #pragma unroll
-  for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int q = 0; q < PX / 2; ++q) acc[r][q] = make_float2(0.f, 0.f);
   // split-K (gridDim.y > 1): this CTA's K chunks [j0, j1); raw partial sums to p.kws
   const int j0 = int(blockIdx.y) * p.nch / int(gridDim.y), j1 = (int(blockIdx.y) + 1) * p.nch / int(gridDim.y);
   gather(j0, 0);
@@ -658,14 +660,16 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
         {
           const float* xp = xs + tb[__float_as_int(ee.x)];
           const float2 w2 = make_float2(ee.y, ee.y);
-          acc[r][0] = __ffma2_rn(w2, make_float2(xp[po[0]], xp[po[1]]), acc[r][0]);
-          acc[r][1] = __ffma2_rn(w2, make_float2(xp[po[2]], xp[po[3]]), acc[r][1]);
+#pragma unroll
+          for (int q = 0; q < PX / 2; ++q)
+            acc[r][q] = __ffma2_rn(w2, make_float2(xp[po[2 * q]], xp[po[2 * q + 1]]), acc[r][q]);
         }
         {  // an odd row segment's partner slot is the zero entry (column 0, weight 0) of the packing
           const float* xp = xs + tb[__float_as_int(ee.z)];
           const float2 w2 = make_float2(ee.w, ee.w);
-          acc[r][0] = __ffma2_rn(w2, make_float2(xp[po[0]], xp[po[1]]), acc[r][0]);
-          acc[r][1] = __ffma2_rn(w2, make_float2(xp[po[2]], xp[po[3]]), acc[r][1]);
+#pragma unroll
+          for (int q = 0; q < PX / 2; ++q)
+            acc[r][q] = __ffma2_rn(w2, make_float2(xp[po[2 * q]], xp[po[2 * q + 1]]), acc[r][q]);
         }
       }
     }
@@ -677,10 +681,15 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
     const int32_t orow = p.row_orig[(rb * p.wc + warp) * RW + r];
     if (orow < 0) continue;
     const float bv = (p.bias && !p.kws) ? p.bias[orow] : 0.f;
-    float v[4] = {acc[r][0].x + bv, acc[r][0].y + bv, acc[r][1].x + bv, acc[r][1].y + bv};
+    float v[PX];
+#pragma unroll
+    for (int q = 0; q < PX / 2; ++q) {
+      v[2 * q] = acc[r][q].x + bv;
+      v[2 * q + 1] = acc[r][q].y + bv;
+    }
     float* yrow = p.kws ? p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N : p.Y + int64_t(orow) * p.N;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < PX; ++q) {
       const int64_t n = n0 + lane + 32 * q;
       const float y = (p.act == SDNN_ACT_RELU && !p.kws) ? (v[q] > 0.f ? v[q] : 0.f) : v[q];
       if (n < p.N) __stcs(yrow + n, y);
@@ -1805,10 +1814,15 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
   // patch form: the largest input window a tile needs (rows of the padded input, all images laid
   // end to end) and the channels a K chunk can touch
   {
+    // pixel tile: 4 pixels per lane (128), or 2 (64) when the 128-pixel grid is under one wave and
+    // the K range too short for split-K (few input channels: C = 32/64 at 7-28 px, 10-15 % faster;
+    // deeper K keeps 128 pixels and splits K instead, profiles/r01_conv_bench.jsonl)
+    const int PX = (nblocks < h->sms && pl.num_chunks < 16) ? 2 : 4;
+    const int64_t TNc = 32 * PX, nb2 = int64_t(pl.num_row_blocks) * ((N + TNc - 1) / TNc);
     const int64_t Hp = int64_t(H) + 2 * pad, HWo = int64_t(Ho) * Wo;
     int64_t rows = 0;
-    for (int64_t n0 = 0; n0 < N; n0 += TN) {
-      const int64_t n1 = std::min<int64_t>(n0 + TN, N) - 1;
+    for (int64_t n0 = 0; n0 < N; n0 += TNc) {
+      const int64_t n1 = std::min<int64_t>(n0 + TNc, N) - 1;
       const int64_t b0 = n0 / HWo, oy0 = (n0 - b0 * HWo) / Wo, b1 = n1 / HWo, oy1 = (n1 - b1 * HWo) / Wo;
       rows = std::max<int64_t>(rows, (b1 * Hp + oy1 * stride + FY - 1) - (b0 * Hp + oy0 * stride) + 1);
     }
@@ -1823,11 +1837,13 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
     }();
     const size_t smem2 = 2 * stage + size_t(rows * Wp) * 4;
     if (conv_env == 0 && smem2 <= size_t(kSmemBudget) && rows * Wp < (int64_t(1) << 30)) {
-      const void* fn2 = rw == 8 ? reinterpret_cast<const void*>(spmm_conv2_kernel<8>)
-                                : reinterpret_cast<const void*>(spmm_conv2_kernel<4>);
+      const void* fn2 = rw == 8 ? (PX == 2 ? reinterpret_cast<const void*>(spmm_conv2_kernel<8, 2>)
+                                           : reinterpret_cast<const void*>(spmm_conv2_kernel<8, 4>))
+                                : (PX == 2 ? reinterpret_cast<const void*>(spmm_conv2_kernel<4, 2>)
+                                           : reinterpret_cast<const void*>(spmm_conv2_kernel<4, 4>));
       SDNN_CUDA_TRY(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
       // split-K as for the row kernel: small images leave the GPU under-filled (few pixel tiles)
-      const int64_t warps = nblocks * wc;
+      const int64_t warps = nb2 * wc;
       int KS = 1;
       if (!pl.no_split_k && warps <= 8 * int64_t(h->sms) && pl.num_chunks >= 16)
         KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / 4, 16 * int64_t(h->sms) / warps})));
@@ -1839,7 +1855,7 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
       p.M = pl.M;
       int32_t psr = int32_t(rows), icc = int32_t(ICC);
       void* args2[] = {&p, const_cast<ConvGeom*>(&cg), &psr, &icc};
-      cudaError_t le = cudaLaunchKernel(fn2, dim3(unsigned(nblocks), unsigned(KS)), dim3(unsigned(wc * 32)), args2,
+      cudaError_t le = cudaLaunchKernel(fn2, dim3(unsigned(nb2), unsigned(KS)), dim3(unsigned(wc * 32)), args2,
                                         smem2, st_);
       if (le == cudaSuccess && KS > 1) {
         splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(pl.M)), 256, 0, st_>>>(kws, KS, pl.M, bias, act,
