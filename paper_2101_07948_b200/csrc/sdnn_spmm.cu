@@ -805,10 +805,23 @@ template <> struct TmemLd<8> {
   }
 };
 
+// Split-K TMEM launches (gridDim.y slices): this CTA's chunk range [first, first + count), cut at
+// even chunks so a chunk's TMEM half (packed into the metadata as 256·(chunk mod 2)) matches the
+// half the CTA's own double buffer gives it.  One slice: all chunks.
+template <bool SPLIT> __device__ __forceinline__ int2 tmem_chunks(int nch) {
+  if constexpr (!SPLIT) {
+    return make_int2(0, nch);
+  } else {
+    const int pairs = (nch + 1) / 2, y = int(blockIdx.y), ny = int(gridDim.y);
+    const int a = 2 * (y * pairs / ny), b = min(nch, 2 * ((y + 1) * pairs / ny));
+    return make_int2(a, b - a);
+  }
+}
+
 // Consumer warp of TMEM lane quarter q, warp slot wi: the chunk loop (wait for the chunk's
 // metadata and TMEM half, 4 / 2 nonzeros per step: tcgen05.ld → FFMA2) and the fused epilogue.
-template <int V, bool MULTI>
-__device__ __forceinline__ void tmem_consume(const TmemParams<MULTI>& p, uint8_t* mring, uint64_t* mfull, uint64_t* mempty,
+template <int V, bool MULTI, bool SPLIT = false>
+__device__ __forceinline__ void tmem_consume(const TmemParams<MULTI || SPLIT>& p, uint8_t* mring, uint64_t* mfull, uint64_t* mempty,
                                              uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0, int q, int wi,
                                              int lane) {
   constexpr int RW = tmem_rows(V);
@@ -821,7 +834,8 @@ __device__ __forceinline__ void tmem_consume(const TmemParams<MULTI>& p, uint8_t
   for (int r = 0; r < RW; ++r)
 #pragma unroll
     for (int c = 0; c < 2 * G; ++c) acc[r][c] = make_float2(0.f, 0.f);
-  for (int j = 0; j < p.nch; ++j) {
+  const int nrel = tmem_chunks<SPLIT>(p.nch).y;
+  for (int j = 0; j < nrel; ++j) {
     const int h = j & 1, m = j % MS;
     mbar_wait(&mfull[m], (j / MS) & 1);
     mbar_wait(&tfull[h], (j >> 1) & 1);
@@ -898,17 +912,21 @@ __device__ __forceinline__ void tmem_consume(const TmemParams<MULTI>& p, uint8_t
   for (int r = 0; r < RW; ++r) {
     const int32_t orow = p.row_orig[(rb * kTmemPanels + wi) * RW + r];
     if (orow < 0) continue;
-    const float b = p.bias ? p.bias[orow] : 0.f;
+    const float b = (p.bias && !SPLIT) ? p.bias[orow] : 0.f;
     float* yrow = MULTI ? nullptr : p.Y + int64_t(orow) * p.N;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int64_t n = n0 + g * 512 + q * 128 + lane * 4;
       float v[4] = {acc[r][2 * g].x + b, acc[r][2 * g].y + b, acc[r][2 * g + 1].x + b, acc[r][2 * g + 1].y + b};
-      if (p.act == SDNN_ACT_RELU) {
+      if (p.act == SDNN_ACT_RELU && !SPLIT) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) v[t] = v[t] > 0.f ? v[t] : 0.f;
       }
-      if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
+      if constexpr (SPLIT) {  // split-K slice: raw partial sums (splitk_reduce_kernel adds bias, act)
+        if (n < p.N)
+          __stcs(reinterpret_cast<float4*>(p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N + n),
+                 make_float4(v[0], v[1], v[2], v[3]));
+      } else if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
         if (n < p.N)
           for (int d = 0; d < p.yo.n; ++d)
             __stcs(reinterpret_cast<float4*>(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n),
@@ -930,9 +948,9 @@ __device__ __forceinline__ void tmem_consume(const TmemParams<MULTI>& p, uint8_t
 template <int FILL> __host__ __device__ constexpr int tmem_side_warps() { return FILL ? 4 : 1; }
 // FILL 2: odd pieces of a chunk by tcgen05.cp (issued by filler 0 lane 0), even pieces by the four
 // filler warps with tcgen05.st — the two fill paths run side by side.
-template <int V, int FILL, bool MULTI = false>
+template <int V, int FILL, bool MULTI = false, bool SPLIT = false>
 __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 32, 1)
-    spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI> p) {
+    spmm_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI || SPLIT> p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 128 * V;
   constexpr int KC = tmem_kc(V);
@@ -980,8 +998,9 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
     const int q = warp & 3;  // warps 16..19 → lane quarters 0..3
     const uint32_t tq = tbase + (uint32_t(q * 32) << 16);
     const bool leader = warp == kTmemConsumers && lane == 0;
-    const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
-    const int total = p.nch * PPC;
+    const int2 jr = tmem_chunks<SPLIT>(p.nch);  // this CTA's chunks (all of them unless split-K)
+    const int64_t* off = p.blk_off + int64_t(rb) * p.nch + jr.x;
+    const int total = jr.y * PPC;
     const int32_t nb = int32_t(n0 / 128);
     auto load_piece = [&](int i) {
       const int s = i % S;
@@ -990,7 +1009,7 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
         return;
       }
       mbar_expect_tx(&slot_full[s], kTmemPieceBytes);
-      tma_load_3d(xring + size_t(s) * kTmemPieceBytes, &tmap, 0, nb, i * PK, &slot_full[s]);
+      tma_load_3d(xring + size_t(s) * kTmemPieceBytes, &tmap, 0, nb, (jr.x * PPC + i) * PK, &slot_full[s]);
     };
     auto load_meta = [&](int j) {
       const int m = j % MS;
@@ -1002,7 +1021,7 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
       for (int i = 0; i < S && i < total; ++i) load_piece(i);
       for (int j = 0; j < MS && j < p.nch; ++j) load_meta(j);
     }
-    for (int j = 0; j < p.nch; ++j) {
+    for (int j = 0; j < jr.y; ++j) {
       const int h = j & 1;
       if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
         mbar_wait(&tfree[h], ((j >> 1) - 1) & 1);
@@ -1105,7 +1124,7 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
     // one code copy for all four lane quarters (four specialised copies exceed the SM's
     // instruction cache: profiles/r01_tmem_fill_diag.log)
     if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0
-    tmem_consume<V, MULTI>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp & 3, warp >> 2, lane);
+    tmem_consume<V, MULTI, SPLIT>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp & 3, warp >> 2, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -1195,7 +1214,7 @@ static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, c
 }
 
 static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                               const YOut& yo, cudaStream_t stream) {
+                               const YOut& yo, cudaStream_t stream, int KS = 1, cudaMemPool_t pool = nullptr) {
   const Plan& pl = h->plan;
   const int V = tmem_v(pl.kernel), TN = 128 * V;
   const int64_t ntiles = (N + TN - 1) / TN;
@@ -1249,6 +1268,27 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   const unsigned grid = unsigned(nblocks);
   const bool multi = !(yo.n == 1 && yo.ld == N && yo.col0 == 0);
   if (multi && fill != 1) return fail(SDNN_ERR_UNSUPPORTED, "multi-destination TMEM launch needs the filler-warp fill");
+  if (KS > 1) {  // split-K slices (raw partial sums) + splitk_reduce_kernel
+    if (multi || fill != 1 || !pool) return fail(SDNN_ERR_INTERNAL, "TMEM split-K needs one destination and a pool");
+    KParamsY q{};
+    static_cast<KParams&>(q) = p;
+    float* kws = nullptr;
+    SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws), size_t(KS) * pl.M * size_t(N) * 4, pool, stream));
+    q.kws = kws;
+    q.M = pl.M;
+    const dim3 g2{grid, unsigned(KS)};
+    if (V == 8) spmm_tmem_kernel<8, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
+    else spmm_tmem_kernel<4, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
+    cudaError_t le = cudaGetLastError();
+    if (le == cudaSuccess) {
+      splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(pl.M)), 256, 0, stream>>>(kws, KS, pl.M, bias, act,
+                                                                                                 yo, N);
+      le = cudaGetLastError();
+    }
+    cudaFreeAsync(kws, stream);
+    if (le != cudaSuccess) return fail(SDNN_ERR_CUDA, std::string("TMEM split-K: ") + cudaGetErrorString(le));
+    return SDNN_OK;
+  }
   if (V == 8 && multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
   else if (V == 8 && fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
   else if (V == 8 && fill == 1) spmm_tmem_kernel<8, 1><<<grid, threads, smem, stream>>>(tmap, p);
@@ -1312,6 +1352,27 @@ static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const Y
   const int64_t ks = std::min<int64_t>({8, pl.num_chunks / 4, 16 * int64_t(h->sms) / warps});
   return ks >= 2 ? int(ks) : 1;
 }
+// TMEM plan with split-K: a call on the TMEM fast path whose grid is under half a wave (so
+// tmem_worth declined it) but whose K range is long: KS ≤ 8 slices (of ≥ 4 chunks, cut at even
+// chunks) bring the grid to about one wave, for N of at least one full TMEM tile
+// (profiles/r01_tmem_split_k.log: c2 768×3072 66 → 58 µs, 512×4096 N = 2048 116 → 85 µs; at
+// N = 256 half the tile's lanes idle and it lost).  SDNN_TMEM_SPLIT_K=0 disables it.
+static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo) {
+  const sdnn_handle_s* a = h->alt;
+  if (!a || h->plan.no_split_k || !h->ws_pool) return 0;
+  if (!(yo.n == 1 && yo.ld == N && yo.col0 == 0)) return 0;
+  if (!(N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))) return 0;
+  static const int env = [] {
+    const char* e = getenv("SDNN_TMEM_SPLIT_K");
+    return e ? atoi(e) : -1;
+  }();
+  if (env == 0) return 0;
+  const int64_t TN = 128 * tmem_v(a->plan.kernel);
+  const int64_t grid = int64_t(a->plan.num_row_blocks) * ((N + TN - 1) / TN);
+  if (2 * grid > h->sms || a->plan.num_chunks < 16 || N < TN) return 0;  // a partial TMEM tile wastes lanes
+  const int64_t ks = std::min<int64_t>({8, a->plan.num_chunks / 4, h->sms / grid});
+  return ks >= 2 ? int(ks) : 0;
+}
 static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
   if (!h->narrow) return false;
   const int64_t tn = 32 * row_tile_v(h->plan, N);
@@ -1321,6 +1382,8 @@ static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
 static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, const YOut& yo,
                           cudaStream_t stream) {
   if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
+  if (const int ks = tmem_split_for(h, X, N, yo); ks > 1)
+    return launch_tmem(h->alt, X, N, bias, act, yo, stream, ks, h->ws_pool);
   if (narrow_worth(h, N)) return launch(h->narrow, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
@@ -1557,6 +1620,12 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
@@ -1976,7 +2045,7 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
 sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const float* Y, int32_t* kernel) {
   if (!h || !kernel || N < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle / kernel or N < 0");
   const YOut yo = y_single(const_cast<float*>(Y), N);
-  if (tmem_worth(h->alt, X, N, yo)) {
+  if (tmem_worth(h->alt, X, N, yo) || tmem_split_for(h, X, N, yo) > 1) {
     *kernel = h->alt->plan.kernel;
     return SDNN_OK;
   }

@@ -321,6 +321,33 @@ def test_split_k(sdnn, oracle_mod, M, K, N, sp, mask):
     np.testing.assert_array_equal(Yg.cpu().numpy(), Y)
 
 
+@pytest.mark.parametrize("M,K,N,mask", [(768, 3072, 1024, "uniform"), (768, 3072, 512, "lognormal"), (512, 4096, 2048, "uniform")])
+def test_tmem_split_k(sdnn, oracle_mod, M, K, N, mask):
+    """Auto calls on the TMEM fast path with too few CTAs but a long K run the TMEM kernel over
+    K-chunk slices (cut at even chunks) + the slice-ordered reduction: oracle parity, deterministic,
+    CUDA-graph capturable; SDNN_FLAG_NO_SPLIT_K falls back to the row plan."""
+    p = synth.make_problem(f"tsk{M}_{K}", M, K, N, 0.9, mask=mask)
+    X = p.x()
+    h = sdnn.Handle.from_problem(p)
+    assert h.kernel_for(N, 256, 256) == 4  # the TMEM plan takes the call
+    Y, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    Y2, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Y, Y2)
+    Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, want_scale=True)[:2]
+    assert_parity(Y, Yo, S, "TMEM split-K")
+    hn = sdnn.Handle.from_problem(p, split_k=False)
+    assert hn.kernel_for(N, 256, 256) != 4
+    Xd, b = torch.from_numpy(X).cuda(), torch.from_numpy(p.bias).cuda()
+    Yg = torch.empty((p.M, p.N), device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        h.spmm(Xd, b, act=1, out=Yg)
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(Yg.cpu().numpy(), Y)
+
+
 def test_get_permutation_and_info(sdnn, oracle_mod):
     p = synth.config_problem("c2_768x768")
     h = sdnn.Handle.from_problem(p)
