@@ -496,6 +496,10 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool valid) {  // zero-fill when !valid
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -571,7 +575,10 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
 // column, pos(n) = (b·Hp + oy·stride − vr0)·Wp + ox·stride per output pixel.  A lane owns the
 // pixels n0 + lane + 32q (q < 4), so each of its four loads per nonzero is a conflict-free
 // warp-contiguous read and the epilogue stores are coalesced.
-template <int RW, int PX>
+// V16 (W % 4 = 0): each patch row keeps a 4-float left margin so the image row lands 16-byte
+// aligned at column 4 and is filled with 16-byte cp.async (a quarter of the copies); margins, pad
+// columns and rows outside the image are zeroed once per kernel and never written again.
+template <int RW, int PX, bool V16>
 __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p, const ConvGeom c, int32_t PSrows,
                                                                int32_t ICC) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -579,7 +586,10 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = int(blockDim.x) >> 5;
   const int rb = blockIdx.x % p.nrb;
   const int64_t n0 = int64_t(blockIdx.x / p.nrb) * TN;
-  const int Hp = c.H + 2 * c.pad, Wp = c.W + 2 * c.pad, PS = PSrows * Wp, FYX = c.FY * c.FX;
+  // padded row: Wp columns; in smem a row is RS floats, padded column xp at smem column xp + CO
+  const int Hp = c.H + 2 * c.pad, Wp = c.W + 2 * c.pad, FYX = c.FY * c.FX;
+  const int CO = V16 ? 4 - c.pad : 0, RS = V16 ? ((4 + c.W + c.pad + 3) & ~3) : Wp, PS = PSrows * RS;
+  const int W4 = c.W >> 2;  // V16: 16-byte pieces per image row
   const int HWo = c.Ho * c.Wo;
   const size_t stage = ((size_t(ICC) * PS * 4 + size_t(p.kc) * 4 + 127) & ~size_t(127)) + size_t(p.m_stage_bytes);
   // srcoff[e], e < PS: offset of patch element e (row e / Wp, column e mod Wp) within one input
@@ -599,12 +609,27 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
   for (int q = 0; q < PX; ++q) {
     const int64_t n = n0 + lane + 32 * q;
     const int b = int(n / HWo), rem = int(n - int64_t(b) * HWo), oy = rem / c.Wo, ox = rem - oy * c.Wo;
-    po[q] = n < p.N ? (b * Hp + oy * c.stride - vr0) * Wp + ox * c.stride : 0;
+    po[q] = n < p.N ? (b * Hp + oy * c.stride - vr0) * RS + ox * c.stride + CO : CO;
   }
   const int64_t icstride = int64_t(c.B) * c.H * c.W;
-  for (int e = int(threadIdx.x); e < PS; e += int(blockDim.x)) {
-    const int r = e / Wp, xp = e - r * Wp, vr = vr0 + r, b = vr / Hp, iy = vr - b * Hp - c.pad, ix = xp - c.pad;
-    srcoff[e] = (b < c.B && iy >= 0 && iy < c.H && ix >= 0 && ix < c.W) ? (b * c.H + iy) * c.W + ix : -1;
+  if constexpr (V16) {
+    // items e < PSrows·W4: row r = e / W4, piece c4; srcoff = element offset of the piece, −1 if the
+    // row is outside the image (stays zero)
+    for (int e = int(threadIdx.x); e < PSrows * W4; e += int(blockDim.x)) {
+      const int r = e / W4, c4 = e - r * W4, vr = vr0 + r, b = vr / Hp, iy = vr - b * Hp - c.pad;
+      srcoff[e] = (b < c.B && iy >= 0 && iy < c.H) ? (b * c.H + iy) * c.W + 4 * c4 : -1;
+      srcoff[PSrows * W4 + e] = r * RS + 4 + 4 * c4;  // destination float offset within a channel
+    }
+    float* z = reinterpret_cast<float*>(smem);  // zero both stages' patches (margins, pad, outside rows)
+    for (int b2 = 0; b2 < 2; ++b2)
+      for (int e = int(threadIdx.x); e < ICC * PS; e += int(blockDim.x))
+        reinterpret_cast<float*>(smem + size_t(b2) * stage)[e] = 0.f;
+    (void)z;
+  } else {
+    for (int e = int(threadIdx.x); e < PS; e += int(blockDim.x)) {
+      const int r = e / Wp, xp = e - r * Wp, vr = vr0 + r, b = vr / Hp, iy = vr - b * Hp - c.pad, ix = xp - c.pad;
+      srcoff[e] = (b < c.B && iy >= 0 && iy < c.H && ix >= 0 && ix < c.W) ? (b * c.H + iy) * c.W + ix : -1;
+    }
   }
   __syncthreads();
   auto gather = [&](int j, int buf) {
@@ -613,15 +638,23 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p
       const int ic = ic_lo + icl;
       const float* src = p.X + int64_t(ic < c.IC ? ic : 0) * icstride;
       float* dst = patch_of(buf) + icl * PS;
-      for (int e = int(threadIdx.x); e < PS; e += int(blockDim.x)) {
-        const int so = srcoff[e];
-        const bool ok = so >= 0 && ic < c.IC;
-        cp_async4(dst + e, ok ? src + so : p.X, ok);
+      if constexpr (V16) {
+        for (int e = int(threadIdx.x); e < PSrows * W4; e += int(blockDim.x)) {
+          const int so = srcoff[e];
+          if (so < 0) continue;  // outside the image: zero since the kernel start
+          cp_async16z(dst + srcoff[PSrows * W4 + e], ic < c.IC ? src + so : p.X, ic < c.IC);
+        }
+      } else {
+        for (int e = int(threadIdx.x); e < PS; e += int(blockDim.x)) {
+          const int so = srcoff[e];
+          const bool ok = so >= 0 && ic < c.IC;
+          cp_async4(dst + e, ok ? src + so : p.X, ok);
+        }
       }
     }
     for (int cl = int(threadIdx.x); cl < p.kc; cl += int(blockDim.x)) {
       const int k = k0 + cl, ic = k / FYX, t = k - ic * FYX, fy = t / c.FX, fx = t - fy * c.FX;
-      tab_of(buf)[cl] = (ic - ic_lo) * PS + fy * Wp + fx;
+      tab_of(buf)[cl] = (ic - ic_lo) * PS + fy * RS + fx;
     }
     const int mbytes = int(off[j + 1] - off[j]);
     const uint8_t* msrc = p.meta + off[j];
@@ -1899,17 +1932,21 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
     // (k_chunk a multiple of FY·FX, e.g. 72 for 3×3), else up to two partial channels more
     const int64_t FYX = int64_t(FY) * FX, ICC = pl.k_chunk % FYX == 0 ? pl.k_chunk / FYX : (pl.k_chunk - 1) / FYX + 2;
     const int64_t Wp = int64_t(W) + 2 * pad;
-    const size_t stage = align_up(int64_t(ICC * rows * Wp * 4 + int64_t(pl.k_chunk) * 4), 128) + size_t(p.m_stage_bytes);
+    const bool v16 = W % 4 == 0 && pad <= 4 && reinterpret_cast<uintptr_t>(X) % 16 == 0;
+    const int64_t RS = v16 ? ((4 + int64_t(W) + pad + 3) & ~int64_t(3)) : Wp;
+    const size_t stage = align_up(int64_t(ICC * rows * RS * 4 + int64_t(pl.k_chunk) * 4), 128) + size_t(p.m_stage_bytes);
     static const int conv_env = [] {
       const char* e = getenv("SDNN_CONV_GATHER");
       return e ? atoi(e) : 0;
     }();
-    const size_t smem2 = 2 * stage + size_t(rows * Wp) * 4;
+    const size_t smem2 = 2 * stage + size_t(rows * (v16 ? 2 * (W / 4) : Wp)) * 4;
     if (conv_env == 0 && smem2 <= size_t(kSmemBudget) && rows * Wp < (int64_t(1) << 30)) {
-      const void* fn2 = rw == 8 ? (PX == 2 ? reinterpret_cast<const void*>(spmm_conv2_kernel<8, 2>)
-                                           : reinterpret_cast<const void*>(spmm_conv2_kernel<8, 4>))
-                                : (PX == 2 ? reinterpret_cast<const void*>(spmm_conv2_kernel<4, 2>)
-                                           : reinterpret_cast<const void*>(spmm_conv2_kernel<4, 4>));
+#define SDNN_CONV2(R, X_, V_) reinterpret_cast<const void*>(spmm_conv2_kernel<R, X_, V_>)
+      const void* fn2 = rw == 8 ? (PX == 2 ? (v16 ? SDNN_CONV2(8, 2, true) : SDNN_CONV2(8, 2, false))
+                                           : (v16 ? SDNN_CONV2(8, 4, true) : SDNN_CONV2(8, 4, false)))
+                                : (PX == 2 ? (v16 ? SDNN_CONV2(4, 2, true) : SDNN_CONV2(4, 2, false))
+                                           : (v16 ? SDNN_CONV2(4, 4, true) : SDNN_CONV2(4, 4, false)));
+#undef SDNN_CONV2
       SDNN_CUDA_TRY(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
       // split-K as for the row kernel: small images leave the GPU under-filled (few pixel tiles)
       const int64_t warps = nb2 * wc;
