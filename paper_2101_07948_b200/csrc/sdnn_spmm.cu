@@ -579,7 +579,9 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
 // aligned at column 4 and is filled with 16-byte cp.async (a quarter of the copies); margins, pad
 // columns and rows outside the image are zeroed once per kernel and never written again.
 template <int RW, int PX, bool V16>
-__global__ void __launch_bounds__(16 * 32, 1) spmm_conv2_kernel(const KParamsY p, const ConvGeom c, int32_t PSrows,
+// (min 2 resident 512-thread blocks → ≤ 64 registers: 4-warp CTAs then fit 8 per SM instead of 4;
+// 256 channels at 28×28: 231 → 180 µs, profiles/r01_conv_regcap.log)
+__global__ void __launch_bounds__(16 * 32, 2) spmm_conv2_kernel(const KParamsY p, const ConvGeom c, int32_t PSrows,
                                                                int32_t ICC) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * PX;  // PX pixels per lane: 4, or 2 for small grids (twice the CTAs)
