@@ -1953,8 +1953,11 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
       // split-K as for the row kernel: small images leave the GPU under-filled (few pixel tiles)
       const int64_t warps = nb2 * wc;
       int KS = 1;
-      if (!pl.no_split_k && warps <= 8 * int64_t(h->sms) && pl.num_chunks >= 16)
-        KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / 4, 16 * int64_t(h->sms) / warps})));
+      // (a conv chunk stages a whole input patch, so for shallow K (< 16 chunks) slices of ≥ 2 chunks
+      // already pay on a tiny grid: 64 channels at 7×7, 25 → 11 µs, profiles/r01_conv_split.log)
+      const int64_t per = pl.num_chunks >= 16 ? 4 : 2;
+      if (!pl.no_split_k && warps <= 8 * int64_t(h->sms) && pl.num_chunks >= 4)
+        KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / per, 16 * int64_t(h->sms) / warps})));
       cudaStream_t st_ = static_cast<cudaStream_t>(stream);
       float* kws = nullptr;
       if (KS > 1) SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws),

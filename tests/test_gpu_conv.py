@@ -55,7 +55,7 @@ def test_conv_no_bias_no_act_and_row_plans(sdnn):
 
 def test_one_by_one_conv_equals_spmm(sdnn):
     p = synth.make_conv_problem("c11", 64, 48, 10, 12, 2, 0.9, FY=1, FX=1, pad=0)
-    Yc, h = run(sdnn, p)
+    Yc, h = run(sdnn, p, split_k=False)  # bitwise: the same (unsplit) summation order on both sides
     X = torch.from_numpy(p.x().reshape(p.IC, -1).copy()).cuda()
     Ys = h.spmm(X, torch.from_numpy(p.bias).cuda(), act=1).cpu().numpy()
     np.testing.assert_array_equal(Yc.reshape(p.OC, -1), Ys)
