@@ -205,6 +205,20 @@ SDNN_API sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32
 SDNN_API sdnn_status sdnn_serialize(sdnn_handle h, void* buf, size_t* size);
 SDNN_API sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out);
 
+/* sdnn_tune: per-matrix autotuning ("we can perform autotuning on the sparse weight
+ * matrix to find the best settings for the microkernel and the tiling factor").  Times every path the
+ * handle can take for this N — TMEM plan, row plan, narrow row plan, each with split-K 1/2/4/8 — on
+ * the caller's DEVICE buffers X (K×N) and Y (M×N, overwritten), and keeps the fastest for every later
+ * fast-path call with this N (N % 4 == 0, 16-byte aligned X / Y, one destination).  Synchronises
+ * `stream`.  The built-in per-call rules are a candidate too and are kept unless a path beats them
+ * by more than 3 %.  path_out (optional) = −1 (the rules) or 16·path + slices (path 0 TMEM, 1 row,
+ * 2 narrow); us_out
+ * (optional) = its time per call in µs.  Results then follow the chosen path's summation order.
+ * Tuning state is per handle, guarded by a mutex, and not serialized.  Codegen handles →
+ * SDNN_ERR_UNSUPPORTED; N % 4 ≠ 0 or unaligned buffers → SDNN_ERR_INVALID_ARGUMENT. */
+SDNN_API sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* stream, int32_t* path_out,
+                               float* us_out);
+
 /* ------------------------------------------------------------------ introspection
  * sdnn_get_permutation: out_perm (HOST, M entries) receives order[i] = original row at permuted
  * position i (Algorithm 1 output, SPEC S:295 convention).  sdnn_get_info fills *info. */

@@ -25,7 +25,7 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
           4: "SDNN_ERR_OUT_OF_MEMORY", 5: "SDNN_ERR_CUDA", 6: "SDNN_ERR_DEVICE_MISMATCH", 7: "SDNN_ERR_INTERNAL"}
 
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
-EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_serialize",
+EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_serialize", "sdnn_tune",
            "sdnn_deserialize", "sdnn_spmm_host", "sdnn_spmm_kernel",
            "sdnn_get_permutation",
            "sdnn_get_info",
@@ -74,6 +74,7 @@ _lib.sdnn_spmm_kernel.argtypes = [_vp, _i64, _vp, _vp, ctypes.POINTER(_i32)]
 _lib.sdnn_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
 _lib.sdnn_csr_permute_columns.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
+_lib.sdnn_tune.argtypes = [_vp, _vp, _i64, _vp, _vp, ctypes.POINTER(_i32), ctypes.POINTER(ctypes.c_float)]
 _lib.sdnn_serialize.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_size_t)]
 _lib.sdnn_deserialize.argtypes = [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)]
 _lib.sdnn_conv2d.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]
@@ -228,6 +229,23 @@ class Handle:
         opts.setdefault("k_chunk", kc if kc <= 128 and IC * fyx >= 2 * kc else 0)
         opts.setdefault("split_rows", False)
         return cls(row_ptr, col_idx, vals, OC, IC * fyx, **opts)
+
+    def tune(self, X, out=None, stream=None) -> dict:
+        """sdnn_tune: measure every path for X's N and keep the fastest for later calls with that N.
+        Returns {"path": "tmem" | "row" | "narrow", "split_k": slices, "us": µs per call}."""
+        import torch
+        if X.dim() != 2 or X.shape[0] != self.K or X.dtype != torch.float32 or not X.is_cuda or not X.is_contiguous():
+            raise ValueError(f"X must be a contiguous CUDA float32 tensor of shape ({self.K}, N)")
+        N = X.shape[1]
+        if out is None:
+            out = torch.empty((self.M, N), dtype=torch.float32, device=X.device)
+        s = torch.cuda.current_stream(X.device) if stream is None else stream
+        path, us = _i32(0), ctypes.c_float(0)
+        _check(_lib.sdnn_tune(self._h, X.data_ptr(), N, out.data_ptr(), s.cuda_stream, ctypes.byref(path),
+                              ctypes.byref(us)), "sdnn_tune")
+        if path.value < 0:
+            return {"path": "auto", "split_k": 0, "us": us.value}
+        return {"path": ("tmem", "row", "narrow")[path.value // 16], "split_k": path.value % 16, "us": us.value}
 
     def serialize(self) -> bytes:
         """The prepared handle as a blob (sdnn_serialize): reload with Handle.deserialize."""

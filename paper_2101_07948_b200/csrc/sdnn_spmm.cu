@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <type_traits>
@@ -69,6 +70,13 @@ struct sdnn_handle_s {
   // auto handles: a row plan with more, smaller row blocks, for row-plan calls whose grid on the
   // main row plan is under one wave (small N: one or two N tiles)
   sdnn_handle_s* narrow = nullptr;
+  // sdnn_tune: measured best path per N (fast-path calls: one 16-byte-aligned destination)
+  struct Tuned {
+    int32_t path = -1;  // 0 TMEM plan, 1 row plan, 2 narrow row plan
+    int32_t ks = 1;     // split-K slices
+  };
+  std::map<int64_t, Tuned> tuned;
+  mutable std::mutex tune_mu;
   int32_t sms = 148;
   HostStage hs;         // sdnn_spmm_host staging (created on first use)
   std::mutex host_mu;
@@ -1414,16 +1422,11 @@ static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
   return int64_t(h->plan.num_row_blocks) * ((N + tn - 1) / tn) < h->sms;
 }
 
-static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, const YOut& yo,
-                          cudaStream_t stream) {
-  if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
-  if (const int ks = tmem_split_for(h, X, N, yo); ks > 1)
-    return launch_tmem(h->alt, X, N, bias, act, yo, stream, ks, h->ws_pool);
-  if (narrow_worth(h, N)) return launch(h->narrow, X, N, bias, act, yo, stream);
+// Row / group plan of h: split rows (stream-ordered workspace, reduced after the main kernel) and
+// split-K (ks_force < 0: automatic, splitk_for; else that many slices), then the kernel.
+static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                              const YOut& yo, cudaStream_t stream, int ks_force) {
   const Plan& pl = h->plan;
-  if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
-  if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))
-    return launch_tmem(h, X, N, bias, act, yo, stream);
   // split rows (row plan): a stream-ordered workspace for the pieces' partial sums, reduced after
   // the main kernel (no host synchronisation; allocation nodes under CUDA-graph capture)
   float* ws = nullptr;
@@ -1434,7 +1437,7 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
   }
   // split-K (row kernel, small grids): KS CTAs per (row block, N tile), each over a K-chunk range,
   // raw partial sums to a stream-ordered workspace, summed in slice order by splitk_reduce_kernel
-  const int KS = ns > 0 ? 1 : splitk_for(h, N, X, yo);
+  const int KS = ns > 0 ? 1 : (ks_force > 0 ? std::min(ks_force, pl.num_chunks) : splitk_for(h, N, X, yo));
   float* kws = nullptr;
   if (KS > 1)
     SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws), size_t(KS) * pl.M * size_t(N) * 4,
@@ -1459,6 +1462,50 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
     cudaFreeAsync(ws, stream);
   }
   return st;
+}
+
+// Fast-path call (aligned X / Y, one destination, N % 4 == 0) that sdnn_tune measured for this N.
+static bool tuned_for(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo, sdnn_handle_s::Tuned* t) {
+  if (!(yo.n == 1 && yo.ld == N && yo.col0 == 0) || N % 4 || reinterpret_cast<uintptr_t>(X) % 16 || !y_aligned16(yo))
+    return false;
+  std::lock_guard<std::mutex> lk(h->tune_mu);
+  const auto it = h->tuned.find(N);
+  if (it == h->tuned.end()) return false;
+  *t = it->second;
+  return true;
+}
+static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                               const YOut& yo, cudaStream_t stream);
+static sdnn_status launch_path(sdnn_handle_s* h, const sdnn_handle_s::Tuned& t, const float* X, int64_t N,
+                               const float* bias, int32_t act, const YOut& yo, cudaStream_t stream) {
+  if (t.path < 0) return launch_auto(h, X, N, bias, act, yo, stream);  // the built-in rules
+  if (t.path == 0) {
+    sdnn_handle_s* th = h->alt ? h->alt : h;
+    return launch_tmem(th, X, N, bias, act, yo, stream, t.ks, h->ws_pool);
+  }
+  return launch_row(t.path == 2 ? h->narrow : h, X, N, bias, act, yo, stream, t.ks);
+}
+
+static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                               const YOut& yo, cudaStream_t stream);
+static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act, const YOut& yo,
+                          cudaStream_t stream) {
+  sdnn_handle_s::Tuned t;
+  if (tuned_for(h, X, N, yo, &t) && t.path >= 0) return launch_path(h, t, X, N, bias, act, yo, stream);
+  return launch_auto(h, X, N, bias, act, yo, stream);
+}
+// The built-in per-call rules (what an untuned call takes).
+static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
+                               const YOut& yo, cudaStream_t stream) {
+  if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
+  if (const int ks = tmem_split_for(h, X, N, yo); ks > 1)
+    return launch_tmem(h->alt, X, N, bias, act, yo, stream, ks, h->ws_pool);
+  if (narrow_worth(h, N)) return launch(h->narrow, X, N, bias, act, yo, stream);
+  const Plan& pl = h->plan;
+  if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
+  if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))
+    return launch_tmem(h, X, N, bias, act, yo, stream);
+  return launch_row(h, X, N, bias, act, yo, stream, -1);
 }
 
 // The row / group / generic kernels of a plan (everything but TMEM and codegen).
@@ -1697,8 +1744,8 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     e = cudaMalloc(&h->d_split, tab.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_split, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
   }
-  // workspace pool of the split-row pieces and the split-K slices (row plans)
-  if (e == cudaSuccess && pl.kernel == 1) {
+  // workspace pool of the split-row pieces and the split-K slices (row and TMEM plans)
+  if (e == cudaSuccess && pl.kernel != 3) {
     cudaMemPoolProps props{};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
@@ -2087,6 +2134,11 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
 sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const float* Y, int32_t* kernel) {
   if (!h || !kernel || N < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle / kernel or N < 0");
   const YOut yo = y_single(const_cast<float*>(Y), N);
+  sdnn_handle_s::Tuned t;
+  if (tuned_for(h, X, N, yo, &t) && t.path >= 0) {
+    *kernel = t.path == 0 ? (h->alt ? h->alt->plan.kernel : h->plan.kernel) : 1;
+    return SDNN_OK;
+  }
   if (tmem_worth(h->alt, X, N, yo) || tmem_split_for(h, X, N, yo) > 1) {
     *kernel = h->alt->plan.kernel;
     return SDNN_OK;
@@ -2264,6 +2316,68 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
   parts[0]->alt = parts[1];
   parts[0]->narrow = parts[2];
   *out = parts[0];
+  return SDNN_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// sdnn_tune: time every applicable path for this N (TMEM plan, row plan, narrow row plan, each with
+// split-K 1/2/4/8) on the caller's buffers and keep the fastest for later calls with this N
+// (the paper's per-matrix autotuning).  Synchronises the stream.
+sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* stream, int32_t* path_out,
+                      float* us_out) {
+  if (!h || !X || !Y || N <= 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle / buffer or N <= 0");
+  if (h->plan.kernel == 3) return fail(SDNN_ERR_UNSUPPORTED, "codegen handles are not tuned");
+  const YOut yo = y_single(Y, N);
+  if (N % 4 || reinterpret_cast<uintptr_t>(X) % 16 || !y_aligned16(yo))
+    return fail(SDNN_ERR_INVALID_ARGUMENT, "sdnn_tune needs N % 4 == 0 and 16-byte aligned X and Y");
+  sdnn_status st = check_device(h);
+  if (st != SDNN_OK) return st;
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  std::vector<sdnn_handle_s::Tuned> cands{{-1, 0}};  // the built-in rules first (ties keep them)
+  const bool has_tmem = (h->alt || h->plan.kernel == 4 || h->plan.kernel == 5) && N % 128 == 0;
+  const bool row_ok = h->plan.kernel == 1 || h->plan.kernel == 2;
+  for (int ks : {1, 2, 4, 8}) {
+    if (has_tmem) cands.push_back({0, ks});
+    if (row_ok) cands.push_back({1, ks});
+    if (h->narrow) cands.push_back({2, ks});
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  SDNN_CUDA_TRY(cudaEventCreate(&e0));
+  SDNN_CUDA_TRY(cudaEventCreate(&e1));
+  float best = 0.f;
+  sdnn_handle_s::Tuned pick;
+  for (const auto& c : cands) {
+    if (c.path == 1 && c.ks > 1 && !h->plan.split_row.empty()) continue;  // split rows: no split-K
+    st = launch_path(h, c, X, N, nullptr, SDNN_ACT_NONE, yo, sm);          // warm-up
+    if (st != SDNN_OK) break;
+    cudaEventRecord(e0, sm);
+    for (int r = 0; r < 5 && st == SDNN_OK; ++r) st = launch_path(h, c, X, N, nullptr, SDNN_ACT_NONE, yo, sm);
+    cudaEventRecord(e1, sm);
+    if (st != SDNN_OK) break;
+    cudaError_t ce = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (ce == cudaSuccess) ce = cudaEventElapsedTime(&ms, e0, e1);
+    if (ce != cudaSuccess) {
+      st = fail(SDNN_ERR_CUDA, std::string("sdnn_tune: ") + cudaGetErrorString(ce));
+      break;
+    }
+    if (&c == &cands.front() || ms < 0.97f * best) {  // a path must beat the rules by > 3 %
+      best = ms;
+      pick = c;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st != SDNN_OK) return st;
+  {
+    std::lock_guard<std::mutex> lk(h->tune_mu);
+    h->tuned[N] = pick;
+  }
+  if (path_out) *path_out = pick.path < 0 ? -1 : pick.path * 16 + pick.ks;
+  if (us_out) *us_out = best * 1000.f / 5.f;
   return SDNN_OK;
 }
 

@@ -348,6 +348,26 @@ def test_tmem_split_k(sdnn, oracle_mod, M, K, N, mask):
     np.testing.assert_array_equal(Yg.cpu().numpy(), Y)
 
 
+@pytest.mark.parametrize("key,N", [("c2_768x3072", 1024), ("c3_512x512", 6272), ("c1", 128), ("narrow", 256)])
+def test_tune(sdnn, oracle_mod, key, N):
+    """sdnn_tune (per-matrix autotuning): the chosen path is kept for this N, its results match
+    the oracle and repeat bitwise, and other N keep the automatic choice."""
+    p = synth.make_problem("tn_nw", 2048, 1024, 256, 0.9) if key == "narrow" else synth.config_problem(key)
+    X = np.ascontiguousarray(p.x_cols(0, N))
+    h = sdnn.Handle.from_problem(p)
+    auto_kernel = h.kernel_for(N // 2 * 2 - 4 if N > 8 else N, 256, 256)
+    r = h.tune(torch.from_numpy(X).cuda())
+    assert r["path"] in ("auto", "tmem", "row", "narrow") and r["us"] > 0
+    if r["path"] != "auto":
+        assert r["split_k"] in (1, 2, 4, 8) and h.kernel_for(N, 256, 256) == (4 if r["path"] == "tmem" else 1)
+    Y, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    Y2, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Y, Y2)
+    Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, want_scale=True)[:2]
+    assert_parity(Y, Yo, S, f"tuned {r}")
+    assert h.kernel_for(N // 2 * 2 - 4 if N > 8 else N, 256, 256) == auto_kernel  # other N: untouched
+
+
 def test_get_permutation_and_info(sdnn, oracle_mod):
     p = synth.config_problem("c2_768x768")
     h = sdnn.Handle.from_problem(p)
