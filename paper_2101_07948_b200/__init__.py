@@ -25,7 +25,7 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
           4: "SDNN_ERR_OUT_OF_MEMORY", 5: "SDNN_ERR_CUDA", 6: "SDNN_ERR_DEVICE_MISMATCH", 7: "SDNN_ERR_INTERNAL"}
 
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
-EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_serialize", "sdnn_tune",
+EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_serialize", "sdnn_tune", "sdnn_conv2d_tune",
            "sdnn_deserialize", "sdnn_spmm_host", "sdnn_spmm_kernel",
            "sdnn_get_permutation",
            "sdnn_get_info",
@@ -74,6 +74,7 @@ _lib.sdnn_spmm_kernel.argtypes = [_vp, _i64, _vp, _vp, ctypes.POINTER(_i32)]
 _lib.sdnn_get_info.argtypes = [_vp, ctypes.POINTER(Info)]
 _lib.sdnn_permutation.argtypes = [_vp, _vp, _i32, _i32, _vp]
 _lib.sdnn_csr_permute_columns.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
+_lib.sdnn_conv2d_tune.argtypes = [_vp, _vp] + [_i32] * 8 + [_vp, _vp, ctypes.POINTER(_i32), ctypes.POINTER(ctypes.c_float)]
 _lib.sdnn_tune.argtypes = [_vp, _vp, _i64, _vp, _vp, ctypes.POINTER(_i32), ctypes.POINTER(ctypes.c_float)]
 _lib.sdnn_serialize.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_size_t)]
 _lib.sdnn_deserialize.argtypes = [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)]
@@ -229,6 +230,20 @@ class Handle:
         opts.setdefault("k_chunk", kc if kc <= 128 and IC * fyx >= 2 * kc else 0)
         opts.setdefault("split_rows", False)
         return cls(row_ptr, col_idx, vals, OC, IC * fyx, **opts)
+
+    def conv2d_tune(self, X, FY: int = 3, FX: int = 3, pad: int = 1, stride: int = 1, stream=None) -> dict:
+        """sdnn_conv2d_tune for X's geometry: {"pixels": 2 | 4 | 0 (rules), "split_k": slices, "us": µs}."""
+        import torch
+        IC, B, H, W = X.shape
+        Ho, Wo = (H + 2 * pad - FY) // stride + 1, (W + 2 * pad - FX) // stride + 1
+        out = torch.empty((self.M, B, Ho, Wo), dtype=torch.float32, device=X.device)
+        s = torch.cuda.current_stream(X.device) if stream is None else stream
+        ch, us = _i32(0), ctypes.c_float(0)
+        _check(_lib.sdnn_conv2d_tune(self._h, X.data_ptr(), B, IC, H, W, FY, FX, pad, stride, out.data_ptr(),
+                                     s.cuda_stream, ctypes.byref(ch), ctypes.byref(us)), "sdnn_conv2d_tune")
+        if ch.value < 0:
+            return {"pixels": 0, "split_k": 0, "us": us.value}
+        return {"pixels": ch.value // 16, "split_k": ch.value % 16, "us": us.value}
 
     def tune(self, X, out=None, stream=None) -> dict:
         """sdnn_tune: measure every path for X's N and keep the fastest for later calls with that N.

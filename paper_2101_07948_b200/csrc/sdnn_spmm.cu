@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -76,6 +77,8 @@ struct sdnn_handle_s {
     int32_t ks = 1;     // split-K slices
   };
   std::map<int64_t, Tuned> tuned;
+  // sdnn_conv2d_tune: per geometry {B, IC, H, W, FY, FX, pad, stride} → (pixels per lane, slices)
+  std::map<std::array<int32_t, 8>, std::pair<int32_t, int32_t>> conv_tuned;
   mutable std::mutex tune_mu;
   int32_t sms = 148;
   HostStage hs;         // sdnn_spmm_host staging (created on first use)
@@ -1915,9 +1918,28 @@ sdnn_status sdnn_spmm_multi(sdnn_handle h, const float* X, int64_t N, const floa
   return launch(h, X, N, bias, act, yo, static_cast<cudaStream_t>(stream));
 }
 
+static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t IC, int32_t H, int32_t W,
+                               int32_t FY, int32_t FX, int32_t pad, int32_t stride, const float* bias, int32_t act,
+                               float* Y, void* stream, int px_force, int ks_force);
+
 sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, int32_t H, int32_t W, int32_t FY,
                         int32_t FX, int32_t pad, int32_t stride, const float* bias, int32_t act, float* Y,
                         void* stream) {
+  int px = -1, ks = -1;
+  if (h) {
+    std::lock_guard<std::mutex> lk(h->tune_mu);
+    const auto it = h->conv_tuned.find({B, IC, H, W, FY, FX, pad, stride});
+    if (it != h->conv_tuned.end()) {
+      px = it->second.first;
+      ks = it->second.second;
+    }
+  }
+  return conv2d_impl(h, X, B, IC, H, W, FY, FX, pad, stride, bias, act, Y, stream, px, ks);
+}
+
+static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t IC, int32_t H, int32_t W,
+                               int32_t FY, int32_t FX, int32_t pad, int32_t stride, const float* bias, int32_t act,
+                               float* Y, void* stream, int px_force, int ks_force) {
   if (!h) return fail(SDNN_ERR_INVALID_ARGUMENT, "handle is NULL");
   if (B < 0 || IC < 1 || H < 1 || W < 1 || FY < 1 || FX < 1 || pad < 0 || stride < 1)
     return fail(SDNN_ERR_INVALID_ARGUMENT, "need B >= 0, IC, H, W, FY, FX, stride >= 1 and pad >= 0");
@@ -1968,7 +1990,7 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
     // pixel tile: 4 pixels per lane (128), or 2 (64) when the 128-pixel grid is under one wave and
     // the K range too short for split-K (few input channels: C = 32/64 at 7-28 px, 10-15 % faster;
     // deeper K keeps 128 pixels and splits K instead, profiles/r01_conv_bench.jsonl)
-    const int PX = (nblocks < h->sms && pl.num_chunks < 16) ? 2 : 4;
+    const int PX = px_force > 0 ? px_force : ((nblocks < h->sms && pl.num_chunks < 16) ? 2 : 4);
     const int64_t TNc = 32 * PX, nb2 = int64_t(pl.num_row_blocks) * ((N + TNc - 1) / TNc);
     const int64_t Hp = int64_t(H) + 2 * pad, HWo = int64_t(Ho) * Wo;
     int64_t rows = 0;
@@ -2003,7 +2025,9 @@ sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32_t IC, in
       // (a conv chunk stages a whole input patch, so for shallow K (< 16 chunks) slices of ≥ 2 chunks
       // already pay on a tiny grid: 64 channels at 7×7, 25 → 11 µs, profiles/r01_conv_split.log)
       const int64_t per = pl.num_chunks >= 16 ? 4 : 2;
-      if (!pl.no_split_k && warps <= 8 * int64_t(h->sms) && pl.num_chunks >= 4)
+      if (ks_force > 0)
+        KS = std::min(ks_force, pl.num_chunks);
+      else if (!pl.no_split_k && warps <= 8 * int64_t(h->sms) && pl.num_chunks >= 4)
         KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / per, 16 * int64_t(h->sms) / warps})));
       cudaStream_t st_ = static_cast<cudaStream_t>(stream);
       float* kws = nullptr;
@@ -2377,6 +2401,60 @@ sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* 
     h->tuned[N] = pick;
   }
   if (path_out) *path_out = pick.path < 0 ? -1 : pick.path * 16 + pick.ks;
+  if (us_out) *us_out = best * 1000.f / 5.f;
+  return SDNN_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// sdnn_conv2d_tune: time sdnn_conv2d's tile choices for this geometry (the built-in rules, then
+// 2 / 4 pixels per lane × 1 / 2 / 4 / 8 K slices) and keep the fastest (> 3 % better than the
+// rules) for later calls with the same geometry.  Synchronises the stream.
+sdnn_status sdnn_conv2d_tune(sdnn_handle h, const float* X, int32_t B, int32_t IC, int32_t H, int32_t W, int32_t FY,
+                             int32_t FX, int32_t pad, int32_t stride, float* Y, void* stream, int32_t* choice_out,
+                             float* us_out) {
+  if (!h || !X || !Y) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle or buffer");
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  std::vector<std::pair<int, int>> cands{{-1, -1}};
+  for (int px : {4, 2})
+    for (int ks : {1, 2, 4, 8}) cands.emplace_back(px, ks);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  SDNN_CUDA_TRY(cudaEventCreate(&e0));
+  SDNN_CUDA_TRY(cudaEventCreate(&e1));
+  float best = 0.f;
+  std::pair<int, int> pick{-1, -1};
+  sdnn_status st = SDNN_OK;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    const auto c = cands[i];
+    st = conv2d_impl(h, X, B, IC, H, W, FY, FX, pad, stride, nullptr, SDNN_ACT_NONE, Y, stream, c.first, c.second);
+    if (st != SDNN_OK) break;
+    cudaEventRecord(e0, sm);
+    for (int r = 0; r < 5 && st == SDNN_OK; ++r)
+      st = conv2d_impl(h, X, B, IC, H, W, FY, FX, pad, stride, nullptr, SDNN_ACT_NONE, Y, stream, c.first, c.second);
+    cudaEventRecord(e1, sm);
+    if (st != SDNN_OK) break;
+    cudaError_t ce = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (ce == cudaSuccess) ce = cudaEventElapsedTime(&ms, e0, e1);
+    if (ce != cudaSuccess) {
+      st = fail(SDNN_ERR_CUDA, std::string("sdnn_conv2d_tune: ") + cudaGetErrorString(ce));
+      break;
+    }
+    if (i == 0 || ms < 0.97f * best) {
+      best = ms;
+      pick = c;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st != SDNN_OK) return st;
+  {
+    std::lock_guard<std::mutex> lk(h->tune_mu);
+    h->conv_tuned[{B, IC, H, W, FY, FX, pad, stride}] = pick;
+  }
+  if (choice_out) *choice_out = pick.first < 0 ? -1 : pick.first * 16 + pick.second;
   if (us_out) *us_out = best * 1000.f / 5.f;
   return SDNN_OK;
 }
