@@ -1415,7 +1415,10 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   if (env == 0) return 0;
   const int64_t TN = 128 * tmem_v(a->plan.kernel);
   const int64_t grid = int64_t(a->plan.num_row_blocks) * ((N + TN - 1) / TN);
-  if (2 * grid > h->sms || a->plan.num_chunks < 16 || N < TN) return 0;  // a partial TMEM tile wastes lanes
+  // a partial TMEM tile wastes lanes; at a single TMEM tile (N < 2·TN) only long K (≥ 48 chunks)
+  // beat the row / narrow plans (profiles/r01_tune_shapes*.log: 2048², 1024² at N = 512 lost;
+  // 512×4096, 1024×4096 at N = 512 and every N ≥ 1024 won)
+  if (2 * grid > h->sms || N < TN || a->plan.num_chunks < (N >= 2 * TN ? 16 : 48)) return 0;
   const int64_t ks = std::min<int64_t>({8, a->plan.num_chunks / 4, h->sms / grid});
   return ks >= 2 ? int(ks) : 0;
 }
@@ -2027,8 +2030,8 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
       const int64_t per = pl.num_chunks >= 16 ? 4 : 2;
       if (ks_force > 0)
         KS = std::min(ks_force, pl.num_chunks);
-      else if (!pl.no_split_k && warps <= 8 * int64_t(h->sms) && pl.num_chunks >= 4)
-        KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / per, 16 * int64_t(h->sms) / warps})));
+      else if (!pl.no_split_k && warps <= 12 * int64_t(h->sms) && pl.num_chunks >= 4)  // ~24 warps/SM target
+        KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / per, 24 * int64_t(h->sms) / warps})));
       cudaStream_t st_ = static_cast<cudaStream_t>(stream);
       float* kws = nullptr;
       if (KS > 1) SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws),
