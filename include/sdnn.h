@@ -25,6 +25,7 @@
 #ifndef SDNN_H_
 #define SDNN_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus

@@ -87,3 +87,15 @@ def test_prepare_without_gpu_fails_cleanly():
     p = synth.config_problem("c1", N=4)
     e = _err(lambda: sdnn.Handle.from_problem(p))
     assert e.status in (5, 3)  # SDNN_ERR_CUDA (no device) — never a silent CPU fallback
+
+
+def test_header_is_plain_c99(tmp_path):
+    """include/sdnn.h is a C ABI: it must compile as C99 with -pedantic -Werror (no C++ types)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.c"
+    src.write_text('#include "sdnn.h"\nint main(void) { sdnn_info i; sdnn_perm_opts o; (void)i; (void)o; '
+                   'return (int)SDNN_OK; }\n')
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I",
+                           os.path.join(root, "include"), "-c", str(src), "-o", str(tmp_path / "t.o")])
