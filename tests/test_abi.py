@@ -99,3 +99,36 @@ def test_header_is_plain_c99(tmp_path):
                    'return (int)SDNN_OK; }\n')
     subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I",
                            os.path.join(root, "include"), "-c", str(src), "-o", str(tmp_path / "t.o")])
+
+
+def test_c_program_links_and_plans(tmp_path):
+    """A plain C program links libsdnn.so and runs the host-only API (Algorithm 1 and planning, no
+    GPU): the worked Alg. 1 trace of SPEC S:310 ({1}, {0,1,2}, {1,2} → [1, 2, 0])."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2101_07948_b200")
+    src = tmp_path / "p.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include "sdnn.h"
+int main(void) {
+  const int32_t rp[4] = {0, 1, 4, 6}, ci[6] = {1, 0, 1, 2, 1, 2};
+  const float v[6] = {1, 1, 1, 1, 1, 1};
+  int32_t order[3];
+  if (sdnn_permutation(rp, ci, 3, 3, order) != SDNN_OK) return 2;
+  sdnn_plan p = NULL;
+  if (sdnn_plan_create(rp, ci, v, 3, 3, NULL, &p) != SDNN_OK) return 3;
+  sdnn_info info;
+  info.struct_size = sizeof info;
+  if (sdnn_plan_get_info(p, &info) != SDNN_OK || info.nnz != 6) return 4;
+  sdnn_plan_destroy(p);
+  printf("%d %d %d\n", order[0], order[1], order[2]);
+  return 0;
+}
+""")
+    exe = tmp_path / "p"
+    subprocess.check_call(["gcc", "-std=c99", "-I", os.path.join(root, "include"), str(src), "-L", libdir, "-lsdnn",
+                           "-Wl,-rpath," + libdir, "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert out == ["1", "2", "0"]
