@@ -40,11 +40,15 @@ using namespace sdnn;
 
 // Persistent state of the host-buffer entry point: 3 streams (H2D, kernel, D2H), their events and
 // two device X/Y column-block buffers.
+#ifndef SDNN_HOST_BUFS  // sdnn_spmm_host pipeline depth (X/Y block buffers)
+#define SDNN_HOST_BUFS 2  // 3 or 4 measured no faster (profiles/r01_host_bufs.log): PCIe-bound
+#endif
+constexpr int kHostBufs = SDNN_HOST_BUFS;
 struct HostStage {
   cudaStream_t s[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev[3][2] = {};
-  float* x[2] = {nullptr, nullptr};
-  float* y[2] = {nullptr, nullptr};
+  cudaEvent_t ev[3][kHostBufs] = {};
+  float* x[kHostBufs] = {};
+  float* y[kHostBufs] = {};
   float* bias = nullptr;
   int64_t cols = 0;
 };
@@ -1851,11 +1855,11 @@ sdnn_status sdnn_destroy(sdnn_handle h) {
     HostStage& hs = h->hs;
     for (int i = 0; i < 3; ++i) {
       if (hs.s[i]) cudaStreamSynchronize(hs.s[i]);
-      for (int b = 0; b < 2; ++b)
+      for (int b = 0; b < kHostBufs; ++b)
         if (hs.ev[i][b]) cudaEventDestroy(hs.ev[i][b]);
       if (hs.s[i]) cudaStreamDestroy(hs.s[i]);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kHostBufs; ++b) {
       cudaFree(hs.x[b]);
       cudaFree(hs.y[b]);
     }
@@ -2099,20 +2103,20 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
   if (!hs.s[0]) {
     for (int i = 0; i < 3 && rs == SDNN_OK; ++i) {
       ck(cudaStreamCreateWithFlags(&hs.s[i], cudaStreamNonBlocking), "cudaStreamCreate");
-      for (int b = 0; b < 2 && rs == SDNN_OK; ++b)
+      for (int b = 0; b < kHostBufs && rs == SDNN_OK; ++b)
         ck(cudaEventCreateWithFlags(&hs.ev[i][b], cudaEventDisableTiming), "cudaEventCreate");
     }
     if (rs == SDNN_OK) ck(cudaMalloc(reinterpret_cast<void**>(&hs.bias), size_t(M * 4)), "cudaMalloc(bias)");
   }
   if (rs == SDNN_OK && hs.cols < nc) {
     ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kHostBufs; ++b) {
       cudaFree(hs.x[b]);
       cudaFree(hs.y[b]);
       hs.x[b] = hs.y[b] = nullptr;
     }
     hs.cols = 0;
-    for (int b = 0; b < 2 && rs == SDNN_OK; ++b) {
+    for (int b = 0; b < kHostBufs && rs == SDNN_OK; ++b) {
       ck(cudaMalloc(reinterpret_cast<void**>(&hs.x[b]), size_t(K * nc * 4)), "cudaMalloc(X block)");
       if (rs == SDNN_OK) ck(cudaMalloc(reinterpret_cast<void**>(&hs.y[b]), size_t(M * nc * 4)), "cudaMalloc(Y block)");
     }
@@ -2127,13 +2131,13 @@ sdnn_status sdnn_spmm_host(sdnn_handle h, const float* X_host, int64_t N, const 
   if (rs == SDNN_OK) {
     // s[0]: H2D copies, s[1]: kernels, s[2]: D2H copies.  ev[0][b]: X block in buffer b ready;
     // ev[1][b]: kernel on buffer b done; ev[2][b]: Y buffer b drained to host.
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kHostBufs; ++b) {
       ck(cudaEventRecord(hs.ev[1][b], s[1]), "cudaEventRecord");
       ck(cudaEventRecord(hs.ev[2][b], s[1]), "cudaEventRecord");
     }
     int i = 0;
     for (int64_t c0 = 0; c0 < N && rs == SDNN_OK; c0 += nc, ++i) {
-      const int b = i & 1;
+      const int b = i % kHostBufs;
       const int64_t w = std::min(nc, N - c0);
       ck(cudaStreamWaitEvent(s[0], hs.ev[1][b], 0), "cudaStreamWaitEvent");
       ck(cudaMemcpy2DAsync(hs.x[b], size_t(w * 4), X_host + c0, size_t(N * 4), size_t(w * 4), size_t(K),

@@ -7,6 +7,8 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("SDNN_PKG_DIR"):  # A/B runs: another build of the package
+    sys.path.insert(0, os.environ["SDNN_PKG_DIR"])
 
 import torch  # noqa: E402
 
