@@ -32,7 +32,8 @@ def parity(Y, Yo, S):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "group"])
-@pytest.mark.parametrize("key,N", [("c2_768x768", 1024), ("c2_768x768", 100), ("c3_512x512", 512)])
+@pytest.mark.parametrize("key,N", [("c2_768x768", 1024), ("c2_768x768", 100), ("c3_512x512", 512),
+                                   ("c2_768x3072", 1024)])  # the last: TMEM split-K under auto
 def test_permuted_output_is_permuted_rows(sdnn, key, N, kernel):
     p = synth.config_problem(key)
     X = torch.from_numpy(np.ascontiguousarray(p.x()[:, :N])).cuda()
