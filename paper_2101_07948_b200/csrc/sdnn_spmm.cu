@@ -11,6 +11,17 @@
 // P:135 fig:spmm / P:139 §3.2.2), in ascending column order.  The fused epilogue adds the bias,
 // applies ReLU (§3.1) and stores each row to its ORIGINAL position (inverse of the Algorithm 1
 // permutation).  No tensor cores (unstructured sparsity is not a dense contraction; north_star).
+//
+// Map of this file:
+//   * helpers (mbarrier, TMA, bulk / cp.async copies), parameter blocks (KParams / KParamsY / YOut);
+//   * row / group kernels (spmm_tma_kernel: TMA ring, V = 2/4/8 columns per lane, optional split-K
+//     slice via blockIdx.y), their generic bounds-checked twin, the split-row and split-K reductions;
+//   * sparse convolution (spmm_conv2_kernel: patch staged per tile; spmm_conv_kernel: gather form);
+//   * TMEM kernel (spmm_tmem_kernel: X tile in tensor memory, filler / consumer warps, optional
+//     multi-destination epilogue and split-K slice, each a separate template instance);
+//   * host side: upload (prepare_one), per-call path rules (launch_auto: TMEM / TMEM split-K /
+//     narrow / row / split-K), tuned paths (launch_path, sdnn_tune, sdnn_conv2d_tune), the C entry
+//     points, the host-buffer pipeline, serialization.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
