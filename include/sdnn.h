@@ -105,6 +105,8 @@ typedef struct {
   int32_t num_pieces;       /* total pieces of the split rows                                         */
   int32_t narrow_row_blocks; /* auto handles: row blocks of the narrow row plan (4-row panels) taken by
                                row-plan calls whose grid is under one wave; 0 = none                 */
+  int32_t narrow4_row_blocks; /* auto handles: row blocks of the second narrow plan (4-row panels, 4 per
+                               CTA) taken instead when its N-tile-128 grid is one to three waves; 0 = none */
 } sdnn_info;
 
 /* sdnn_perm_opts.flags */
@@ -208,12 +210,12 @@ SDNN_API sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle*
 
 /* sdnn_tune: per-matrix autotuning ("we can perform autotuning on the sparse weight
  * matrix to find the best settings for the microkernel and the tiling factor").  Times every path the
- * handle can take for this N — TMEM plan, row plan, narrow row plan, each with split-K 1/2/4/8 — on
+ * handle can take for this N — TMEM plan, row plan, narrow row plans, each with split-K 1/2/4/8 — on
  * the caller's DEVICE buffers X (K×N) and Y (M×N, overwritten), and keeps the fastest for every later
  * fast-path call with this N (N % 4 == 0, 16-byte aligned X / Y, one destination).  Synchronises
  * `stream`.  The built-in per-call rules are a candidate too and are kept unless a path beats them
  * by more than 3 %.  path_out (optional) = −1 (the rules) or 16·path + slices (path 0 TMEM, 1 row,
- * 2 narrow); us_out
+ * 2 narrow, 3 narrow4); us_out
  * (optional) = its time per call in µs.  Results then follow the chosen path's summation order.
  * Tuning state is per handle, guarded by a mutex, and not serialized.  Codegen handles →
  * SDNN_ERR_UNSUPPORTED; N % 4 ≠ 0 or unaligned buffers → SDNN_ERR_INVALID_ARGUMENT. */

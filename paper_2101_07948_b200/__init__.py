@@ -57,7 +57,7 @@ class Info(ctypes.Structure):
                 ("num_row_blocks", ctypes.c_int32), ("k_chunk", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("meta_bytes", ctypes.c_int64), ("max_block_bytes", ctypes.c_int32), ("alt_kernel", ctypes.c_int32),
                 ("max_panel_nnz", ctypes.c_int64), ("num_split_rows", ctypes.c_int32), ("num_pieces", ctypes.c_int32),
-                ("narrow_row_blocks", ctypes.c_int32)]
+                ("narrow_row_blocks", ctypes.c_int32), ("narrow4_row_blocks", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "struct_size"}
@@ -247,7 +247,7 @@ class Handle:
 
     def tune(self, X, out=None, stream=None) -> dict:
         """sdnn_tune: measure every path for X's N and keep the fastest for later calls with that N.
-        Returns {"path": "tmem" | "row" | "narrow", "split_k": slices, "us": µs per call}."""
+        Returns {"path": "tmem" | "row" | "narrow" | "narrow4", "split_k": slices, "us": µs per call}."""
         import torch
         if X.dim() != 2 or X.shape[0] != self.K or X.dtype != torch.float32 or not X.is_cuda or not X.is_contiguous():
             raise ValueError(f"X must be a contiguous CUDA float32 tensor of shape ({self.K}, N)")
@@ -260,7 +260,7 @@ class Handle:
                               ctypes.byref(us)), "sdnn_tune")
         if path.value < 0:
             return {"path": "auto", "split_k": 0, "us": us.value}
-        return {"path": ("tmem", "row", "narrow")[path.value // 16], "split_k": path.value % 16, "us": us.value}
+        return {"path": ("tmem", "row", "narrow", "narrow4")[path.value // 16], "split_k": path.value % 16, "us": us.value}
 
     def serialize(self) -> bytes:
         """The prepared handle as a blob (sdnn_serialize): reload with Handle.deserialize."""

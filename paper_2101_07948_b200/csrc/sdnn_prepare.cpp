@@ -616,6 +616,7 @@ static void fill_info(const Plan& p, int32_t device, sdnn_info* info) {
   info->num_split_rows = int32_t(p.split_row.size());
   info->num_pieces = int32_t(p.piece_row.size());
   info->narrow_row_blocks = 0;
+  info->narrow4_row_blocks = 0;
 }
 
 namespace sdnn {

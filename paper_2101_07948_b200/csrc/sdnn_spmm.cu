@@ -86,9 +86,12 @@ struct sdnn_handle_s {
   // auto handles: a row plan with more, smaller row blocks, for row-plan calls whose grid on the
   // main row plan is under one wave (small N: one or two N tiles)
   sdnn_handle_s* narrow = nullptr;
+  // and, when narrow has more than 4 panels per CTA, a plan of 4-panel (16-row) row blocks for the
+  // calls whose TN = 128 grid on it is one to three waves (narrow_pick)
+  sdnn_handle_s* narrow4 = nullptr;
   // sdnn_tune: measured best path per N (fast-path calls: one 16-byte-aligned destination)
   struct Tuned {
-    int32_t path = -1;  // 0 TMEM plan, 1 row plan, 2 narrow row plan
+    int32_t path = -1;  // 0 TMEM plan, 1 row plan, 2 narrow row plan, 3 narrow4 row plan
     int32_t ks = 1;     // split-K slices
   };
   std::map<int64_t, Tuned> tuned;
@@ -1433,14 +1436,34 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   // a partial TMEM tile wastes lanes; at a single TMEM tile (N < 2·TN) only long K (≥ 48 chunks)
   // beat the row / narrow plans (profiles/r01_tune_shapes*.log: 2048², 1024² at N = 512 lost;
   // 512×4096, 1024×4096 at N = 512 and every N ≥ 1024 won)
-  if (2 * grid > h->sms || N < TN || a->plan.num_chunks < (N >= 2 * TN ? 16 : 48)) return 0;
-  const int64_t ks = std::min<int64_t>({8, a->plan.num_chunks / 4, h->sms / grid});
+  // — unless the matrix is dense enough (≥ 20 % nonzeros) that a 32-chunk K range already pays
+  // (profiles/r01_tune_grid.log: 2048² at 70 / 80 %, N = 512: 113 → 88 µs, 81 → 71 µs)
+  const Plan& ap = a->plan;
+  const bool dense = 5 * ap.nnz >= int64_t(ap.M) * ap.K;
+  if (2 * grid > h->sms || N < TN || ap.num_chunks < (N >= 2 * TN ? 16 : dense ? 32 : 48)) return 0;
+  const int64_t ks = std::min<int64_t>({8, ap.num_chunks / 4, h->sms / grid});
+  // several TMEM tiles: the split CTAs must keep ≥ 3.5 MFLOP each, else the partial-sum round trip
+  // and the per-CTA fill start-up lose to the row plans (r01_tune_grid.log: 1024² at 80-95 % and
+  // 2048² at 95 %, N = 1024: 35-70 µs against 21-63 µs; c2 768×3072, N = 1024, 3.7 MFLOP, still wins)
+  if (N >= 2 * TN && ap.nnz * N * 4 < int64_t(7000000) * grid * ks) return 0;
   return ks >= 2 ? int(ks) : 0;
 }
 static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
   if (!h->narrow) return false;
   const int64_t tn = 32 * row_tile_v(h->plan, N);
   return int64_t(h->plan.num_row_blocks) * ((N + tn - 1) / tn) < h->sms;
+}
+// The narrow plan a call takes: 16-row blocks (5-warp CTAs, TN = 128) when that grid is one to three
+// waves, else the ≥ 64-block plan (profiles/r01_tune_grid.log, N = 128 / 256: 4096² 169 → 127 µs at
+// 70 % and 72 → 67 µs at 90 %, 3072² 109 → 78 µs and 57 → 42 µs, 2048² at N = 256 75 → 67 µs; the
+// 4096², N = 256 grid of 512 CTAs and the 2048², N = 128 grid of 128 lost).
+static sdnn_handle_s* narrow_pick(const sdnn_handle_s* h, int64_t N) {
+  if (!narrow_worth(h, N)) return nullptr;
+  if (h->narrow4) {
+    const int64_t g = int64_t(h->narrow4->plan.num_row_blocks) * ((N + 127) / 128);
+    if (g > h->sms && g <= 3 * int64_t(h->sms)) return h->narrow4;
+  }
+  return h->narrow;
 }
 
 // Row / group plan of h: split rows (stream-ordered workspace, reduced after the main kernel) and
@@ -1504,7 +1527,7 @@ static sdnn_status launch_path(sdnn_handle_s* h, const sdnn_handle_s::Tuned& t, 
     sdnn_handle_s* th = h->alt ? h->alt : h;
     return launch_tmem(th, X, N, bias, act, yo, stream, t.ks, h->ws_pool);
   }
-  return launch_row(t.path == 2 ? h->narrow : h, X, N, bias, act, yo, stream, t.ks);
+  return launch_row(t.path == 3 ? h->narrow4 : t.path == 2 ? h->narrow : h, X, N, bias, act, yo, stream, t.ks);
 }
 
 static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
@@ -1521,7 +1544,7 @@ static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, cons
   if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
   if (const int ks = tmem_split_for(h, X, N, yo); ks > 1)
     return launch_tmem(h->alt, X, N, bias, act, yo, stream, ks, h->ws_pool);
-  if (narrow_worth(h, N)) return launch(h->narrow, X, N, bias, act, yo, stream);
+  if (sdnn_handle_s* nw = narrow_pick(h, N)) return launch(nw, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
   if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))
@@ -1850,6 +1873,18 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
         return fail(st, m);
       }
       (*out)->narrow = nar;
+      if (wc > 4 && (M + 15) / 16 > nar->plan.num_row_blocks) {
+        n.cta_panels = 4;
+        sdnn_handle nar4 = nullptr;
+        st = prepare_one(csr_ptr, col_idx, vals, M, K, &n, &nar4, perm);
+        if (st != SDNN_OK) {
+          std::string m = sdnn_last_error_message();
+          sdnn_destroy(*out);
+          *out = nullptr;
+          return fail(st, m);
+        }
+        (*out)->narrow4 = nar4;
+      }
     }
   }
   return SDNN_OK;
@@ -1859,6 +1894,7 @@ sdnn_status sdnn_destroy(sdnn_handle h) {
   if (!h) return SDNN_OK;
   if (h->alt) sdnn_destroy(h->alt);
   if (h->narrow) sdnn_destroy(h->narrow);
+  if (h->narrow4) sdnn_destroy(h->narrow4);
   int cur = -1;
   cudaGetDevice(&cur);
   if (cur != h->device) cudaSetDevice(h->device);
@@ -2185,7 +2221,7 @@ sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const flo
     *kernel = h->alt->plan.kernel;
     return SDNN_OK;
   }
-  if (narrow_worth(h, N)) return sdnn_spmm_kernel(h->narrow, N, X, Y, kernel);
+  if (sdnn_handle_s* nw = narrow_pick(h, N)) return sdnn_spmm_kernel(nw, N, X, Y, kernel);
   const int k = h->plan.kernel;
   const bool tma = N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo);
   *kernel = (k == 4 || k == 5) ? (N % 128 == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
@@ -2205,6 +2241,7 @@ sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info) {
   info->meta_bytes = h->plan.meta_size_uploaded;
   info->alt_kernel = h->alt ? h->alt->plan.kernel : 0;
   info->narrow_row_blocks = h->narrow ? h->narrow->plan.num_row_blocks : 0;
+  info->narrow4_row_blocks = h->narrow4 ? h->narrow4->plan.num_row_blocks : 0;
   return SDNN_OK;
 }
 
@@ -2212,9 +2249,9 @@ sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info) {
 
 // ------------------------------------------------------------------------------------------------
 // Serialization of a prepared handle (the paper's reusable preparation): every plan
-// of the handle (main, TMEM, narrow) with its packed metadata, so a process can skip Algorithm 1
-// and the packing.  Blob: "SDNNPLAN", u32 version, u32 plan count, then per plan a u32 role
-// (0 main, 1 TMEM, 2 narrow) and its fields in a fixed order (little-endian, sizes as u64).
+// of the handle (main, TMEM, narrow, narrow4) with its packed metadata, so a process can skip
+// Algorithm 1 and the packing.  Blob: "SDNNPLAN", u32 version, u32 plan count, then per plan a u32
+// role (0 main, 1 TMEM, 2 narrow, 3 narrow4) and its fields in a fixed order (little-endian, sizes as u64).
 namespace {
 constexpr uint32_t kBlobVersion = 1;
 struct BlobW {
@@ -2283,7 +2320,7 @@ extern "C" {
 
 sdnn_status sdnn_serialize(sdnn_handle h, void* buf, size_t* size) {
   if (!h || !size) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle or size");
-  const sdnn_handle_s* parts[3] = {h, h->alt, h->narrow};
+  const sdnn_handle_s* parts[4] = {h, h->alt, h->narrow, h->narrow4};
   for (const sdnn_handle_s* q : parts)
     if (q && q->plan.kernel == 3)
       return fail(SDNN_ERR_UNSUPPORTED, "codegen plans are JIT-compiled from the CSR and are not serialized");
@@ -2294,8 +2331,8 @@ sdnn_status sdnn_serialize(sdnn_handle h, void* buf, size_t* size) {
     const char magic[8] = {'S', 'D', 'N', 'N', 'P', 'L', 'A', 'N'};
     w.b.insert(w.b.end(), magic, magic + 8);
     w.s(kBlobVersion);
-    w.s(uint32_t((h->alt ? 1 : 0) + (h->narrow ? 1 : 0) + 1));
-    for (uint32_t role = 0; role < 3; ++role) {
+    w.s(uint32_t((h->alt ? 1 : 0) + (h->narrow ? 1 : 0) + (h->narrow4 ? 1 : 0) + 1));
+    for (uint32_t role = 0; role < 4; ++role) {
       if (!parts[role]) continue;
       Plan pl;
       st = plan_with_meta(parts[role], pl);
@@ -2330,8 +2367,8 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
   r.s(ver);
   r.s(count);
   if (!r.ok || ver != kBlobVersion) return fail(SDNN_ERR_UNSUPPORTED, "blob version " + std::to_string(ver) + " != 1");
-  if (count < 1 || count > 3) return fail(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan count)");
-  sdnn_handle parts[3] = {nullptr, nullptr, nullptr};
+  if (count < 1 || count > 4) return fail(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan count)");
+  sdnn_handle parts[4] = {nullptr, nullptr, nullptr, nullptr};
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     for (auto& q : parts)
       if (q) sdnn_destroy(q);
@@ -2339,11 +2376,11 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
   };
   try {
     for (uint32_t i = 0; i < count; ++i) {
-      uint32_t role = 3;
+      uint32_t role = 4;
       r.s(role);
       Plan pl;
       plan_fields(r, pl);
-      if (!r.ok || role > 2 || parts[role] || !plan_sane(pl) || (role == 0) != (i == 0))
+      if (!r.ok || role > 3 || parts[role] || (role == 3 && !parts[2]) || !plan_sane(pl) || (role == 0) != (i == 0))
         return cleanup(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan " + std::to_string(i) + ")");
       sdnn_status st = prepare_one(nullptr, nullptr, nullptr, pl.M, pl.K, nullptr, &parts[role], nullptr, &pl);
       if (st != SDNN_OK) {
@@ -2357,6 +2394,7 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
   if (r.off != size) return cleanup(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (trailing bytes)");
   parts[0]->alt = parts[1];
   parts[0]->narrow = parts[2];
+  parts[0]->narrow4 = parts[3];
   *out = parts[0];
   return SDNN_OK;
 }
@@ -2365,7 +2403,7 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
 
 extern "C" {
 
-// sdnn_tune: time every applicable path for this N (TMEM plan, row plan, narrow row plan, each with
+// sdnn_tune: time every applicable path for this N (TMEM plan, row plan, narrow row plans, each with
 // split-K 1/2/4/8) on the caller's buffers and keep the fastest for later calls with this N
 // (the paper's per-matrix autotuning).  Synchronises the stream.
 sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* stream, int32_t* path_out,
@@ -2385,6 +2423,7 @@ sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* 
     if (has_tmem) cands.push_back({0, ks});
     if (row_ok) cands.push_back({1, ks});
     if (h->narrow) cands.push_back({2, ks});
+    if (h->narrow4) cands.push_back({3, ks});
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   SDNN_CUDA_TRY(cudaEventCreate(&e0));

@@ -273,7 +273,7 @@ def test_auto_takes_tmem_plan_when_it_fills_a_wave(sdnn):
     assert h.kernel_for(p.N) == 4 and h.kernel_for(102) == -1 and h.kernel_for(128) == 1  # 35·1·2 < 148
 
 
-@pytest.mark.parametrize("M,K,sp", [(2048, 2048, 0.9), (4096, 1024, 0.7)])
+@pytest.mark.parametrize("M,K,sp", [(2048, 2048, 0.9), (4096, 1024, 0.7), (3072, 3072, 0.9)])
 def test_auto_narrow_row_plan_for_small_grids(sdnn, oracle_mod, M, K, sp):
     """An auto handle whose row plan has few row blocks also keeps a narrow row plan (4-row panels,
     ≥ 64 row blocks, same permutation) for row-plan calls under one wave of CTAs (small N).  Same
@@ -282,8 +282,10 @@ def test_auto_narrow_row_plan_for_small_grids(sdnn, oracle_mod, M, K, sp):
     h = sdnn.Handle.from_problem(p, split_k=False)
     info = h.info()
     assert info["narrow_row_blocks"] >= 64 and info["narrow_row_blocks"] > info["num_row_blocks"]
+    # and the 16-row-block plan (narrow4) for N-tile-128 grids of one to three waves
+    assert info["narrow4_row_blocks"] == (M + 15) // 16
     hr = sdnn.Handle.from_problem(p, kernel="row", split_k=False)
-    assert hr.info()["narrow_row_blocks"] == 0
+    assert hr.info()["narrow_row_blocks"] == 0 and hr.info()["narrow4_row_blocks"] == 0
     for N in (128, 256, 100):
         X = np.ascontiguousarray(p.x()[:, :N])
         Ya, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
@@ -357,7 +359,7 @@ def test_tune(sdnn, oracle_mod, key, N):
     h = sdnn.Handle.from_problem(p)
     auto_kernel = h.kernel_for(N // 2 * 2 - 4 if N > 8 else N, 256, 256)
     r = h.tune(torch.from_numpy(X).cuda())
-    assert r["path"] in ("auto", "tmem", "row", "narrow") and r["us"] > 0
+    assert r["path"] in ("auto", "tmem", "row", "narrow", "narrow4") and r["us"] > 0
     if r["path"] != "auto":
         assert r["split_k"] in (1, 2, 4, 8) and h.kernel_for(N, 256, 256) == (4 if r["path"] == "tmem" else 1)
     Y, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
