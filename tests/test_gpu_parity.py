@@ -295,6 +295,23 @@ def test_auto_narrow_row_plan_for_small_grids(sdnn, oracle_mod, M, K, sp):
         assert_parity(Ya, Yo, S, f"narrow N={N}")
 
 
+@pytest.mark.parametrize("M,K,N,sp", [(3072, 3072, 128, 0.9), (4096, 4096, 128, 0.7), (2048, 2048, 256, 0.95),
+                                      (3072, 3072, 200, 0.9)])
+def test_auto_narrow4_with_split_k(sdnn, oracle_mod, M, K, N, sp):
+    """Auto handles at N where the 16-row-block plan (narrow4) takes the call — with split-K where its
+    grid leaves SMs under-filled (3072², N = 128: 192 CTAs of 5 warps → 2 slices), and N = 200
+    (ragged tail tile): oracle parity and bitwise repeatability."""
+    p = synth.make_problem(f"n4_{M}_{sp}", M, K, N, sp)
+    h = sdnn.Handle.from_problem(p)
+    assert h.info()["narrow4_row_blocks"] == (M + 15) // 16
+    X = p.x()
+    Y, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    Y2, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Y, Y2)
+    Yo, S = oracle_mod.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1, want_scale=True)[:2]
+    assert_parity(Y, Yo, S, f"narrow4 {M}x{K} N={N}")
+
+
 @pytest.mark.parametrize("M,K,N,sp,mask", [(512, 4096, 128, 0.9, "uniform"), (768, 3072, 128, 0.9, "uniform"),
                                             (768, 3072, 64, 0.9, "lognormal"), (256, 2048, 96, 0.8, "uniform")])
 def test_split_k(sdnn, oracle_mod, M, K, N, sp, mask):
