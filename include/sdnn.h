@@ -293,6 +293,9 @@ SDNN_API int32_t sdnn_abi_version(void);
  *   SDNN_SPLIT_K     row kernel: force this many K slices (1 = never split); default: automatic for
  *                    under-filled calls (see SDNN_FLAG_NO_SPLIT_K)
  *   SDNN_CONV_GATHER 1 = sdnn_conv2d stages the virtual matrix itself instead of the input patch
+ *   SDNN_ROW_V       2 | 4: row kernel's N-tile width (floats per lane) on calls whose automatic
+ *                    choice is between the two (small grids, no split-K)
+ *   SDNN_TMEM_SPLIT_K 0 = never split the TMEM plan's K range
  * (and, at build time, -DSDNN_DIAG=1|2: TMEM consumer without tcgen05.ld / without FFMA2). */
 
 #ifdef __cplusplus

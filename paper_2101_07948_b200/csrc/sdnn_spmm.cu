@@ -1387,6 +1387,13 @@ static int row_tile_v(const Plan& pl, int64_t N) {
 // N = 128: 44 → 26 µs; with 16-warp CTAs a 1.7-wave V = 2 grid lost: 4096², N = 256, 91 → 121 µs).
 static int row_tile_v_small(const Plan& pl, int64_t N, int sms) {
   const int v = row_tile_v(pl, N);
+  static const int env = [] {  // SDNN_ROW_V=2|4: force the small-N tile choice (experiments)
+    const char* e = getenv("SDNN_ROW_V");
+    return e ? atoi(e) : 0;
+  }();
+  if (pl.kernel == 1 && v == 4 && (env == 2 || env == 4)) return env;
+  // one 64-column tile: wider tiles would leave lanes idle (r01_row_v.log: 4096², N = 64, 127 → 98 µs)
+  if (pl.kernel == 1 && N <= 64) return 2;
   if (pl.kernel != 1 || v != 4) return v;
   const int64_t g4 = int64_t(pl.num_row_blocks) * ((N + 127) / 128);
   return (2 * g4 <= sms || (g4 < sms && pl.cta_panels <= 8)) ? 2 : 4;
@@ -1409,7 +1416,9 @@ static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const Y
     return e ? atoi(e) : 0;
   }();
   if (env > 0) return std::max(1, std::min(env, pl.num_chunks));
-  const int64_t tn = 32 * row_tile_v_small(pl, N, h->sms);
+  // counted on the V = 4 tile (N > 64) that launch_main then takes for split calls: K slices fill
+  // the GPU better than V = 2's extra CTAs (r01_row_v.log: 768×3072, N = 256: 54 → 45 µs)
+  const int64_t tn = N <= 64 ? 64 : 32 * row_tile_v(pl, N);
   const int64_t ctas = int64_t(pl.num_row_blocks) * ((N + tn - 1) / tn);
   const int64_t warps = ctas * (pl.cta_panels + 1);
   if (warps > 8 * int64_t(h->sms) || pl.num_chunks < 32) return 1;  // only clearly under-filled GPUs
@@ -1559,6 +1568,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
   int V = row_tile_v_small(pl, N, h->sms);
+  if (KS > 1 && pl.kernel == 1 && N > 64 && row_tile_v(pl, N) == 4) V = 4;  // split-K calls: see splitk_for
   if (pl.kernel == 4 || pl.kernel == 5) V = 4;  // TMEM plan, ragged / unaligned call: generic kernel
   const int TN = 32 * V;
   const int64_t ntiles = (N + TN - 1) / TN;
