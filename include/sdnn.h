@@ -296,6 +296,7 @@ SDNN_API int32_t sdnn_abi_version(void);
  *   SDNN_ROW_V       2 | 4: row kernel's N-tile width (floats per lane) on calls whose automatic
  *                    choice is between the two (small grids, no split-K)
  *   SDNN_TMEM_SPLIT_K 0 = never split the TMEM plan's K range
+ *   SDNN_CONV_PX, SDNN_CONV_KS  sdnn_conv2d: force 2 | 4 output pixels per lane / this many K slices
  * (and, at build time, -DSDNN_DIAG=1|2: TMEM consumer without tcgen05.ld / without FFMA2). */
 
 #ifdef __cplusplus

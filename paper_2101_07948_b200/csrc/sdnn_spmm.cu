@@ -2008,6 +2008,13 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
   if (B < 0 || IC < 1 || H < 1 || W < 1 || FY < 1 || FX < 1 || pad < 0 || stride < 1)
     return fail(SDNN_ERR_INVALID_ARGUMENT, "need B >= 0, IC, H, W, FY, FX, stride >= 1 and pad >= 0");
   if (act != SDNN_ACT_NONE && act != SDNN_ACT_RELU) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown act");
+  static const std::pair<int, int> conv_force = [] {  // SDNN_CONV_PX / SDNN_CONV_KS (experiments)
+    const char* a = getenv("SDNN_CONV_PX");
+    const char* b = getenv("SDNN_CONV_KS");
+    return std::make_pair(a ? atoi(a) : 0, b ? atoi(b) : 0);
+  }();
+  if (px_force <= 0 && (conv_force.first == 2 || conv_force.first == 4)) px_force = conv_force.first;
+  if (ks_force <= 0 && conv_force.second > 0) ks_force = conv_force.second;
   const Plan& pl = h->plan;
   if (int64_t(IC) * FY * FX != pl.K)
     return fail(SDNN_ERR_INVALID_ARGUMENT, "handle K = " + std::to_string(pl.K) + " != IC·FY·FX");
@@ -2086,13 +2093,18 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
       // split-K as for the row kernel: small images leave the GPU under-filled (few pixel tiles)
       const int64_t warps = nb2 * wc;
       int KS = 1;
-      // (a conv chunk stages a whole input patch, so for shallow K (< 16 chunks) slices of ≥ 2 chunks
-      // already pay on a tiny grid: 64 channels at 7×7, 25 → 11 µs, profiles/r01_conv_split.log)
-      const int64_t per = pl.num_chunks >= 16 ? 4 : 2;
+      // (a conv chunk stages a whole input patch, so slices of ≥ 2 chunks already pay on a tiny grid:
+      // 64 channels at 7×7, 25 → 11 µs, profiles/r01_conv_split.log), up to ~32 warps per SM, a power
+      // of two; a 4-chunk K range only on grids under 8 warps per SM (graph-timed conv suite,
+      // r01_conv_bench_rules.jsonl: 32 channels at 56 px 24 → 19 µs unsplit; 128 channels at 7 px
+      // 19 → 15 µs with 8 slices instead of 4)
       if (ks_force > 0)
         KS = std::min(ks_force, pl.num_chunks);
-      else if (!pl.no_split_k && warps <= 12 * int64_t(h->sms) && pl.num_chunks >= 4)  // ~24 warps/SM target
-        KS = int(std::max<int64_t>(1, std::min<int64_t>({8, pl.num_chunks / per, 24 * int64_t(h->sms) / warps})));
+      else if (!pl.no_split_k && warps <= 12 * int64_t(h->sms) &&
+               (pl.num_chunks >= 8 || (pl.num_chunks >= 4 && warps <= 8 * int64_t(h->sms)))) {
+        const int64_t ks = std::min<int64_t>({8, pl.num_chunks / 2, 32 * int64_t(h->sms) / warps});
+        KS = ks >= 8 ? 8 : ks >= 4 ? 4 : ks >= 2 ? 2 : 1;
+      }
       cudaStream_t st_ = static_cast<cudaStream_t>(stream);
       float* kws = nullptr;
       if (KS > 1) SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws),
