@@ -1470,7 +1470,11 @@ static sdnn_handle_s* narrow_pick(const sdnn_handle_s* h, int64_t N) {
   if (!narrow_worth(h, N)) return nullptr;
   if (h->narrow4) {
     const int64_t g = int64_t(h->narrow4->plan.num_row_blocks) * ((N + 127) / 128);
-    if (g > h->sms && g <= 3 * int64_t(h->sms)) return h->narrow4;
+    // at N ≤ 64 (V = 2 tiles, little work per CTA) only where split-K still applies to it (≤ 8 warps
+    // per SM); else the ≥ 64-block plan with split-K (graph-timed A/B, r01_ab_rules.log: 4096² 90 %,
+    // N = 64: 58 → 43 µs; 3072², 192 blocks: narrow4 31 µs against 34)
+    const int64_t warps = g * (h->narrow4->plan.cta_panels + 1);
+    if (g > h->sms && g <= 3 * int64_t(h->sms) && (N > 64 || warps <= 8 * int64_t(h->sms))) return h->narrow4;
   }
   return h->narrow;
 }

@@ -19,6 +19,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("SDNN_PKG_DIR"):  # A/B runs: another build of the package
+    sys.path.insert(0, os.environ["SDNN_PKG_DIR"])
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -57,6 +59,7 @@ def main():
     ap.add_argument("--ns", default="128,512,2048")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
+    ap.add_argument("--sdnn-only", action="store_true", help="skip the library baselines (A/B of builds)")
     a = ap.parse_args()
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
@@ -86,6 +89,10 @@ def main():
                 def dense():
                     torch.clamp_min(torch.addmm(b[:, None], Wd, X), 0.0, out=Ys)
 
+                if a.sdnn_only:
+                    print(json.dumps({"M": p.M, "sparsity": sp, "N": N, "kernel": kid, "sdnn_us": round(t_sdnn, 2),
+                                      "lib": sdnn.LIB_PATH}), flush=True)
+                    continue
                 try:
                     t_cusp = graph_time(cusp, a.reps)
                 except Exception as e:  # capture of the sparse op not supported: eager timing
