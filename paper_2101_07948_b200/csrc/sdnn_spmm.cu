@@ -1421,7 +1421,14 @@ static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const Y
   const int64_t tn = N <= 64 ? 64 : 32 * row_tile_v(pl, N);
   const int64_t ctas = int64_t(pl.num_row_blocks) * ((N + tn - 1) / tn);
   const int64_t warps = ctas * (pl.cta_panels + 1);
-  if (warps > 8 * int64_t(h->sms) || pl.num_chunks < 32) return 1;  // only clearly under-filled GPUs
+  if (warps > 8 * int64_t(h->sms) || pl.num_chunks < 8) return 1;  // only clearly under-filled GPUs
+  if (pl.num_chunks < 32) {
+    // short K ranges (8-31 chunks): slices of ≥ 2 chunks, a power of two — the serial chunk chain
+    // of a small call is its latency (graph-timed, profiles/r01_split_k_small.log: 1024², N = 128,
+    // 23 → 15 µs; 512² 90 %, N = 64, 9.7 → 6.9 µs; no gain at 4 chunks, 256²)
+    const int64_t ks = std::min<int64_t>({8, pl.num_chunks / 2, 16 * int64_t(h->sms) / warps});
+    return ks >= 8 ? 8 : ks >= 4 ? 4 : ks >= 2 ? 2 : 1;
+  }
   const int64_t ks = std::min<int64_t>({8, pl.num_chunks / 4, 16 * int64_t(h->sms) / warps});
   return ks >= 2 ? int(ks) : 1;
 }

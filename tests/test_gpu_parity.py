@@ -267,8 +267,8 @@ def test_auto_takes_tmem_plan_when_it_fills_a_wave(sdnn):
     Ya, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
     Yr, _ = run_gpu(sdnn, p, X, p.bias, 1, kernel="row")
     np.testing.assert_array_equal(Ya, Yr)
-    Xs = np.ascontiguousarray(X[:, :100])  # ragged: the row plan
-    Ya, _ = run_gpu(sdnn, p, Xs, p.bias, 1, handle=h)
+    Xs = np.ascontiguousarray(X[:, :100])  # ragged: the row plan (split-K off: the bitwise order)
+    Ya, _ = run_gpu(sdnn, p, Xs, p.bias, 1, handle=sdnn.Handle.from_problem(p, split_k=False))
     np.testing.assert_array_equal(Ya, Yr[:, :100])
     assert h.kernel_for(p.N) == 4 and h.kernel_for(102) == -1 and h.kernel_for(128) == 1  # 35·1·2 < 148
 
