@@ -223,11 +223,15 @@ class Handle:
     def for_conv(cls, row_ptr, col_idx, vals, OC: int, IC: int, FY: int, FX: int, **opts):
         """A handle for sdnn_conv2d: filters as the OC × (IC·FY·FX) CSR, no split rows, and K chunks of
         whole input channels when a multiple of FY·FX fits the chunk rules (72 for 3×3: 8-12 % faster,
-        profiles/r01_conv_kchunk.log)."""
+        profiles/r01_conv_kchunk.log), and 8 panels per CTA from 64 output channels up: taller CTAs
+        stage each input patch for more filters (graph-timed, profiles/r01_conv_cta.log: 256 channels
+        at 56 px 483 → 393 µs, 128 at 14 px 21 → 19 µs; 64 at 28 px 3 % slower)."""
         import math
         fyx = FY * FX
         kc = fyx * 8 // math.gcd(fyx, 8)  # lcm(FY·FX, 8)
         opts.setdefault("k_chunk", kc if kc <= 128 and IC * fyx >= 2 * kc else 0)
+        if OC >= 64 and not opts.get("panel_rows") and not opts.get("cta_panels"):
+            opts["cta_panels"] = 8
         opts.setdefault("split_rows", False)
         return cls(row_ptr, col_idx, vals, OC, IC * fyx, **opts)
 
