@@ -1461,7 +1461,10 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   // several TMEM tiles: the split CTAs must keep ≥ 3.5 MFLOP each, else the partial-sum round trip
   // and the per-CTA fill start-up lose to the row plans (r01_tune_grid.log: 1024² at 80-95 % and
   // 2048² at 95 %, N = 1024: 35-70 µs against 21-63 µs; c2 768×3072, N = 1024, 3.7 MFLOP, still wins)
-  if (N >= 2 * TN && ap.nnz * N * 4 < int64_t(7000000) * grid * ks) return 0;
+  // — unless the K range is long (≥ 32 chunks) and cut at least 4 ways, where the split is what
+  // fills the GPU (r01_tune_shapes_rules.log: 512×4096 at 95 %, N = 1024 / 2048, 1.5 MFLOP per CTA:
+  // 54 → 43 µs, 92 → 68 µs)
+  if (N >= 2 * TN && ap.nnz * N * 4 < int64_t(7000000) * grid * ks && !(ap.num_chunks >= 32 && ks >= 4)) return 0;
   return ks >= 2 ? int(ks) : 0;
 }
 static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
