@@ -12,6 +12,12 @@ X per rank ≥ 512 MiB > 126 MB L2, so every step streams X from HBM (no flush n
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+`python bench.py --gpus N` (N > 1) without an outer launcher (WORLD_SIZE unset) re-executes itself
+under `torch.distributed.run` with N ranks on this node (127.0.0.1, NCCL_DEBUG=INFO by default so
+the communicators' nRanks lines print); `--dry-run` does the same on the CPU (gloo, no CUDA: each
+rank runs the oracle on its column shard of c1) to exercise the launcher, sharding and
+max-over-ranks reduction without a GPU.
 """
 from __future__ import annotations
 
@@ -54,11 +60,11 @@ def max_over_ranks(x: float, dist=None) -> float:
     return float(t.item())
 
 
-def plan_hash(info: dict, perm: np.ndarray) -> str:
-    h = hashlib.sha256()
-    h.update(json.dumps({k: v for k, v in sorted(info.items()) if k != "device"}).encode())
-    h.update(np.ascontiguousarray(perm).tobytes())
-    return h.hexdigest()[:16]
+def plan_hash(blob: bytes) -> str:
+    """Hash of a prepared handle's packed arrays: sdnn_serialize writes every plan of the handle (row,
+    TMEM, narrow) — meta, blk_off, row_orig, the split tables and the geometry — so equal hashes on
+    every rank prove identical preparation."""
+    return hashlib.sha256(blob).hexdigest()[:16]
 
 
 def check_same_across_ranks(s: str, dist=None) -> bool:
@@ -150,6 +156,16 @@ def fill_x(p, c0: int, c1: int, out: np.ndarray, threads: int = 16):
         list(ex.map(one, blocks))
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -181,6 +197,101 @@ def oracle_sample(p, target_s: float = 12.0, max_cols: int = 16384, threads: int
     gflops = 2.0 * p.nnz * cols * reps / dt / 1e9
     return gflops, used, (f"{WORKLOAD} W (all {p.nnz} nonzeros) on X[:, 0:{cols}] ({cols} of {p.N} columns)"
                           f" x {reps}"), dt
+
+
+def tmem_operand_bytes(p, N: int, kc: int = 64) -> int:
+    """TMEM → register bytes one launch of the TMEM kernel reads: every (row, K chunk) segment is
+    padded to whole pairs of entries, and each entry is one 512-byte tcgen05.ld.32x32b.x4 per
+    128-column N tile (4 bytes per entry per column of N)."""
+    rows = np.repeat(np.arange(p.M), np.diff(p.row_ptr))
+    cnt = np.bincount(rows * ((p.K + kc - 1) // kc) + p.col_idx // kc, minlength=p.M * ((p.K + kc - 1) // kc))
+    padded = int(((cnt + 1) // 2 * 2).sum())
+    return padded * 4 * N
+
+
+def bench_configs(sdnn, torch, dev, fp32_peak_tf: float, hbm_peak_gbs: float, with_parity: bool):
+    """BASELINE configs[0..3] (c1-c4) through the auto kernel choice, each timed as a CUDA graph of 20
+    back-to-back launches (per launch; L2-warm, launch overhead amortised — SURVEY §8(d) "warm"),
+    with the oracle's full-Y parity (max |Y − Y_oracle| / S) when `with_parity`."""
+    out = {}
+    for key in [k for k in synth.CONFIGS if k != WORKLOAD]:
+        p = synth.config_problem(key)
+        Xn = p.x()
+        X = torch.from_numpy(Xn).to(dev)
+        b = torch.from_numpy(p.bias).to(dev)
+        Y = torch.empty((p.M, p.N), dtype=torch.float32, device=dev)
+        h = sdnn.Handle.from_problem(p)
+        kid = h.kernel_for(p.N, X.data_ptr(), Y.data_ptr())
+        for _ in range(3):
+            h.spmm(X, b, act=1, out=Y)
+        torch.cuda.synchronize()
+        s_ = torch.cuda.Stream(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s_):
+            for _ in range(20):
+                h.spmm(X, b, act=1, out=Y)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(3):
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / 20)
+        us = statistics.median(ts)
+        del g
+        flops = 2.0 * p.nnz * p.N
+        alg_bytes = p.nnz * 8 + (p.K + p.M) * p.N * 4
+        t_roof = max(flops / (fp32_peak_tf * 1e12), alg_bytes / (hbm_peak_gbs * 1e9))
+        d = {"M": p.M, "K": p.K, "N": p.N, "nnz": p.nnz, "kernel": kid, "us": round(us, 2),
+             "gflops": round(flops / us / 1e3, 1), "roof_frac": round(t_roof / (us * 1e-6), 4),
+             "bound": "alu" if flops / (fp32_peak_tf * 1e12) >= alg_bytes / (hbm_peak_gbs * 1e9) else "hbm"}
+        if with_parity:
+            import oracle
+            Yo, S, _ = oracle.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, Xn, p.bias, act=1, want_scale=True)
+            Yg = Y.cpu().numpy().astype(np.float64)
+            err = np.abs(Yg - Yo) / np.where(S > 0, S, 1.0)
+            d["parity_max_err_over_scale"] = float(err.max())
+            d["parity_ok"] = bool(err.max() <= 1e-4 and np.all(Yg[S == 0] == Yo[S == 0]))
+        out[key] = d
+        h.close()
+        del X, Y, b
+    return out
+
+
+def shard_proxy(h, X, bias, Y, torch, dev, stream, steps: int = 5):
+    """Single-GPU proxy of per-rank efficiency (labelled as a proxy: one GPU, ranks run one after
+    another): the c5 shard geometries of g = 2, 4, 8 (N/g contiguous columns, the shard a rank owns)
+    timed on this GPU, and the shard's Y compared bitwise with the g = 1 call's columns."""
+    N = X.shape[1]
+    full = None
+    res = {}
+    for g in (1, 2, 4, 8):
+        n = N // g
+        Xs = X[:, :n].contiguous() if g > 1 else X
+        Ys = torch.empty((Y.shape[0], n), dtype=torch.float32, device=dev) if g > 1 else Y
+        for _ in range(2):
+            h.spmm(Xs, bias, act=1, out=Ys)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            h.spmm(Xs, bias, act=1, out=Ys)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if g == 1:
+            full = ms
+            res["g1_ms"] = round(ms, 3)
+        else:
+            res[f"g{g}"] = {"n_per_rank": n, "ms": round(ms, 3), "efficiency_proxy": round(full / (g * ms), 4),
+                            "bitwise_equal_to_g1_columns": bool(torch.equal(Ys, Y[:, :n]))}
+            del Xs, Ys
+    res["note"] = ("single-GPU proxy: shard geometries timed sequentially on one B200; not a multi-GPU "
+                   "measurement")
+    return res
 
 
 # ----------------------------------------------------------------------------- reference arm (oracle)
@@ -230,7 +341,8 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
     h = sdnn.Handle.from_problem(p, kernel=args.kernel, group_sb=args.group_sb)
     prep_ms = 1e3 * (time.perf_counter() - t0)
     info = h.info()
-    same = check_same_across_ranks(plan_hash(info, h.permutation()), dist)
+    phash = plan_hash(h.serialize())
+    same = check_same_across_ranks(phash, dist)
 
     # ---- inputs: rank's X shard generated on host (pinned), copied to HBM once
     Xh = torch.empty((p.K, Nr), dtype=torch.float32, pin_memory=True)
@@ -242,7 +354,8 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
     kid = h.kernel_for(Nr, X.data_ptr(), Y.data_ptr())
     kernel_desc = {1: f"spmm_tma_kernel<row,R_w={info['panel_rows']}>", 2: "spmm_tma_kernel<group>",
                    3: f"sdnn_cg_p<0..{info['num_panels'] - 1}> (generated PTX)",
-                   4: "spmm_tmem_kernel<V=4,FILL=1> (X tile in TMEM, tcgen05.ld operands; 24 consumer warps x 10 rows)",
+                   4: "spmm_tmemr_kernel (X tile in TMEM, replicated lane quarters, TN=128; tcgen05.ld operands; "
+                      "24 consumer warps x 10 rows)",
                    5: "spmm_tmem_kernel<V=8,FILL=1> (X tile in TMEM, tcgen05.ld operands; 24 consumer warps x 5 rows)"
                    }.get(abs(kid), str(kid)) + (" [generic fallback]" if kid < 0 else "")
 
@@ -281,6 +394,11 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
         Yo, S, _ = oracle.spmm_omp(p.row_ptr, p.col_idx, p.vals, p.M, p.K, Xs, p.bias, act=1, want_scale=True)
         err = np.abs(Ys.astype(np.float64) - Yo) / np.where(S > 0, S, 1.0)
         parity = max_over_ranks(float(err.max()), dist)
+
+    # ---- per-rank efficiency proxy at the g = 2/4/8 shard sizes (one GPU, N = 1 runs only)
+    proxy = None
+    if world == 1 and not args.no_proxy and args.scaling == "strong":
+        proxy = shard_proxy(h, X, bias, Y, torch, dev, stream)
 
     # ---- optional Y all-gather, reported separately from the SpMM step:
     # nccl = all_gather_into_tensor of the shards after the step (collective alone);
@@ -344,7 +462,12 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
     for _ in range(e2e_steps):
         h.spmm_host_ptr(Xh.data_ptr(), Nr, p.bias.ctypes.data, 1, Yh.data_ptr())
     e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t0) / e2e_steps, dist)
-    e2e_ok = bool(torch.equal(Yh[:, :8].to(dev), Y[:, :8]))
+    # the host path tiles N in 4096-column blocks: compare the first and last column of every block
+    # (and the call's last column) with the device-buffer result, bitwise
+    edge = sorted(set([c for b0 in range(0, Nr, 4096) for c in (b0, min(b0 + 4095, Nr - 1))] + [Nr - 1]))
+    et = torch.tensor(edge, dtype=torch.long)
+    e2e_ok = bool(torch.equal(Yh[:, et].to(dev), Y[:, et.to(dev)]))
+    e2e_cols_checked = len(edge)
 
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only
     cpu = None
@@ -352,22 +475,37 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
         g, cores, sample, dt = oracle_sample(p, target_s=args.cpu_s)
         g1, _, sample1, _ = oracle_sample(p, target_s=min(4.0, args.cpu_s), threads=1)
         cpu = {"value": round(g, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
-               "seconds": round(dt, 2), "one_thread": {"value": round(g1, 3), "sample": sample1}}
+               "seconds": round(dt, 2), "cpu_model": cpu_model(),
+               "one_thread": {"value": round(g1, 3), "sample": sample1}}
 
     if rank != 0:
         return 0
+    peaks = measured_peaks()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_mhz_max = float(peaks.get("sm_max_mhz") or (clk.sm_max or 1965))
+    fp32_peak_tf = nsm * 128 * 2 * sm_mhz_max * 1e6 / 1e12
+    hbm_peak = float(peaks.get("hbm_gbs") or 6650.0)
+    # ---- BASELINE configs[0..3] (c1-c4), after the headline timing (rank 0)
+    cfgs = None
+    if not args.no_configs:
+        cfgs = bench_configs(sdnn, torch, dev, fp32_peak_tf, hbm_peak, with_parity=not args.no_parity)
     N_job = Nr * world if args.scaling == "weak" else args.n_total
     flops_job = 2.0 * p.nnz * N_job
     value = flops_job / (ms * 1e-3) / 1e9
     flops_launch = 2.0 * p.nnz * Nr
     achieved_tf = flops_launch / (ms_rank * 1e-3) / 1e12
-    peaks = measured_peaks()
-    sm_mhz_max = float(peaks.get("sm_max_mhz") or (clk.sm_max or 1965))
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak_tf = nsm * 128 * 2 * sm_mhz_max * 1e6 / 1e12
     alg_bytes = p.nnz * 8 + (p.K + p.M) * Nr * 4
     hbm_gbs = alg_bytes / (ms_rank * 1e-3) / 1e9
-    hbm_peak = float(peaks.get("hbm_gbs") or 6650.0)
+    # design ceiling of the TMEM kernel: its operand path, tcgen05.ld.32x32b.x4 at 201.7 B/clk/SM
+    # (24 warps, profiles/r01_tmem_bw.log) over the padded entries it loads
+    design = None
+    if abs(kid) == 4:
+        tb = tmem_operand_bytes(p, Nr)
+        t_design = tb / (201.7 * nsm * sm_mhz_max * 1e6)
+        design = {"path": "TMEM tcgen05.ld.32x32b.x4 at 201.7 B/clk/SM (measured, profiles/r01_tmem_bw.log)",
+                  "tmem_bytes_per_launch": tb, "padded_entries_per_nnz": round(tb / (4 * Nr) / p.nnz, 4),
+                  "t_design_ms": round(1e3 * t_design, 3), "frac_of_design_ceiling": round(1e3 * t_design / ms_rank, 4),
+                  "design_ceiling_frac_of_fp32_peak": round(flops_launch / t_design / 1e12 / fp32_peak_tf, 4)}
     trf = ncu_traffic(f"{WORKLOAD}_g{world}_{args.scaling}")
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -381,8 +519,10 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
                    "kernel": kernel_desc,
                    "group_entries_per_nnz": info["group_entries_per_nnz_x1000"] / 1000, "group_sb": info["group_sb"],
                    "panel_rows": info["panel_rows"], "cta_panels": info["cta_panels"], "k_chunk": info["k_chunk"],
-                   "permuted": bool(info["permuted"]), "prep_ms": round(prep_ms, 1), "plan_hash_identical": same},
+                   "permuted": bool(info["permuted"]), "prep_ms": round(prep_ms, 1), "plan_hash": phash,
+                   "plan_hash_identical": same},
         "roofline": {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(fp32_peak_tf, 2),
+                     "design_ceiling": design,
                      "unit": "TFLOP/s", "frac": round(achieved_tf / fp32_peak_tf, 4),
                      "traffic": None if trf is None else trf.get("dram_bytes_per_launch"),
                      "peak_source": f"fp32 FFMA: {nsm} SMs x 128 lanes x 2 flop x {sm_mhz_max:.0f} MHz "
@@ -396,13 +536,15 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
         "e2e": {"value": round(flops_job / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": int(p.K * Nr * 4 + p.M * 4), "d2h_bytes_per_step": int(p.M * Nr * 4),
                 "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps, "api": "sdnn_spmm_host (pinned host buffers)",
-                "matches_device_result": e2e_ok},
+                "matches_device_result": e2e_ok, "columns_checked": e2e_cols_checked},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
         "parity_max_err_over_scale": parity,
         "allgather_ms": None if ag_ms is None else round(ag_ms, 3),
         "fused_allgather_step_ms": None if fused_ms is None else round(fused_ms, 3),
         "fused_allgather_ok": fused_ok,
+        "shard_proxy": proxy,
+        "configs": cfgs,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -424,17 +566,24 @@ def main(argv=None):
     ap.add_argument("--cpu-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-configs", action="store_true", help="skip the c1-c4 per-config record")
+    ap.add_argument("--no-proxy", action="store_true", help="skip the g = 2/4/8 single-GPU shard proxy")
+    ap.add_argument("--dry-run", action="store_true", help="CPU only (gloo): launcher + sharding check")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "product":
+        return spawn_ranks(args.gpus, dry=args.dry_run)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, max(world, args.gpus) if rank == 0 else world)
+    if args.dry_run:
+        return run_dry(args, rank, world)
     dist = None
     if world > 1:
         import torch
@@ -445,6 +594,59 @@ def main(argv=None):
         return run_product(args, rank, world, local_rank, dist)
     finally:
         if dist is not None and dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def spawn_ranks(n: int, dry: bool = False) -> int:
+    """One process per GPU on this node: re-execute this script under torch.distributed.run with the
+    same arguments (rank 0 prints the JSON line; the others print nothing)."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    if not dry:
+        env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nRanks) on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_dry(args, rank: int, world: int) -> int:
+    """CPU rehearsal of the multi-rank path (gloo): rank r owns columns shard_range(N, r, world) of
+    c1, computes them (the oracle stands in for the kernel), the step time is reduced with MAX over
+    ranks, and rank 0 checks that the gathered shards equal the unsharded result."""
+    import torch.distributed as dist
+    import oracle
+    if world > 1:
+        dist.init_process_group("gloo")
+    try:
+        p = synth.config_problem("c1")
+        X = p.x()
+        c0, c1 = shard_range(p.N, rank, world)
+        t0 = time.perf_counter()
+        Ys, _ = oracle.spmm(p.row_ptr, p.col_idx, p.vals, p.M, p.K, np.ascontiguousarray(X[:, c0:c1]), p.bias, act=1)
+        dt = max_over_ranks(time.perf_counter() - t0, dist if world > 1 else None)
+        parts = [None] * world
+        if world > 1:
+            dist.all_gather_object(parts, (c0, c1, Ys))
+        else:
+            parts = [(c0, c1, Ys)]
+        if rank != 0:
+            return 0
+        Yf, _ = oracle.spmm(p.row_ptr, p.col_idx, p.vals, p.M, p.K, X, p.bias, act=1)
+        cat = np.concatenate([y for _, _, y in sorted(parts, key=lambda t: t[0])], axis=1)
+        line = {"metric": METRIC, "dry_run": True, "value": round(2.0 * p.nnz * p.N / dt / 1e9, 4), "unit": "GFLOP/s",
+                "n_gpus": world, "steps": 1, "warmup": args.warmup, "ms_per_step": round(1e3 * dt, 3),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accumulate/f32-io",
+                "data": "synthetic (c1)", "config": {"workload": "c1 (dry run, CPU oracle per shard, gloo)",
+                                                     "shards": [[a, b] for a, b, _ in sorted(parts, key=lambda t: t[0])]},
+                "shards_equal_unsharded": bool(np.array_equal(cat, Yf))}
+        print(json.dumps(line), flush=True)
+        return 0
+    finally:
+        if world > 1 and dist.is_initialized():
             dist.destroy_process_group()
 
 

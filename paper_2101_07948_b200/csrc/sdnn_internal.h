@@ -87,12 +87,16 @@ constexpr int kCgMaxRows = 128;     // codegen kernel: accumulators (rows) per p
 constexpr int kCgWarps = 6;         // codegen kernel: warps per CTA (2 CTAs/SM at <= 168 registers)
 constexpr int kCgPrefetch = 24;     // codegen kernel: X columns in flight per lane
 
-// TMEM kernels (sdnn_spmm.cu): the X tile lives in tensor memory.  TMEM lane L holds V columns of
-// N (n0 + 4L + v and, for V = 8, n0 + 512 + 4L + v): N tile 128·V; TMEM column V·k_local + v; two
-// halves of 256 columns → K chunk 256 / V.  24 consumer warps = 6 warp slots per lane quarter, each
-// slot a panel of tmem_rows(V) rows (accumulators: rows · V registers per thread; 28 warps → 72
-// registers).  Slots × rows measured on c5 (profiles/r01_tmem_fill_diag.log): 4×16 53.3 ms, 5×12
-// 53.3, 6×10 51.1, 6×11 65.6 (spills), 7×8 56.9.
+// TMEM kernels (sdnn_spmm.cu): the X tile lives in tensor memory.
+//   kernel 4 ("tmem", V = 4, replicated lane quarters): every TMEM lane quarter holds the same 128
+//     columns of N (lane 32q + l ↔ n0 + 4l .. 4l+3; TMEM column 4·k_local + v + 256·half), and the 24
+//     consumer warps each own their own tmem_rows(4) = 10-row panel (240 rows per CTA), so the X
+//     tile staged once serves 4× the rows of a non-replicated layout (a quarter of the L2 → SM fill
+//     traffic) and the TMEM lane base of warp w's quarter (w % 4) is packed into its metadata.
+//     Row segments are padded to whole pairs (tmem_pad(4) = 2).
+//   kernel 5 ("tmem8", V = 8): lane L ↔ columns n0 + 4L + v and n0 + 512 + 4L + v (N tile 1024),
+//     6 warp slots × 5 rows shared by the 4 quarters (30 rows per CTA), segments padded to pairs.
+// K chunk = one TMEM half of 256 columns (256 / V K rows), double-buffered.
 #ifdef __CUDACC__
 #define SDNN_HD __host__ __device__
 #else
@@ -100,10 +104,13 @@ constexpr int kCgPrefetch = 24;     // codegen kernel: X columns in flight per l
 #endif
 SDNN_HD constexpr int tmem_rows(int V) { return V == 4 ? 10 : 5; }
 SDNN_HD constexpr int tmem_kc(int V) { return 256 / V; }
-SDNN_HD constexpr int tmem_pad(int V) { return V == 4 ? 4 : 2; }  // row segments padded to multiples of this
-constexpr int kTmemPanels = 6;
-constexpr int kTmemPieces = 4;  // smem ring depth (32 KB TMA pieces)
+SDNN_HD constexpr int tmem_pad(int V) { return 2; }  // row segments padded to whole pairs
+constexpr int kTmemPanels = 6;        // kernel 5: warp slots per lane quarter
+constexpr int kTmemRWarps = 24;       // kernel 4: consumer warps (= panels per row block)
+constexpr int kTmemPieces = 4;        // kernel 5: smem ring depth (32 KB TMA pieces)
+constexpr int kTmemRPieces = 8;       // kernel 4: smem ring depth (8 KB TMA pieces: 16 K rows × 128 columns)
 inline int tmem_v(int kernel) { return kernel == 5 ? 8 : 4; }
+inline int tmem_tn(int kernel) { return kernel == 5 ? 1024 : 128; }  // N tile of a TMEM plan
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 

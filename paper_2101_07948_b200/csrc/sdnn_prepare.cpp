@@ -143,9 +143,11 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
       int64_t bytes = 0;
       if (g.kernel == 1) {
         // TMEM variant (g.tmem = V): the column field is the TMEM column offset of X[col] in the
-        // chunk's TMEM half (V·col_local + 256·(j mod 2)), and every row segment is padded to a
-        // multiple of tmem_pad(V) entries with zero weights (the count in the header includes the
-        // padding) so the kernel runs one unrolled loop body per row; the padding adds 0·X (X finite).
+        // chunk's TMEM half (V·col_local + 256·(j mod 2)) — for kernel 4 (g.wc = 24, replicated lane
+        // quarters) with the TMEM lane base of the slot's warp, (32·(warp mod 4)) << 16, added — and
+        // every row segment is padded to whole pairs of entries with zero weights (the count in the
+        // header includes the padding) so the kernel loads entries two at a time; the padding adds
+        // 0·X (X finite).
         // V = 4 also counts leading runs: while a row segment starts with aligned 1×4 runs (four
         // nonzeros at columns k..k+3, k % 4 == 0 — the blocks of a block-clustered mask), their
         // number goes into header bits 8..15 so the kernel fetches each run's four X row slices with
@@ -156,6 +158,8 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
         int32_t e = 0;
         for (int32_t s = 0; s < rcta; ++s) {
           const int32_t orow = row_orig[size_t(b) * rcta + s];
+          // kernel 4: TMEM lane base of the quarter of warp s / rw
+          const uint32_t lane_base = (g.tmem == 4 && g.wc == kTmemRWarps) ? uint32_t(32 * ((s / g.rw) & 3)) << 16 : 0u;
           int32_t c = 0, runs = 0;
           bool leading = true;
           auto put = [&](uint32_t cl, float w) {
@@ -173,18 +177,18 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
               const int32_t col = col_idx[p];
               if (stp == 1 && g.tmem == 4 && leading && col % 4 == 0 && p + 3 < end && col_idx[p + 3] == col + 3 &&
                   col + 3 < hi) {
-                for (int32_t t = 0; t < 4; ++t) put(uint32_t(col + t - lo) * 4u + half, vals[p + t]);
+                for (int32_t t = 0; t < 4; ++t) put((uint32_t(col + t - lo) * 4u + half) | lane_base, vals[p + t]);
                 p += 4;
                 ++runs;
                 continue;
               }
               leading = false;
-              put(g.tmem ? uint32_t(col - lo) * uint32_t(g.tmem) + half : uint32_t(col - lo), vals[p]);
+              put(g.tmem ? (uint32_t(col - lo) * uint32_t(g.tmem) + half) | lane_base : uint32_t(col - lo), vals[p]);
               p += stp;
             }
           }
           const int32_t cpad = g.tmem ? int32_t(align_up(c, tmem_pad(g.tmem))) : c;
-          while (c < cpad) put(half, 0.f);
+          while (c < cpad) put(half | lane_base, 0.f);
           if (blk) reinterpret_cast<uint32_t*>(blk)[s] = (uint32_t(e) << 16) | (uint32_t(runs) << 8) | uint32_t(cpad);
           e += int32_t(align_up(cpad, 2));
         }
@@ -362,12 +366,13 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     auto make_geo = [&](int32_t kernel, int32_t sb) {
       Geometry g{};
       if (kernel == 4 || kernel == 5) {
-        // TMEM kernels (sdnn_spmm.cu): row-kernel format, tmem_rows(V)-row warp panels, 4 panels
-        // per CTA row block (one per warp slot of a TMEM lane quarter), K chunk = one TMEM half.
+        // TMEM kernels (sdnn_spmm.cu): row-kernel format, tmem_rows(V)-row warp panels; kernel 4: 24
+        // panels per CTA row block (one per consumer warp, replicated lane quarters), kernel 5: 6
+        // (one per warp slot, shared by the 4 lane quarters); K chunk = one TMEM half.
         g.kernel = 1;
         g.tmem = tmem_v(kernel);
         g.rw = tmem_rows(g.tmem);
-        g.wc = kTmemPanels;
+        g.wc = kernel == 4 ? kTmemRWarps : kTmemPanels;
         g.nrb = (M + g.rw * g.wc - 1) / (g.rw * g.wc);
         return g;
       }
@@ -474,6 +479,8 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
         g.kc = c;
         g.nch = (K + c - 1) / c;
         emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries, &pcs);
+        if (g.tmem == 4)  // kernel 4: 8 KB TMA pieces × kTmemRPieces + two metadata slots
+          return int64_t(kTmemRPieces) * 8192 + 2 * align_up(max_of(sizes), 128) + 1024 <= kSmemBudget;
         const int32_t s = stages_for(c, max_of(sizes));
         if (s >= 3 || (s >= 2 && (o.k_chunk || c == 8))) return true;
       }
@@ -518,7 +525,15 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       for (Geometry c : cands) {
         std::vector<int32_t> r = row_orig_for(c, &pcs);
         EmitStats st;
-        if (!choose_kc(c, r, &st)) continue;
+        bool fits = choose_kc(c, r, &st);
+        // kernel 4 (240 rows per CTA): a dense matrix's metadata block can outgrow its shared-memory
+        // slot — spread the rows over more row blocks (fewer rows per warp) until it fits
+        while (!fits && c.tmem == 4 && int64_t(c.nrb) * c.wc < M) {
+          c.nrb = int32_t(std::min<int64_t>(int64_t(c.nrb) * 2, (M + c.wc - 1) / c.wc));
+          r = row_orig_for(c, &pcs);
+          fits = choose_kc(c, r, &st);
+        }
+        if (!fits) continue;
         const double cc = cost(c, st);
         if (!found || cc < best) { best = cc; g = c; ro.swap(r); stats = st; found = true; best_pcs = pcs; }
       }

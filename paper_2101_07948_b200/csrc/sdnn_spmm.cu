@@ -373,9 +373,9 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
 // column; blockIdx.y = split row.  split = {rows[ns], first piece[ns], piece count[ns]}.
 __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t* __restrict__ split, int32_t ns,
                                     const float* __restrict__ bias, int32_t act, const YOut yo, int64_t N) {
-  const int32_t sr = int32_t(blockIdx.y);
   const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (n >= N) return;
+  for (int32_t sr = int32_t(blockIdx.y); sr < ns; sr += int32_t(gridDim.y)) {  // gridDim.y ≤ 65535
   const int32_t row = split[sr], first = split[ns + sr], cnt = split[2 * ns + sr];
   float v = ws[int64_t(first) * N + n];
   for (int32_t k = 1; k < cnt; ++k) v += ws[int64_t(first + k) * N + n];
@@ -384,23 +384,25 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t*
 #pragma unroll
   for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
     if (d < yo.n) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+  }
 }
 
 // Split-K (row kernel): Y[row] = act(Σ_{s < KS} kws[s][row] (slice order) + b[row]).  One thread per
 // column; blockIdx.y = row.
 __global__ void splitk_reduce_kernel(const float* __restrict__ kws, int32_t KS, int32_t M, const float* __restrict__ bias,
                                      int32_t act, const YOut yo, int64_t N) {
-  const int32_t row = int32_t(blockIdx.y);
   const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (n >= N) return;
   const int64_t slice = int64_t(M) * N;
-  float v = kws[int64_t(row) * N + n];
-  for (int32_t s = 1; s < KS; ++s) v += kws[s * slice + int64_t(row) * N + n];
-  if (bias) v += bias[row];
-  if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
+  for (int32_t row = int32_t(blockIdx.y); row < M; row += int32_t(gridDim.y)) {  // gridDim.y ≤ 65535
+    float v = kws[int64_t(row) * N + n];
+    for (int32_t s = 1; s < KS; ++s) v += kws[s * slice + int64_t(row) * N + n];
+    if (bias) v += bias[row];
+    if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
 #pragma unroll
-  for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
-    if (d < yo.n) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+    for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
+      if (d < yo.n) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+  }
 }
 
 // Fast path: TMA producer warp + W_c consumer warps, mbarrier stage ring.
@@ -469,7 +471,8 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
 // Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
 // threads using bounds-checked loads (zero fill) and a block barrier instead of TMA/mbarriers.
 template <int KIND, int RW, int V, int SB = 0>
-__global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : 16 * 32, 1) spmm_generic_kernel(const KParamsY p) {
+__global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : KIND == 4 ? kTmemRWarps * 32 : 16 * 32, 1)
+    spmm_generic_kernel(const KParamsY p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1083,7 +1086,7 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
     };
     if (leader) {
       for (int i = 0; i < S && i < total; ++i) load_piece(i);
-      for (int j = 0; j < MS && j < p.nch; ++j) load_meta(j);
+      for (int j = 0; j < MS && j < jr.y; ++j) load_meta(j);  // this slice's chunks only
     }
     for (int j = 0; j < jr.y; ++j) {
       const int h = j & 1;
@@ -1197,6 +1200,233 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
 }
 
 // ------------------------------------------------------------------------------------------------
+// TMEM kernel, replicated lane quarters (kernel 4, the c5 bench kernel).
+//   * N tile TN = 128; every TMEM lane quarter holds the same tile: lane 32q + l ↔ columns
+//     n0 + 4l .. 4l+3, TMEM column 4·k + v (+ 256 for the odd K chunks) ↔ X[k0 + k].  Two halves of
+//     256 columns double-buffer K chunks of 64 rows.
+//   * filler warp q (one per quarter) copies every 8 KB TMA piece (16 K rows × 128 columns) from the
+//     shared-memory ring into its quarter (LDS.128 → tcgen05.st.32x32b.x16); filler 0 lane 0 issues
+//     the TMA pieces and the per-chunk metadata bulk copies.  Each X element staged from L2 serves
+//     240 rows (24 warps × 10), 4× the rows of a non-replicated 512-column tile — a quarter of the
+//     L2 → SM traffic for the same accumulator registers.
+//   * consumer warp w (quarter w % 4) owns a 10-row panel; its metadata already holds the TMEM
+//     address (lane base | column), so per pair of nonzeros: one LDS.128 (col, w, col, w), two R2UR,
+//     two tcgen05.ld.32x32b.x4, four FFMA2 — two pairs per step while ≥ 2 remain; rows are padded to
+//     whole pairs only (8 % padding on c5 against 23 % at steps of four).
+//   * leading aligned 1×4 runs (block-clustered masks, c4): one tcgen05.ld.x16 per run.
+// Every row accumulates in ascending column order with fp32 FMA: bitwise equal to the row kernel.
+// ------------------------------------------------------------------------------------------------
+constexpr int kTmemRConsumers = kTmemRWarps;  // 24 consumer warps
+constexpr int kTmemRPieceBytes = 16 * 128 * 4;  // 8 KB: 16 K rows × 128 columns
+constexpr int kTmemRMetaSlots = 2;
+constexpr size_t tmemr_smem_bytes(int m_stage_bytes) {
+  return size_t(kTmemRPieces) * kTmemRPieceBytes + size_t(kTmemRMetaSlots) * m_stage_bytes + 32 * 8 + 16;
+}
+
+template <bool MULTI, bool SPLIT>
+__device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& p, uint8_t* mring, uint64_t* mfull,
+                                              uint64_t* mempty, uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0,
+                                              int warp, int lane) {
+  constexpr int RW = tmem_rows(4);
+  constexpr int MS = kTmemRMetaSlots;
+  float2 acc[RW][2];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+  const int nrel = tmem_chunks<SPLIT>(p.nch).y;
+  for (int j = 0; j < nrel; ++j) {
+    const int h = j & 1, m = j % MS;
+    mbar_wait(&mfull[m], (j / MS) & 1);
+    mbar_wait(&tfull[h], (j >> 1) & 1);
+    tc_fence_after();
+    const uint8_t* ms = mring + size_t(m) * p.m_stage_bytes;
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + warp * RW;
+    const float4* ent = reinterpret_cast<const float4*>(ms + p.hdr_bytes);
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const uint32_t hh = hdr[r];
+      int n = int(hh & 0xffu);  // entries (a whole number of pairs)
+      const float4* e = ent + (hh >> 17);
+      for (int nrun = int((hh >> 8) & 0xffu); nrun > 0; --nrun, e += 2, n -= 4) {  // aligned 1×4 runs
+        const float4 e0 = e[0], e1 = e[1];
+        float4 xa, xb, xc, xd;
+        tmem_ld16(__float_as_uint(e0.x), xa, xb, xc, xd);
+        tmem_wait_ld(xa, xb, xc, xd);
+        fma4(acc[r], e0.y, xa);
+        fma4(acc[r], e0.w, xb);
+        fma4(acc[r], e1.y, xc);
+        fma4(acc[r], e1.w, xd);
+      }
+      for (; n >= 4; n -= 4, e += 2) {  // two pairs: four loads in flight
+        const float4 e0 = e[0], e1 = e[1];
+        float4 xa, xb, xc, xd;
+        tmem_ld4(__float_as_uint(e0.x), xa);
+        tmem_ld4(__float_as_uint(e0.z), xb);
+        tmem_ld4(__float_as_uint(e1.x), xc);
+        tmem_ld4(__float_as_uint(e1.z), xd);
+        tmem_wait_ld(xa, xb, xc, xd);
+        fma4(acc[r], e0.y, xa);
+        fma4(acc[r], e0.w, xb);
+        fma4(acc[r], e1.y, xc);
+        fma4(acc[r], e1.w, xd);
+      }
+      if (n) {  // one pair
+        const float4 e0 = e[0];
+        float4 xa, xb;
+        tmem_ld4(__float_as_uint(e0.x), xa);
+        tmem_ld4(__float_as_uint(e0.z), xb);
+        tmem_wait_ld(xa, xb);
+        fma4(acc[r], e0.y, xa);
+        fma4(acc[r], e0.w, xb);
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&tfree[h]);
+      mbar_arrive(&mempty[m]);
+    }
+  }
+  // epilogue: panel rb·24 + warp; lane columns n0 + 4·lane
+  const int64_t n = n0 + lane * 4;
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int32_t orow = p.row_orig[(rb * kTmemRConsumers + warp) * RW + r];
+    if (orow < 0) continue;
+    const float b = (p.bias && !SPLIT) ? p.bias[orow] : 0.f;
+    float v[4] = {acc[r][0].x + b, acc[r][0].y + b, acc[r][1].x + b, acc[r][1].y + b};
+    if (p.act == SDNN_ACT_RELU && !SPLIT) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) v[t] = v[t] > 0.f ? v[t] : 0.f;
+    }
+    if (n >= p.N) continue;
+    if constexpr (SPLIT) {  // split-K slice: raw partial sums (splitk_reduce_kernel adds bias, act)
+      __stcs(reinterpret_cast<float4*>(p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N + n),
+             make_float4(v[0], v[1], v[2], v[3]));
+    } else if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
+      for (int d = 0; d < p.yo.n; ++d)
+        __stcs(reinterpret_cast<float4*>(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n),
+               make_float4(v[0], v[1], v[2], v[3]));
+    } else {
+      __stcs(reinterpret_cast<float4*>(p.Y + int64_t(orow) * p.N + n), make_float4(v[0], v[1], v[2], v[3]));
+    }
+  }
+}
+
+template <bool MULTI = false, bool SPLIT = false>
+__global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
+    spmm_tmemr_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI || SPLIT> p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int PK = 16;          // K rows per TMA piece
+  constexpr int PPC = 64 / PK;    // pieces per K chunk
+  constexpr int S = kTmemRPieces, MS = kTmemRMetaSlots;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = blockIdx.x % p.nrb;
+  const int64_t n0 = int64_t(blockIdx.x / p.nrb) * 128;
+  uint8_t* xring = smem;
+  uint8_t* mring = smem + size_t(S) * kTmemRPieceBytes;
+  uint64_t* slot_full = reinterpret_cast<uint64_t*>(mring + size_t(MS) * p.m_stage_bytes);
+  uint64_t* slot_empty = slot_full + S;
+  uint64_t* tfull = slot_empty + S;  // [2]: K chunk resident in TMEM half h
+  uint64_t* tfree = tfull + 2;       // [2]: every consumer warp is done with TMEM half h
+  uint64_t* mfull = tfree + 2;       // [MS]
+  uint64_t* mempty = mfull + MS;     // [MS]
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(mempty + MS);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&slot_full[s], 1);
+      mbar_init(&slot_empty[s], 4);
+    }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&tfull[h], 4);
+      mbar_init(&tfree[h], kTmemRConsumers);
+    }
+    for (int m = 0; m < MS; ++m) {
+      mbar_init(&mfull[m], 1);
+      mbar_init(&mempty[m], kTmemRConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tbase_s;
+
+  if (warp >= kTmemRConsumers) {  // fillers: TMA → smem ring → LDS.128 → tcgen05.st → TMEM half
+    const int q = warp & 3;
+    const uint32_t tq = tbase + (uint32_t(q * 32) << 16);
+    const bool leader = warp == kTmemRConsumers && lane == 0;
+    const int2 jr = tmem_chunks<SPLIT>(p.nch);  // this CTA's chunks (all of them unless split-K)
+    const int64_t* off = p.blk_off + int64_t(rb) * p.nch + jr.x;
+    const int total = jr.y * PPC;
+    auto load_piece = [&](int i) {
+      const int s = i % S;
+      if (p.dbg & 1) {
+        mbar_arrive(&slot_full[s]);
+        return;
+      }
+      mbar_expect_tx(&slot_full[s], kTmemRPieceBytes);
+      tma_load_2d(xring + size_t(s) * kTmemRPieceBytes, &tmap, int32_t(n0), (jr.x * PPC + i) * PK, &slot_full[s]);
+    };
+    auto load_meta = [&](int j) {
+      const int m = j % MS;
+      const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
+      mbar_expect_tx(&mfull[m], mbytes);
+      bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[j], mbytes, &mfull[m]);
+    };
+    if (leader) {
+      for (int i = 0; i < S && i < total; ++i) load_piece(i);
+      for (int j = 0; j < MS && j < jr.y; ++j) load_meta(j);
+    }
+    for (int j = 0; j < jr.y; ++j) {
+      const int h = j & 1;
+      if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
+        mbar_wait(&tfree[h], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      if (leader && j >= MS) {
+        mbar_wait(&mempty[j % MS], ((j / MS) - 1) & 1);
+        load_meta(j);
+      }
+      for (int pc = 0; pc < PPC; ++pc) {
+        const int i = j * PPC + pc, s = i % S;
+        mbar_wait(&slot_full[s], (i / S) & 1);
+        if (!(p.dbg & 4)) {
+          const float4* src = reinterpret_cast<const float4*>(xring + size_t(s) * kTmemRPieceBytes) + lane;
+          float4 v[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) v[u][t] = src[(4 * u + t) * 32];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tmem_st16(tq + uint32_t(h * 256 + (pc * PK + 4 * u) * 4), v[u]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&slot_empty[s]);
+        if (leader && i + S < total) {
+          mbar_wait(&slot_empty[s], (i / S) & 1);
+          load_piece(i + S);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfull[h]);
+    }
+  } else {
+    if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0 (addresses are absolute)
+    tmemr_consume<MULTI, SPLIT>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+// ------------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------------
 #define SDNN_CUDA_TRY(call)                                                                            \
@@ -1280,10 +1510,17 @@ static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, c
 static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                const YOut& yo, cudaStream_t stream, int KS = 1, cudaMemPool_t pool = nullptr) {
   const Plan& pl = h->plan;
-  const int V = tmem_v(pl.kernel), TN = 128 * V;
+  const bool rep = pl.kernel == 4;  // replicated-quarter kernel (V = 4, TN = 128); else V = 8 (TN = 1024)
+  const int V = tmem_v(pl.kernel), TN = tmem_tn(pl.kernel);
   const int64_t ntiles = (N + TN - 1) / TN;
   const int64_t nblocks = ntiles * pl.num_row_blocks;
   if (nblocks > 0x7fffffffLL) return fail(SDNN_ERR_UNSUPPORTED, "N too large for one launch");
+  // split-K: slices are cut at even chunks (a chunk's TMEM half is packed into the metadata); every
+  // slice keeps at least two chunk pairs, else no split
+  if (KS > 1) {
+    KS = std::min(KS, ((pl.num_chunks + 1) / 2) / 2);
+    if (KS < 2) KS = 1;
+  }
   KParamsY p{};
   p.meta = h->d_meta;
   p.blk_off = h->d_blk_off;
@@ -1310,25 +1547,37 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   }
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  // 3-D view of X: {128 columns, N/128 column blocks, K rows}, so one box {128, V, 8192/TN} lands in
-  // shared memory as contiguous TN-column K rows (32 KB).
   CUtensorMap tmap;
-  const cuuint64_t dims[3] = {128, cuuint64_t(N / 128), cuuint64_t(pl.K)};
-  const cuuint64_t strides[2] = {512, cuuint64_t(N) * 4};
-  const cuuint32_t box[3] = {128, cuuint32_t(V), cuuint32_t(8192 / TN)};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(int(cr)));
-  const size_t smem = tmem_smem_bytes(p.m_stage_bytes);
+  CUresult cr;
+  if (rep) {
+    // 2-D view of X {N, K}: one box {128 columns, 16 K rows} = one 8 KB piece, rows contiguous
+    const cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(pl.K)};
+    const cuuint64_t strides[1] = {cuuint64_t(N) * 4};
+    const cuuint32_t box[2] = {128, 16};
+    const cuuint32_t estr[2] = {1, 1};
+    cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    // 3-D view of X: {128 columns, N/128 column blocks, K rows}, so one box {128, V, 8192/TN} lands in
+    // shared memory as contiguous TN-column K rows (32 KB).
+    const cuuint64_t dims[3] = {128, cuuint64_t(N / 128), cuuint64_t(pl.K)};
+    const cuuint64_t strides[2] = {512, cuuint64_t(N) * 4};
+    const cuuint32_t box[3] = {128, cuuint32_t(V), cuuint32_t(8192 / TN)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
+  const size_t smem = rep ? tmemr_smem_bytes(p.m_stage_bytes) : tmem_smem_bytes(p.m_stage_bytes);
   if (smem > size_t(kSmemBudget) + 1024) return fail(SDNN_ERR_INTERNAL, "TMEM kernel stage does not fit shared memory");
   static const int fill_env = [] {
     const char* e = getenv("SDNN_TMEM_FILL");
     return e ? atoi(e) : -1;
   }();
-  const int fill = fill_env >= 0 ? fill_env : pl.tmem_fill;
-  const unsigned threads = unsigned(kTmemConsumers + (fill ? 4 : 1)) * 32;
+  const int fill = rep ? 1 : (fill_env >= 0 ? fill_env : pl.tmem_fill);
+  const unsigned threads = rep ? unsigned(kTmemRConsumers + 4) * 32 : unsigned(kTmemConsumers + (fill ? 4 : 1)) * 32;
   const unsigned grid = unsigned(nblocks);
   const bool multi = !(yo.n == 1 && yo.ld == N && yo.col0 == 0);
   if (multi && fill != 1) return fail(SDNN_ERR_UNSUPPORTED, "multi-destination TMEM launch needs the filler-warp fill");
@@ -1341,11 +1590,11 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     q.kws = kws;
     q.M = pl.M;
     const dim3 g2{grid, unsigned(KS)};
-    if (V == 8) spmm_tmem_kernel<8, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
-    else spmm_tmem_kernel<4, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
+    if (rep) spmm_tmemr_kernel<false, true><<<g2, threads, smem, stream>>>(tmap, q);
+    else spmm_tmem_kernel<8, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
     cudaError_t le = cudaGetLastError();
     if (le == cudaSuccess) {
-      splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(pl.M)), 256, 0, stream>>>(kws, KS, pl.M, bias, act,
+      splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, stream>>>(kws, KS, pl.M, bias, act,
                                                                                                  yo, N);
       le = cudaGetLastError();
     }
@@ -1353,14 +1602,12 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     if (le != cudaSuccess) return fail(SDNN_ERR_CUDA, std::string("TMEM split-K: ") + cudaGetErrorString(le));
     return SDNN_OK;
   }
-  if (V == 8 && multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (V == 8 && fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (V == 8 && fill == 1) spmm_tmem_kernel<8, 1><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (V == 8) spmm_tmem_kernel<8, 0><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (multi) spmm_tmem_kernel<4, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (fill == 2) spmm_tmem_kernel<4, 2><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (fill == 1) spmm_tmem_kernel<4, 1><<<grid, threads, smem, stream>>>(tmap, p);
-  else spmm_tmem_kernel<4, 0><<<grid, threads, smem, stream>>>(tmap, p);
+  if (rep && multi) spmm_tmemr_kernel<true, false><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (rep) spmm_tmemr_kernel<false, false><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
+  else if (multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (fill == 1) spmm_tmem_kernel<8, 1><<<grid, threads, smem, stream>>>(tmap, p);
+  else spmm_tmem_kernel<8, 0><<<grid, threads, smem, stream>>>(tmap, p);
   SDNN_CUDA_TRY(cudaGetLastError());
   return SDNN_OK;
 }
@@ -1370,8 +1617,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
 // c3 512² — while the row kernel, several CTAs per SM, wins on c3 256×128 (65 TMEM CTAs) and below).
 static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const YOut& yo) {
   return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo) &&
-         2 * int64_t(a->plan.num_row_blocks) * ((N + 128 * tmem_v(a->plan.kernel) - 1) / (128 * tmem_v(a->plan.kernel))) >=
-             a->sms;
+         2 * int64_t(a->plan.num_row_blocks) * ((N + tmem_tn(a->plan.kernel) - 1) / tmem_tn(a->plan.kernel)) >= a->sms;
 }
 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
@@ -1447,7 +1693,7 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
     return e ? atoi(e) : -1;
   }();
   if (env == 0) return 0;
-  const int64_t TN = 128 * tmem_v(a->plan.kernel);
+  const int64_t TN = tmem_tn(a->plan.kernel);
   const int64_t grid = int64_t(a->plan.num_row_blocks) * ((N + TN - 1) / TN);
   // a partial TMEM tile wastes lanes; at a single TMEM tile (N < 2·TN) only long K (≥ 48 chunks)
   // beat the row / narrow plans (profiles/r01_tune_shapes*.log: 2048², 1024² at N = 512 lost;
@@ -1504,7 +1750,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   }
   // split-K (row kernel, small grids): KS CTAs per (row block, N tile), each over a K-chunk range,
   // raw partial sums to a stream-ordered workspace, summed in slice order by splitk_reduce_kernel
-  const int KS = ns > 0 ? 1 : (ks_force > 0 ? std::min(ks_force, pl.num_chunks) : splitk_for(h, N, X, yo));
+  const int KS = ns > 0 || pl.no_split_k ? 1 : (ks_force > 0 ? std::min(ks_force, pl.num_chunks) : splitk_for(h, N, X, yo));
   float* kws = nullptr;
   if (KS > 1)
     SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws), size_t(KS) * pl.M * size_t(N) * 4,
@@ -1512,7 +1758,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   sdnn_status st = launch_main(h, X, N, bias, act, yo, ws, stream, kws, KS);
   if (KS > 1) {
     if (st == SDNN_OK) {
-      const dim3 grid{unsigned((N + 255) / 256), unsigned(pl.M)};
+      const dim3 grid{unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))};
       splitk_reduce_kernel<<<grid, 256, 0, stream>>>(kws, KS, pl.M, bias, act, yo, N);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("splitk_reduce_kernel: ") + cudaGetErrorString(le));
@@ -1521,7 +1767,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   }
   if (ns > 0) {
     if (st == SDNN_OK) {
-      const dim3 grid{unsigned((N + 255) / 256), unsigned(ns)};
+      const dim3 grid{unsigned((N + 255) / 256), unsigned(std::min(ns, 65535))};
       split_reduce_kernel<<<grid, 256, 0, stream>>>(ws, h->d_split, ns, bias, act, yo, N);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("split_reduce_kernel: ") + cudaGetErrorString(le));
@@ -1759,25 +2005,22 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
       ae = cudaFuncSetAttribute(spmm_generic_kernel<5, tmem_rows(8), 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
-    if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
-    if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_tmem_kernel<4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1868,7 +2111,9 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
   const std::vector<int32_t>* perm = &(*out)->plan.perm;  // Algorithm 1 once per handle
   sdnn_handle alt = nullptr;
   st = prepare_one(csr_ptr, col_idx, vals, M, K, &o, &alt, perm);
-  if (st != SDNN_OK) {
+  if (st == SDNN_ERR_UNSUPPORTED) {
+    alt = nullptr;  // no TMEM plan fits this matrix (metadata blocks beyond shared memory): row plans only
+  } else if (st != SDNN_OK) {
     std::string m = sdnn_last_error_message();
     sdnn_destroy(*out);
     *out = nullptr;
@@ -2029,6 +2274,7 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
   }();
   if (px_force <= 0 && (conv_force.first == 2 || conv_force.first == 4)) px_force = conv_force.first;
   if (ks_force <= 0 && conv_force.second > 0) ks_force = conv_force.second;
+  if (h->plan.no_split_k && ks_force > 1) ks_force = 1;  // a tuned / forced split never overrides the flag
   const Plan& pl = h->plan;
   if (int64_t(IC) * FY * FX != pl.K)
     return fail(SDNN_ERR_INVALID_ARGUMENT, "handle K = " + std::to_string(pl.K) + " != IC·FY·FX");
@@ -2130,7 +2376,7 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
       cudaError_t le = cudaLaunchKernel(fn2, dim3(unsigned(nb2), unsigned(KS)), dim3(unsigned(wc * 32)), args2,
                                         smem2, st_);
       if (le == cudaSuccess && KS > 1) {
-        splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(pl.M)), 256, 0, st_>>>(kws, KS, pl.M, bias, act,
+        splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, st_>>>(kws, KS, pl.M, bias, act,
                                                                                                 y_single(Y, N), N);
         le = cudaGetLastError();
       }
@@ -2337,17 +2583,72 @@ sdnn_status plan_with_meta(const sdnn_handle_s* h, Plan& out) {
   return SDNN_OK;
 }
 // Structural checks of a deserialized plan before it is uploaded and launched.
-bool plan_sane(const Plan& p) {
+bool plan_sane(const Plan& p, uint32_t role) {
   if (p.M < 1 || p.K < 1 || p.kernel < 1 || p.kernel > 5 || p.kernel == 3) return false;
+  // plan kind per role: 0 main (row / group / TMEM), 1 TMEM alternative, 2-3 narrow row plans
+  if ((role == 1 && p.kernel != 4 && p.kernel != 5) || (role >= 2 && p.kernel != 1)) return false;
   if (p.perm.size() != size_t(p.M) || p.num_row_blocks < 1 || p.num_chunks < 1 || p.k_chunk < 1) return false;
+  if (p.num_chunks != (p.K + p.k_chunk - 1) / p.k_chunk) return false;
+  // panel geometry the kernels are compiled for
+  if (p.num_panels != int64_t(p.num_row_blocks) * p.cta_panels) return false;
+  if (p.kernel == 4 && (p.panel_rows != tmem_rows(4) || p.cta_panels != kTmemRWarps || p.k_chunk != tmem_kc(4)))
+    return false;
+  if (p.kernel == 5 && (p.panel_rows != tmem_rows(8) || p.cta_panels != kTmemPanels || p.k_chunk != tmem_kc(8)))
+    return false;
+  if (p.kernel == 1 && ((p.panel_rows != 4 && p.panel_rows != 8) || p.cta_panels < 1 || p.cta_panels > 16)) return false;
+  if (p.kernel == 2 && (p.panel_rows != 16 || p.cta_panels < 1 || p.cta_panels > kMaxGroupWarps)) return false;
   if (p.blk_off.size() != size_t(p.num_row_blocks) * size_t(p.num_chunks) + 1) return false;
   if (p.row_orig.size() != size_t(p.num_panels) * size_t(p.panel_rows)) return false;
   if (p.blk_off.front() != 0 || p.blk_off.back() != int64_t(p.meta.size())) return false;
+  if (p.max_block_bytes < 16) return false;
+  // the stage ring the launch sizes from max_block_bytes must fit shared memory
+  const int mstage = int(align_up(p.max_block_bytes, 128));
+  if (p.kernel == 4 && tmemr_smem_bytes(mstage) > size_t(kSmemBudget) + 1024) return false;
+  if (p.kernel == 5 && tmem_smem_bytes(mstage) > size_t(kSmemBudget) + 1024) return false;
+  if ((p.kernel == 1 || p.kernel == 2) && int64_t(p.k_chunk) * kMaxTN * 4 + mstage > kSmemBudget) return false;
   for (size_t i = 1; i < p.blk_off.size(); ++i)
-    if (p.blk_off[i] < p.blk_off[i - 1] || p.blk_off[i] - p.blk_off[i - 1] > p.max_block_bytes) return false;
+    if (p.blk_off[i] < p.blk_off[i - 1] || p.blk_off[i] - p.blk_off[i - 1] > p.max_block_bytes ||
+        p.blk_off[i] % 16)
+      return false;
+  // split rows: piece tables of one length, split ranges inside them, output rows inside Y
+  if (p.piece_begin.size() != p.piece_row.size() || p.piece_end.size() != p.piece_row.size()) return false;
+  if (p.split_first.size() != p.split_row.size() || p.split_count.size() != p.split_row.size()) return false;
+  if (p.kernel != 1 && !p.piece_row.empty()) return false;
+  for (size_t i = 0; i < p.split_row.size(); ++i)
+    if (p.split_row[i] < 0 || p.split_row[i] >= p.M || p.split_first[i] < 0 || p.split_count[i] < 1 ||
+        int64_t(p.split_first[i]) + p.split_count[i] > int64_t(p.piece_row.size()))
+      return false;
   for (int32_t r : p.row_orig)
     if (r >= p.M || (r <= -2 && size_t(-2 - int64_t(r)) >= p.piece_row.size())) return false;
-  if (p.split_first.size() != p.split_row.size() || p.split_count.size() != p.split_row.size()) return false;
+  // row-format metadata (row / TMEM kernels): every slot's segment inside its block, columns inside
+  // the chunk (the kernels index shared / tensor memory with them)
+  if (p.kernel != 2) {
+    const int64_t rcta = int64_t(p.panel_rows) * p.cta_panels;
+    const int64_t hdr = align_up(rcta * 4, 16);
+    const int V = (p.kernel == 4 || p.kernel == 5) ? tmem_v(p.kernel) : 0;
+    for (int64_t b = 0; b + 1 < int64_t(p.blk_off.size()); ++b) {
+      const int64_t bytes = p.blk_off[b + 1] - p.blk_off[b];
+      if (bytes < hdr) return false;
+      const uint8_t* blk = p.meta.data() + p.blk_off[b];
+      const int64_t nent = (bytes - hdr) / 8;
+      for (int64_t sl = 0; sl < rcta; ++sl) {
+        uint32_t h;
+        std::memcpy(&h, blk + sl * 4, 4);
+        const int64_t start = h >> 16, cnt = V ? (h & 0xffu) : (h & 0xffffu), runs = V ? (h >> 8) & 0xffu : 0;
+        if (start + cnt + (cnt & 1) > nent || 4 * runs > cnt || (V && (start % 2 || cnt % 2))) return false;
+        for (int64_t e = start; e < start + cnt; ++e) {
+          uint32_t c;
+          std::memcpy(&c, blk + hdr + e * 8, 4);
+          if (V) {  // TMEM column V·k + 256·half | lane base of the slot's warp (kernel 4)
+            const uint32_t lb = p.kernel == 4 ? uint32_t(32 * ((sl / p.panel_rows) & 3)) << 16 : 0u;
+            if ((c & ~0xffffu) != lb || (c & 0xffffu) >= 512u || (c & 0xffu) % uint32_t(V)) return false;
+          } else if (c >= uint32_t(p.k_chunk)) {
+            return false;
+          }
+        }
+      }
+    }
+  }
   return true;
 }
 }  // namespace
@@ -2416,7 +2717,7 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
       r.s(role);
       Plan pl;
       plan_fields(r, pl);
-      if (!r.ok || role > 3 || parts[role] || (role == 3 && !parts[2]) || !plan_sane(pl) || (role == 0) != (i == 0))
+      if (!r.ok || role > 3 || parts[role] || (role == 3 && !parts[2]) || !plan_sane(pl, role) || (role == 0) != (i == 0))
         return cleanup(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan " + std::to_string(i) + ")");
       sdnn_status st = prepare_one(nullptr, nullptr, nullptr, pl.M, pl.K, nullptr, &parts[role], nullptr, &pl);
       if (st != SDNN_OK) {
@@ -2455,8 +2756,13 @@ sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* 
   std::vector<sdnn_handle_s::Tuned> cands{{-1, 0}};  // the built-in rules first (ties keep them)
   const bool has_tmem = (h->alt || h->plan.kernel == 4 || h->plan.kernel == 5) && N % 128 == 0;
   const bool row_ok = h->plan.kernel == 1 || h->plan.kernel == 2;
+  // TMEM split-K slices are cut at even chunks and keep ≥ 2 chunk pairs each (launch_tmem caps KS):
+  // candidates beyond that cap would repeat a smaller KS
+  const Plan& tp = h->alt ? h->alt->plan : h->plan;
+  const int tmem_ks_max = std::max(1, ((tp.num_chunks + 1) / 2) / 2);
   for (int ks : {1, 2, 4, 8}) {
-    if (has_tmem) cands.push_back({0, ks});
+    if (ks > 1 && h->plan.no_split_k) break;  // SDNN_FLAG_NO_SPLIT_K: never split the K range
+    if (has_tmem && (ks == 1 || ks <= tmem_ks_max)) cands.push_back({0, ks});
     if (row_ok) cands.push_back({1, ks});
     if (h->narrow) cands.push_back({2, ks});
     if (h->narrow4) cands.push_back({3, ks});
@@ -2469,6 +2775,10 @@ sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* 
   for (const auto& c : cands) {
     if (c.path == 1 && c.ks > 1 && !h->plan.split_row.empty()) continue;  // split rows: no split-K
     st = launch_path(h, c, X, N, nullptr, SDNN_ACT_NONE, yo, sm);          // warm-up
+    if (st != SDNN_OK && &c != &cands.front() && cudaPeekAtLastError() == cudaSuccess) {
+      st = SDNN_OK;  // a candidate this call cannot launch (e.g. a grid limit): skip it, keep tuning
+      continue;
+    }
     if (st != SDNN_OK) break;
     cudaEventRecord(e0, sm);
     for (int r = 0; r < 5 && st == SDNN_OK; ++r) st = launch_path(h, c, X, N, nullptr, SDNN_ACT_NONE, yo, sm);
@@ -2512,7 +2822,8 @@ sdnn_status sdnn_conv2d_tune(sdnn_handle h, const float* X, int32_t B, int32_t I
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   std::vector<std::pair<int, int>> cands{{-1, -1}};
   for (int px : {4, 2})
-    for (int ks : {1, 2, 4, 8}) cands.emplace_back(px, ks);
+    for (int ks : {1, 2, 4, 8})
+      if (ks == 1 || !h->plan.no_split_k) cands.emplace_back(px, ks);  // SDNN_FLAG_NO_SPLIT_K: never split
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   SDNN_CUDA_TRY(cudaEventCreate(&e0));
   SDNN_CUDA_TRY(cudaEventCreate(&e1));

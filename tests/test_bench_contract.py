@@ -28,3 +28,18 @@ def test_bench_rejects_short_warmup():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1"],
                        capture_output=True, text=True, timeout=120, cwd=ROOT)
     assert r.returncode != 0 and "warmup" in r.stderr
+
+
+def test_bench_self_launches_ranks_dry_run():
+    """`bench.py --gpus 2` with no outer launcher spawns the ranks itself (torch.distributed.run);
+    --dry-run does it on the CPU (gloo): 2 ranks, shards tile N, MAX-reduced time, rank 0 prints
+    one line with n_gpus = 2 and the gathered shards equal to the unsharded result."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] is True and d["shards_equal_unsharded"] is True
+    assert d["config"]["shards"] == [[0, 64], [64, 128]]

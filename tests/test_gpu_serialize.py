@@ -54,3 +54,74 @@ def test_codegen_not_serialized(sdnn):
     with pytest.raises(sdnn.SdnnError) as e:
         sdnn.Handle.from_problem(p, kernel="codegen").serialize()
     assert e.value.status == 3
+
+
+# blob layout (sdnn_spmm.cu plan_fields): scalar fields, then length-prefixed vectors
+_SCALARS = [("M", "i4"), ("K", "i4"), ("nnz", "i8"), ("permuted", "i4"), ("permuted_output", "i4"),
+            ("no_split_k", "i4"), ("kernel", "i4"), ("group_entries", "i8"), ("group_sb", "i4"),
+            ("group_subblocks", "i8"), ("panel_rows", "i4"), ("cta_panels", "i4"), ("num_panels", "i4"),
+            ("num_row_blocks", "i4"), ("k_chunk", "i4"), ("num_chunks", "i4"), ("max_block_bytes", "i4"),
+            ("max_panel_nnz", "i8"), ("tmem_fill", "i4")]
+_VECTORS = [("perm", "i4"), ("row_orig", "i4"), ("blk_off", "i8"), ("meta", "u1"), ("piece_row", "i4"),
+            ("piece_begin", "i4"), ("piece_end", "i4"), ("split_row", "i4"), ("split_first", "i4"),
+            ("split_count", "i4")]
+
+
+def _index(blob: bytes):
+    """{(plan index, field): (byte offset, dtype, count)} of every plan in a blob."""
+    off, out = 16, {}
+    nplans = int.from_bytes(blob[12:16], "little")
+    for i in range(nplans):
+        out[(i, "role")] = (off, "u4", 1)
+        off += 4
+        for name, dt in _SCALARS:
+            out[(i, name)] = (off, dt, 1)
+            off += np.dtype(dt).itemsize
+        for name, dt in _VECTORS:
+            n = int.from_bytes(blob[off:off + 8], "little")
+            out[(i, name)] = (off + 8, dt, n)
+            off += 8 + n * np.dtype(dt).itemsize
+    assert off == len(blob)
+    return out
+
+
+def _patch(blob: bytes, idx, plan: int, field: str, value, at: int = 0) -> bytes:
+    off, dt, n = idx[(plan, field)]
+    assert at < n
+    size = np.dtype(dt).itemsize
+    b = bytearray(blob)
+    b[off + at * size:off + (at + 1) * size] = np.array([value], dtype=dt).tobytes()
+    return bytes(b)
+
+
+def test_corrupt_fields_rejected(sdnn):
+    """Structural corruptions the kernels would turn into out-of-bounds accesses are rejected by the
+    deserializer: split-row targets, split / piece table bounds, panel geometry, plan kind
+    per role, metadata segment bounds and TMEM columns."""
+    p = synth.config_problem("c2_768x768")  # auto: row plan with split rows (role 0) + TMEM plan (role 1)
+    blob = sdnn.Handle.from_problem(p).serialize()
+    idx = _index(blob)
+    roles = {int(np.frombuffer(blob, "u4", 1, idx[(i, "role")][0])[0]): i for i in range(len({k[0] for k in idx}))}
+    row, tm = roles[0], roles[1]
+    assert idx[(row, "split_row")][2] > 0  # the fixture really has split rows
+    meta_off, _, _ = idx[(tm, "meta")]
+    hdr_bytes = 10 * 24 * 4
+    first_entry = int(np.frombuffer(blob, "u4", 1, meta_off)[0]) >> 16
+    bad = [
+        _patch(blob, idx, row, "split_row", p.M),                        # reduction writes past Y
+        _patch(blob, idx, row, "split_row", -1),
+        _patch(blob, idx, row, "split_first", 10**6),                   # beyond the piece table
+        _patch(blob, idx, row, "split_count", 0),
+        _patch(blob, idx, row, "num_panels", 1),                        # != row blocks × CTA panels
+        _patch(blob, idx, row, "panel_rows", 6),                        # not a compiled geometry
+        _patch(blob, idx, tm, "cta_panels", 6),                         # TMEM kernel: 24 warps
+        _patch(blob, idx, tm, "kernel", 1),                             # role 1 must be a TMEM plan
+        _patch(blob, idx, tm, "max_block_bytes", 200 * 1024),           # stage ring beyond shared memory
+        _patch(blob, idx, tm, "meta", 0xFF, at=2),                      # slot 0: start 0x..FF.. beyond block
+        _patch(blob, idx, tm, "meta", 0x7F, at=hdr_bytes + 8 * first_entry + 1),  # TMEM column ≥ 512
+    ]
+    for i, b in enumerate(bad):
+        with pytest.raises(sdnn.SdnnError) as e:
+            sdnn.Handle.deserialize(b)
+        assert e.value.status == 1, i  # SDNN_ERR_INVALID_ARGUMENT
+    sdnn.Handle.deserialize(blob).close()  # the unmodified blob still loads

@@ -31,7 +31,15 @@ def _worker(rank, world, port, q):
         c0, c1 = bench.shard_range(p.N, rank, world)
         t = bench.max_over_ranks(float(rank + 1), dist)
         plan = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K)
-        same = bench.check_same_across_ranks(bench.plan_hash(plan.info(), sdnn.permutation(p.row_ptr, p.col_idx, p.M, p.K)), dist)
+        # the hash covers the packed arrays (meta, blk_off, row_orig, split tables), not just the info:
+        # a one-byte difference in one rank's metadata must be caught
+        arrays = [*plan.export(), *plan.export_pieces()]
+        packed = b"".join(np.ascontiguousarray(a).tobytes() for a in arrays)
+        same = bench.check_same_across_ranks(bench.plan_hash(packed), dist)
+        meta = arrays[2].copy()
+        meta[len(meta) // 2] ^= 1 if rank == 1 else 0
+        tampered = b"".join(np.ascontiguousarray(a).tobytes() for a in [arrays[0], arrays[1], meta, *arrays[3:]])
+        caught = not bench.check_same_across_ranks(bench.plan_hash(tampered), dist)
         differ = bench.check_same_across_ranks(f"rank{rank}", dist)
         Y, _ = oracle.spmm(p.row_ptr, p.col_idx, p.vals, p.M, p.K, p.x_cols(c0, c1), p.bias, act=1, want_scale=False)
         parts = [None] * world
@@ -42,7 +50,7 @@ def _worker(rank, world, port, q):
         Yg = nccl_gather(torch.from_numpy(Y), column_bounds(p.N, world)).numpy()
         Yfull, _ = oracle.spmm(p.row_ptr, p.col_idx, p.vals, p.M, p.K, p.x(), p.bias, act=1, want_scale=False)
         assert np.array_equal(Yg, Yfull)
-        q.put((rank, c0, c1, t, same, differ, parts if rank == 0 else None))
+        q.put((rank, c0, c1, t, same and caught, differ, parts if rank == 0 else None))
     finally:
         dist.destroy_process_group()
 

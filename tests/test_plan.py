@@ -15,8 +15,8 @@ def decode(p, plan):
     row_orig, blk_off, meta = plan.export()
     rw, wc, kc, nch, nrb = (info[k] for k in ("panel_rows", "cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
     V = {4: 4, 5: 8}.get(info["kernel"], 0)
-    if V:
-        assert (rw, wc, kc) == ((10, 6, 64) if V == 4 else (5, 6, 32))
+    if V:  # kernel 4: 24 warps with their own panels (replicated TMEM lane quarters); kernel 5: 6 slots
+        assert (rw, wc, kc) == ((10, 24, 64) if V == 4 else (5, 6, 32))
     rcta = rw * wc
     hdr_bytes = (rcta * 4 + 15) // 16 * 16
     assert blk_off[0] == 0 and blk_off[-1] == meta.size and np.all(np.diff(blk_off) > 0)
@@ -49,8 +49,8 @@ def decode(p, plan):
                 if orow < 0:
                     assert cnt == 0
                     continue
-                if V:  # TMEM format: segments padded to multiples of 4 (V = 4) / 2 (V = 8)
-                    assert cnt % (4 if V == 4 else 2) == 0
+                if V:  # TMEM format: segments padded to whole pairs
+                    assert cnt % 2 == 0
                 elif cnt % 2:  # row format: an odd segment's partner slot is the zero entry the kernels read
                     assert not np.any(ent[(start + cnt) * 8:(start + cnt) * 8 + 8])
                 for i in range(cnt):
@@ -58,6 +58,10 @@ def decode(p, plan):
                     cl = int(e[:4].view(np.uint32)[0])
                     w = e[4:].view(np.float32)[0]
                     if V:  # column field = V·col_local + 256·(chunk parity): the TMEM column of X[col]
+                        # (kernel 4: | TMEM lane base of the slot's warp quarter, (32·(warp % 4)) << 16)
+                        lane_base = ((32 * ((s // rw) % 4)) << 16) if V == 4 else 0
+                        assert cl & ~0xFFFF == lane_base
+                        cl &= 0xFFFF
                         half = 256 * (j & 1)
                         if w == 0:
                             assert cl == half  # padding entry
@@ -71,7 +75,8 @@ def decode(p, plan):
                     triples.append((orow, col, w))
     for b, j, at in runs:  # a run is 4 consecutive columns k..k+3, k % 4 == 0
         blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]]
-        cols = [int(blk[hdr_bytes + (at + t) * 8:hdr_bytes + (at + t) * 8 + 4].view(np.uint32)[0]) for t in range(4)]
+        cols = [int(blk[hdr_bytes + (at + t) * 8:hdr_bytes + (at + t) * 8 + 4].view(np.uint32)[0]) & 0xFFFF
+                for t in range(4)]
         assert cols == [cols[0] + 4 * t for t in range(4)] and (cols[0] % 256) % 16 == 0
     decode.runs = len(runs)
     # pieces of a row: consecutive ids q = 0..P-1, piece q = entries row_ptr[r] + q, + P, … (interleaved)
