@@ -99,6 +99,7 @@ struct sdnn_handle_s {
   std::map<std::array<int32_t, 8>, std::pair<int32_t, int32_t>> conv_tuned;
   mutable std::mutex tune_mu;
   int32_t sms = 148;
+  bool tmem_runs = true;  // kernel 4 plan with aligned 1×4 runs in its metadata (else the run-free consumer)
   HostStage hs;         // sdnn_spmm_host staging (created on first use)
   std::mutex host_mu;
 };
@@ -1223,7 +1224,7 @@ constexpr size_t tmemr_smem_bytes(int m_stage_bytes) {
   return size_t(kTmemRPieces) * kTmemRPieceBytes + size_t(kTmemRMetaSlots) * m_stage_bytes + 32 * 8 + 16;
 }
 
-template <bool MULTI, bool SPLIT>
+template <bool MULTI, bool SPLIT, bool RUNS>
 __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& p, uint8_t* mring, uint64_t* mfull,
                                               uint64_t* mempty, uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0,
                                               int warp, int lane) {
@@ -1240,21 +1241,27 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
     tc_fence_after();
     const uint8_t* ms = mring + size_t(m) * p.m_stage_bytes;
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + warp * RW;
-    const float4* ent = reinterpret_cast<const float4*>(ms + p.hdr_bytes);
+    // the warp's row segments are contiguous in the block (emit order): one stream pointer for all
+    // of them, started at the first row's segment; row headers give the entry counts (prefetched one
+    // row ahead)
+    uint32_t hn = hdr[0];
+    const float4* e = reinterpret_cast<const float4*>(ms + p.hdr_bytes) + (hn >> 17);
 #pragma unroll
     for (int r = 0; r < RW; ++r) {
-      const uint32_t hh = hdr[r];
-      int n = int(hh & 0xffu);  // entries (a whole number of pairs)
-      const float4* e = ent + (hh >> 17);
-      for (int nrun = int((hh >> 8) & 0xffu); nrun > 0; --nrun, e += 2, n -= 4) {  // aligned 1×4 runs
-        const float4 e0 = e[0], e1 = e[1];
-        float4 xa, xb, xc, xd;
-        tmem_ld16(__float_as_uint(e0.x), xa, xb, xc, xd);
-        tmem_wait_ld(xa, xb, xc, xd);
-        fma4(acc[r], e0.y, xa);
-        fma4(acc[r], e0.w, xb);
-        fma4(acc[r], e1.y, xc);
-        fma4(acc[r], e1.w, xd);
+      const uint32_t hh = hn;
+      if (r + 1 < RW) hn = hdr[r + 1];
+      int n = int(hh & 0xffu);  // entries (a whole number of pairs), runs included
+      if constexpr (RUNS) {
+        for (int nrun = int((hh >> 8) & 0xffu); nrun > 0; --nrun, e += 2, n -= 4) {  // aligned 1×4 runs
+          const float4 e0 = e[0], e1 = e[1];
+          float4 xa, xb, xc, xd;
+          tmem_ld16(__float_as_uint(e0.x), xa, xb, xc, xd);
+          tmem_wait_ld(xa, xb, xc, xd);
+          fma4(acc[r], e0.y, xa);
+          fma4(acc[r], e0.w, xb);
+          fma4(acc[r], e1.y, xc);
+          fma4(acc[r], e1.w, xd);
+        }
       }
       for (; n >= 4; n -= 4, e += 2) {  // two pairs: four loads in flight
         const float4 e0 = e[0], e1 = e[1];
@@ -1277,6 +1284,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
         tmem_wait_ld(xa, xb);
         fma4(acc[r], e0.y, xa);
         fma4(acc[r], e0.w, xb);
+        ++e;
       }
     }
     tc_fence_before();
@@ -1312,7 +1320,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
   }
 }
 
-template <bool MULTI = false, bool SPLIT = false>
+template <bool MULTI = false, bool SPLIT = false, bool RUNS = true>
 __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     spmm_tmemr_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI || SPLIT> p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1383,8 +1391,9 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     }
     for (int j = 0; j < jr.y; ++j) {
       const int h = j & 1;
-      if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
-        mbar_wait(&tfree[h], ((j >> 1) - 1) & 1);
+      if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it (suspending:
+                     // a filler polling try_wait took ~18 % of the SM's issue slots, ncu r2_tmemr_full)
+        mbar_wait_sleep(&tfree[h], ((j >> 1) - 1) & 1);
         tc_fence_after();
       }
       if (leader && j >= MS) {
@@ -1418,7 +1427,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     }
   } else {
     if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0 (addresses are absolute)
-    tmemr_consume<MULTI, SPLIT>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
+    tmemr_consume<MULTI, SPLIT, RUNS>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -1603,7 +1612,8 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     return SDNN_OK;
   }
   if (rep && multi) spmm_tmemr_kernel<true, false><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (rep) spmm_tmemr_kernel<false, false><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
+  else if (rep && h->tmem_runs) spmm_tmemr_kernel<false, false, true><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
+  else if (rep) spmm_tmemr_kernel<false, false, false><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
   else if (multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
   else if (fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
   else if (fill == 1) spmm_tmem_kernel<8, 1><<<grid, threads, smem, stream>>>(tmap, p);
@@ -2007,7 +2017,10 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
@@ -2044,6 +2057,19 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
   if (e != cudaSuccess)
     return cleanup(e == cudaErrorMemoryAllocation ? SDNN_ERR_OUT_OF_MEMORY : SDNN_ERR_CUDA,
                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  if (pl.kernel == 4) {  // any aligned 1×4 runs (header bits 8..15)?  else launches take the run-free consumer
+    h->tmem_runs = false;
+    const int64_t rcta = int64_t(pl.panel_rows) * pl.cta_panels;
+    for (size_t b = 0; b + 1 < pl.blk_off.size() && !h->tmem_runs; ++b)
+      for (int64_t sl = 0; sl < rcta; ++sl) {
+        uint32_t hw;
+        std::memcpy(&hw, pl.meta.data() + pl.blk_off[b] + sl * 4, 4);
+        if ((hw >> 8) & 0xffu) {
+          h->tmem_runs = true;
+          break;
+        }
+      }
+  }
   if (!pl.meta.empty()) e = cudaMemcpy(h->d_meta, pl.meta.data(), pl.meta.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(h->d_blk_off, pl.blk_off.data(), pl.blk_off.size() * 8, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
