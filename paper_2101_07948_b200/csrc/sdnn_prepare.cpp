@@ -3,6 +3,7 @@
 // execution-ordered format the kernel reads sequentially (§3.2.2).  No CUDA here; the
 // upload lives in sdnn_spmm.cu.  Independent of oracle/ (shares no code with it).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -96,6 +97,7 @@ void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32
 struct Geometry {
   int32_t kernel, rw, wc, kc, nch, nrb, sb;
   int32_t tmem = 0;  // TMEM kernel variant of the row format (see emit_blocks)
+  bool runs = true;  // TMEM V = 4: encode leading aligned 1×4 runs (block-clustered masks only)
 };
 struct EmitStats {
   int64_t entries = 0;    // row kernel: padded entries; group kernel: union entries
@@ -175,7 +177,7 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
             const int32_t stp = step[s];
             while (p < end && col_idx[p] < hi) {
               const int32_t col = col_idx[p];
-              if (stp == 1 && g.tmem == 4 && leading && col % 4 == 0 && p + 3 < end && col_idx[p + 3] == col + 3 &&
+              if (stp == 1 && g.tmem == 4 && g.runs && leading && col % 4 == 0 && p + 3 < end && col_idx[p + 3] == col + 3 &&
                   col + 3 < hi) {
                 for (int32_t t = 0; t < 4; ++t) put((uint32_t(col + t - lo) * 4u + half) | lane_base, vals[p + t]);
                 p += 4;
@@ -372,6 +374,17 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
         g.kernel = 1;
         g.tmem = tmem_v(kernel);
         g.rw = tmem_rows(g.tmem);
+        // runs pay only on block-clustered masks: encode them when ≥ 1/4 of the nonzeros sit in aligned
+        // 1×4 groups (a uniform 90 % mask has ~0.1 % by chance — then the kernel takes its run-free loop)
+        if (g.tmem == 4) {
+          int64_t in_runs = 0;
+          for (int32_t r = 0; r < M; ++r)
+            for (int32_t q = csr_ptr[r]; q + 3 < csr_ptr[r + 1]; ++q)
+              if (col_idx[q] % 4 == 0 && col_idx[q + 3] == col_idx[q] + 3) in_runs += 4;
+          g.runs = 4 * in_runs >= nnz;
+        }
+        // (rows per warp: 10 measured against 9 and 8 on c5 — 41.8 / 43.4 / 48.1 ms,
+        // profiles/r02_tmemr_rows_per_warp.log: fewer rows per CTA cost more than the freed registers gain)
         g.wc = kernel == 4 ? kTmemRWarps : kTmemPanels;
         g.nrb = (M + g.rw * g.wc - 1) / (g.rw * g.wc);
         return g;

@@ -1224,11 +1224,10 @@ constexpr size_t tmemr_smem_bytes(int m_stage_bytes) {
   return size_t(kTmemRPieces) * kTmemRPieceBytes + size_t(kTmemRMetaSlots) * m_stage_bytes + 32 * 8 + 16;
 }
 
-template <bool MULTI, bool SPLIT, bool RUNS>
+template <bool MULTI, bool SPLIT, bool RUNS, int RW>
 __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& p, uint8_t* mring, uint64_t* mfull,
                                               uint64_t* mempty, uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0,
                                               int warp, int lane) {
-  constexpr int RW = tmem_rows(4);
   constexpr int MS = kTmemRMetaSlots;
   float2 acc[RW][2];
 #pragma unroll
@@ -1320,7 +1319,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
   }
 }
 
-template <bool MULTI = false, bool SPLIT = false, bool RUNS = true>
+template <bool MULTI = false, bool SPLIT = false, bool RUNS = true, int RW = tmem_rows(4)>
 __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     spmm_tmemr_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI || SPLIT> p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1427,7 +1426,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     }
   } else {
     if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0 (addresses are absolute)
-    tmemr_consume<MULTI, SPLIT, RUNS>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
+    tmemr_consume<MULTI, SPLIT, RUNS, RW>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -2022,6 +2021,7 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
+
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
