@@ -1205,11 +1205,13 @@ __global__ void __launch_bounds__((kTmemConsumers + tmem_side_warps<FILL>()) * 3
 //   * N tile TN = 128; every TMEM lane quarter holds the same tile: lane 32q + l ↔ columns
 //     n0 + 4l .. 4l+3, TMEM column 4·k + v (+ 256 for the odd K chunks) ↔ X[k0 + k].  Two halves of
 //     256 columns double-buffer K chunks of 64 rows.
-//   * filler warp q (one per quarter) copies every 8 KB TMA piece (16 K rows × 128 columns) from the
-//     shared-memory ring into its quarter (LDS.128 → tcgen05.st.32x32b.x16); filler 0 lane 0 issues
-//     the TMA pieces and the per-chunk metadata bulk copies.  Each X element staged from L2 serves
-//     240 rows (24 warps × 10), 4× the rows of a non-replicated 512-column tile — a quarter of the
-//     L2 → SM traffic for the same accumulator registers.
+//   * issuer warp q (lane 0) streams piece q (16 K rows × 128 columns, 8 KB) of every K chunk: TMA into
+//     its own two shared-memory slots, then one tcgen05.cp.32x128b.warpx4 per K row, which copies the
+//     row's 512 bytes into the same 32 lanes × 16 B of all four lane quarters (the copy engine does
+//     the replication: one shared-memory read per X element; the LDS.128 + tcgen05.st fill it replaced
+//     read every element four times and cost 12 % of the kernel, profiles/r02_fill_lds_vs_sttm.log,
+//     r02_ab_tmemr_cp.log).  Issuer 0 also bulk-copies the per-chunk metadata.  Each X element staged
+//     from L2 serves 240 rows (24 warps × 10), 4× the rows of a non-replicated 512-column tile.
 //   * consumer warp w (quarter w % 4) owns a 10-row panel; its metadata already holds the TMEM
 //     address (lane base | column), so per pair of nonzeros: one LDS.128 (col, w, col, w), two R2UR,
 //     two tcgen05.ld.32x32b.x4, four FFMA2 — two pairs per step while ≥ 2 remain; rows are padded to
@@ -1341,10 +1343,10 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&slot_full[s], 1);
-      mbar_init(&slot_empty[s], 4);
+      mbar_init(&slot_empty[s], 1);  // the issuer's tcgen05.commit
     }
     for (int h = 0; h < 2; ++h) {
-      mbar_init(&tfull[h], 4);
+      mbar_init(&tfull[h], 4);  // one tcgen05.commit per issuer
       mbar_init(&tfree[h], kTmemRConsumers);
     }
     for (int m = 0; m < MS; ++m) {
@@ -1362,67 +1364,57 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
   tc_fence_after();
   const uint32_t tbase = *tbase_s;
 
-  if (warp >= kTmemRConsumers) {  // fillers: TMA → smem ring → LDS.128 → tcgen05.st → TMEM half
+  if (warp >= kTmemRConsumers) {
+    // issuers: filler q owns piece q (16 K rows) of every chunk: TMA → its own two smem slots (q, q + 4
+    // for even / odd chunks) → 16 × tcgen05.cp.32x128b.warpx4 (one per K row: 512 B of smem into the
+    // same 32 lanes × 16 B of all four lane quarters) → commit to the slot's and the half's mbarriers.
+    // One smem read per X element instead of four LDS.128 (one per quarter): the LDS fill cost 12 % of
+    // the kernel (profiles/r02_fill_lds_vs_sttm.log).
     const int q = warp & 3;
-    const uint32_t tq = tbase + (uint32_t(q * 32) << 16);
-    const bool leader = warp == kTmemRConsumers && lane == 0;
-    const int2 jr = tmem_chunks<SPLIT>(p.nch);  // this CTA's chunks (all of them unless split-K)
-    const int64_t* off = p.blk_off + int64_t(rb) * p.nch + jr.x;
-    const int total = jr.y * PPC;
-    auto load_piece = [&](int i) {
-      const int s = i % S;
-      if (p.dbg & 1) {
-        mbar_arrive(&slot_full[s]);
-        return;
-      }
-      mbar_expect_tx(&slot_full[s], kTmemRPieceBytes);
-      tma_load_2d(xring + size_t(s) * kTmemRPieceBytes, &tmap, int32_t(n0), (jr.x * PPC + i) * PK, &slot_full[s]);
-    };
-    auto load_meta = [&](int j) {
-      const int m = j % MS;
-      const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
-      mbar_expect_tx(&mfull[m], mbytes);
-      bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[j], mbytes, &mfull[m]);
-    };
-    if (leader) {
-      for (int i = 0; i < S && i < total; ++i) load_piece(i);
-      for (int j = 0; j < MS && j < jr.y; ++j) load_meta(j);
-    }
-    for (int j = 0; j < jr.y; ++j) {
-      const int h = j & 1;
-      if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it (suspending:
-                     // a filler polling try_wait took ~18 % of the SM's issue slots, ncu r2_tmemr_full)
-        mbar_wait_sleep(&tfree[h], ((j >> 1) - 1) & 1);
-        tc_fence_after();
-      }
-      if (leader && j >= MS) {
-        mbar_wait(&mempty[j % MS], ((j / MS) - 1) & 1);
-        load_meta(j);
-      }
-      for (int pc = 0; pc < PPC; ++pc) {
-        const int i = j * PPC + pc, s = i % S;
-        mbar_wait(&slot_full[s], (i / S) & 1);
-        if (!(p.dbg & 4)) {
-          const float4* src = reinterpret_cast<const float4*>(xring + size_t(s) * kTmemRPieceBytes) + lane;
-          float4 v[4][4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int t = 0; t < 4; ++t) v[u][t] = src[(4 * u + t) * 32];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) tmem_st16(tq + uint32_t(h * 256 + (pc * PK + 4 * u) * 4), v[u]);
+    const int2 jr = tmem_chunks<SPLIT>(p.nch);
+    if (lane == 0) {
+      const int64_t* off = p.blk_off + int64_t(rb) * p.nch + jr.x;
+      auto load_piece = [&](int j) {
+        const int s = q + 4 * (j & 1);
+        if (p.dbg & 1) {
+          mbar_arrive(&slot_full[s]);
+          return;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&slot_empty[s]);
-        if (leader && i + S < total) {
-          mbar_wait(&slot_empty[s], (i / S) & 1);
-          load_piece(i + S);
+        mbar_expect_tx(&slot_full[s], kTmemRPieceBytes);
+        tma_load_2d(xring + size_t(s) * kTmemRPieceBytes, &tmap, int32_t(n0), (jr.x + j) * 64 + q * PK, &slot_full[s]);
+      };
+      auto load_meta = [&](int j) {
+        const int m = j % MS;
+        const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
+        mbar_expect_tx(&mfull[m], mbytes);
+        bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[j], mbytes, &mfull[m]);
+      };
+      for (int j = 0; j < 2 && j < jr.y; ++j) load_piece(j);
+      if (q == 0)
+        for (int j = 0; j < MS && j < jr.y; ++j) load_meta(j);
+      for (int j = 0; j < jr.y; ++j) {
+        const int h = j & 1, s = q + 4 * h;
+        if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
+          mbar_wait_sleep(&tfree[h], ((j >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        if (q == 0 && j >= MS) {
+          mbar_wait(&mempty[j % MS], ((j / MS) - 1) & 1);
+          load_meta(j);
+        }
+        mbar_wait(&slot_full[s], (j >> 1) & 1);
+        const uint32_t src = smem_u32(xring + size_t(s) * kTmemRPieceBytes);
+#pragma unroll
+        for (int kk = 0; kk < PK; ++kk)
+          asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tbase + uint32_t(h * 256 + (q * PK + kk) * 4)),
+                       "l"(cp_desc(src + uint32_t(kk) * 512)) : "memory");
+        tc_commit(&slot_empty[s]);
+        tc_commit(&tfull[h]);
+        if (j + 2 < jr.y) {
+          mbar_wait(&slot_empty[s], (j >> 1) & 1);
+          load_piece(j + 2);
         }
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tfull[h]);
     }
   } else {
     if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0 (addresses are absolute)
