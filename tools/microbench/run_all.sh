@@ -1,6 +1,7 @@
 #!/bin/bash
 # microbenchmarks on the box (B3b); output -> gpurun_out/microbench.log
 cd "$(dirname "$0")"
+python gen_bigcode.py  # bigcode*.inc for peaks.cu (generated, not committed)
 mkdir -p ../../gpurun_out
 {
 echo "== host"; nproc; grep -m1 "model name" /proc/cpuinfo; free -g | head -2; python -c "import os; print('affinity', len(os.sched_getaffinity(0)))"
