@@ -199,6 +199,16 @@ def oracle_sample(p, target_s: float = 12.0, max_cols: int = 16384, threads: int
                           f" x {reps}"), dt
 
 
+def plan_geometry(p, info: dict, kid: int, kernel: str) -> dict:
+    """Geometry of the plan the timed call launched: the handle's TMEM plan (built beside the row plan
+    by an auto handle) when the call took the TMEM kernel, else the handle's own plan."""
+    if abs(kid) == 4 and info["kernel"] != 4:
+        import paper_2101_07948_b200 as sdnn
+        info = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem").info()
+    return {"panel_rows": info["panel_rows"], "cta_panels": info["cta_panels"], "k_chunk": info["k_chunk"],
+            "num_row_blocks": info["num_row_blocks"]}
+
+
 def tmem_operand_bytes(p, N: int, kc: int = 64) -> int:
     """TMEM → register bytes one launch of the TMEM kernel reads: every (row, K chunk) segment is
     padded to whole pairs of entries, and each entry is one 512-byte tcgen05.ld.32x32b.x4 per
@@ -518,7 +528,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
                    "l2": "inputs larger than L2 (X shard %.0f MiB > 126 MB L2); no flush" % (p.K * Nr * 4 / 2**20),
                    "kernel": kernel_desc,
                    "group_entries_per_nnz": info["group_entries_per_nnz_x1000"] / 1000, "group_sb": info["group_sb"],
-                   "panel_rows": info["panel_rows"], "cta_panels": info["cta_panels"], "k_chunk": info["k_chunk"],
+                   **plan_geometry(p, info, kid, args.kernel),
                    "permuted": bool(info["permuted"]), "prep_ms": round(prep_ms, 1), "plan_hash": phash,
                    "plan_hash_identical": same},
         "roofline": {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(fp32_peak_tf, 2),
