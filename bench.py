@@ -415,7 +415,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
     # fused = the whole step with the gather in the epilogue (sdnn_spmm_multi into every rank's
     # symmetric-memory Y + barrier), to set beside ms_per_step
     ag_ms = fused_ms = None
-    fused_ok = None
+    fused_ok = fused_mode = None
     if args.allgather and world > 1:
         Yall = torch.empty((world, p.M, Nr), dtype=torch.float32, device=dev)
         for _ in range(2):
@@ -440,6 +440,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
             print(f"fused all-gather unavailable: {e}", file=sys.stderr)
             fg = None
         if fg is not None:
+            fused_mode = fg.mode  # "multicast" (multimem.st through NVSwitch) or "peer" (stores to every rank)
             for _ in range(2):
                 fg.spmm(h, X, bias, act=1)
             torch.cuda.synchronize()
@@ -553,6 +554,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
         "allgather_ms": None if ag_ms is None else round(ag_ms, 3),
         "fused_allgather_step_ms": None if fused_ms is None else round(fused_ms, 3),
         "fused_allgather_ok": fused_ok,
+        "fused_allgather_mode": fused_mode,
         "shard_proxy": proxy,
         "configs": cfgs,
     }

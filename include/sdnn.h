@@ -169,6 +169,16 @@ SDNN_API sdnn_status sdnn_spmm(sdnn_handle h, const float* X, int64_t N, const f
 SDNN_API sdnn_status sdnn_spmm_multi(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act,
                                      float* const* Y_dsts, int32_t n_dst, int64_t ldy, int64_t col0, void* stream);
 
+/* sdnn_spmm_multicast: the fused all-gather through NVLink SHARP multicast: Y_mc is a
+ * multicast address — one virtual address bound to every rank's M×ldy row-major Y buffer (e.g.
+ * torch symmetric memory's multicast_ptr) — and the epilogue writes each output element once with
+ * multimem.st; NVSwitch replicates it into every rank's buffer at columns [col0, col0 + N).  Same
+ * argument rules and errors as sdnn_spmm_multi with n_dst = 1; the caller owns the multicast object
+ * and orders visibility with its barrier.  Without multicast support use sdnn_spmm_multi with the
+ * peers' addresses. */
+SDNN_API sdnn_status sdnn_spmm_multicast(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act,
+                                         float* Y_mc, int64_t ldy, int64_t col0, void* stream);
+
 /* sdnn_spmm_host: the same operation on HOST buffers (X host K×N, bias host fp32[M] or NULL, Y host
  * M×N).  Columns are processed in blocks of `block_cols` (0 = auto), with host→device copy, kernel
  * and device→host copy of successive blocks overlapped on internal streams; pinned (page-locked)

@@ -25,7 +25,7 @@ STATUS = {0: "SDNN_OK", 1: "SDNN_ERR_INVALID_ARGUMENT", 2: "SDNN_ERR_INVALID_CSR
           4: "SDNN_ERR_OUT_OF_MEMORY", 5: "SDNN_ERR_CUDA", 6: "SDNN_ERR_DEVICE_MISMATCH", 7: "SDNN_ERR_INTERNAL"}
 
 # exported symbols (must match include/sdnn.h; checked by tests/test_abi.py)
-EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_conv2d", "sdnn_serialize", "sdnn_tune", "sdnn_conv2d_tune",
+EXPORTS = ["sdnn_prepare", "sdnn_destroy", "sdnn_spmm", "sdnn_spmm_multi", "sdnn_spmm_multicast", "sdnn_conv2d", "sdnn_serialize", "sdnn_tune", "sdnn_conv2d_tune",
            "sdnn_deserialize", "sdnn_spmm_host", "sdnn_spmm_kernel",
            "sdnn_get_permutation",
            "sdnn_get_info",
@@ -68,6 +68,7 @@ _lib.sdnn_prepare.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.POINTER(PermOpts
 _lib.sdnn_destroy.argtypes = [_vp]
 _lib.sdnn_spmm.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _vp]
 _lib.sdnn_spmm_multi.argtypes = [_vp, _vp, _i64, _vp, _i32, ctypes.POINTER(_vp), _i32, _i64, _i64, _vp]
+_lib.sdnn_spmm_multicast.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64, _i64, _vp]
 _lib.sdnn_spmm_host.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64]
 _lib.sdnn_get_permutation.argtypes = [_vp, _vp]
 _lib.sdnn_spmm_kernel.argtypes = [_vp, _i64, _vp, _vp, ctypes.POINTER(_i32)]
@@ -356,6 +357,19 @@ class Handle:
         _check(_lib.sdnn_spmm_multi(self._h, X.data_ptr(), X.shape[1], None if bias is None else bias.data_ptr(),
                                     _act(act), arr, len(dst_ptrs), int(ldy), int(col0), s.cuda_stream),
                "sdnn_spmm_multi")
+
+    def spmm_multicast(self, X, mc_ptr: int, ldy: int, col0: int, bias=None, act="relu", stream=None):
+        """Y = act(W·X + b) stored once through a multicast address (multimem.st; NVSwitch writes every
+        rank's buffer), M×ldy row-major, columns [col0, col0 + N) — sdnn_spmm_multicast."""
+        import torch
+        if X.dim() != 2 or X.shape[0] != self.K or X.dtype != torch.float32 or not X.is_cuda or not X.is_contiguous():
+            raise ValueError(f"X must be a contiguous CUDA float32 tensor of shape ({self.K}, N)")
+        if bias is not None and (bias.numel() != self.M or bias.dtype != torch.float32 or not bias.is_cuda):
+            raise ValueError("bias must be a CUDA float32 tensor of M elements")
+        s = torch.cuda.current_stream(X.device) if stream is None else stream
+        _check(_lib.sdnn_spmm_multicast(self._h, X.data_ptr(), X.shape[1], None if bias is None else bias.data_ptr(),
+                                        _act(act), int(mc_ptr), int(ldy), int(col0), s.cuda_stream),
+               "sdnn_spmm_multicast")
 
     def spmm_host(self, X: np.ndarray, bias: np.ndarray | None = None, act="relu", out: np.ndarray | None = None,
                   block_cols: int = 0):

@@ -160,8 +160,31 @@ constexpr int kMaxDst = 8;
 struct YOut {
   float* y[kMaxDst];
   int32_t n;
+  int32_t mc;  // 1: y[0] is a multicast address (sdnn_spmm_multicast): stores are multimem.st, which
+               // NVSwitch replicates into every rank's buffer
   int64_t ld, col0;
 };
+// Y written as sdnn_spmm writes it: one plain destination, leading dimension N, no offset
+static bool y_plain(const YOut& o, int64_t N) { return o.n == 1 && o.ld == N && o.col0 == 0 && !o.mc; }
+// stores of output elements: plain (streaming) or multimem (multicast destination)
+__device__ __forceinline__ void y_st4(float* p, float a, float b, float c, float d, bool mc) {
+  if (mc)
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+  else
+    __stcs(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));
+}
+__device__ __forceinline__ void y_st2(float* p, float a, float b, bool mc) {
+  if (mc)
+    asm volatile("multimem.st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+  else
+    __stcs(reinterpret_cast<float2*>(p), make_float2(a, b));
+}
+__device__ __forceinline__ void y_st1(float* p, float a, bool mc) {
+  if (mc)
+    asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+  else
+    *p = a;
+}
 static YOut y_single(float* Y, int64_t N) {
   YOut o{};
   o.y[0] = Y;
@@ -329,11 +352,12 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
                       : piece  ? p.ws + int64_t(-2 - orow) * p.N
                       : single ? p.Y + int64_t(orow) * p.N
                                : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
+        const bool mc = !single && !p.kws && p.yo.mc;
         if (VEC) {
-          if (n < p.N) __stcs(reinterpret_cast<float2*>(yrow + n), make_float2(v[0], v[1]));
+          if (n < p.N) y_st2(yrow + n, v[0], v[1], mc);
         } else {
-          if (n < p.N) yrow[n] = v[0];
-          if (n + 1 < p.N) yrow[n + 1] = v[1];
+          if (n < p.N) y_st1(yrow + n, v[0], mc);
+          if (n + 1 < p.N) y_st1(yrow + n + 1, v[1], mc);
         }
       }
       continue;
@@ -358,12 +382,13 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
                       : piece  ? p.ws + int64_t(-2 - orow) * p.N
                       : single ? p.Y + int64_t(orow) * p.N
                                : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
+        const bool mc = !single && !p.kws && p.yo.mc;
         if (VEC) {
-          if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
+          if (n < p.N) y_st4(yrow + n, v[0], v[1], v[2], v[3], mc);
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (n + q < p.N) yrow[n + q] = v[q];
+            if (n + q < p.N) y_st1(yrow + n + q, v[q], mc);
         }
       }
     }
@@ -384,7 +409,7 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t*
   if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
 #pragma unroll
   for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
-    if (d < yo.n) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+    if (d < yo.n) y_st1(yo.y[d] + int64_t(row) * yo.ld + yo.col0 + n, v, yo.mc);
   }
 }
 
@@ -402,7 +427,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ kws, int32_t KS, 
     if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
 #pragma unroll
     for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
-      if (d < yo.n) yo.y[d][int64_t(row) * yo.ld + yo.col0 + n] = v;
+      if (d < yo.n) y_st1(yo.y[d] + int64_t(row) * yo.ld + yo.col0 + n, v, yo.mc);
   }
 }
 
@@ -997,8 +1022,7 @@ __device__ __forceinline__ void tmem_consume(const TmemParams<MULTI || SPLIT>& p
       } else if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
         if (n < p.N)
           for (int d = 0; d < p.yo.n; ++d)
-            __stcs(reinterpret_cast<float4*>(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n),
-                   make_float4(v[0], v[1], v[2], v[3]));
+            y_st4(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n, v[0], v[1], v[2], v[3], p.yo.mc);
       } else {
         if (n < p.N) __stcs(reinterpret_cast<float4*>(yrow + n), make_float4(v[0], v[1], v[2], v[3]));
       }
@@ -1313,8 +1337,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
              make_float4(v[0], v[1], v[2], v[3]));
     } else if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
       for (int d = 0; d < p.yo.n; ++d)
-        __stcs(reinterpret_cast<float4*>(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n),
-               make_float4(v[0], v[1], v[2], v[3]));
+        y_st4(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n, v[0], v[1], v[2], v[3], p.yo.mc);
     } else {
       __stcs(reinterpret_cast<float4*>(p.Y + int64_t(orow) * p.N + n), make_float4(v[0], v[1], v[2], v[3]));
     }
@@ -1528,7 +1551,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   p.X = X;
   p.bias = bias;
   p.yo = yo;
-  p.Y = (yo.n == 1 && yo.ld == N && yo.col0 == 0) ? yo.y[0] : nullptr;
+  p.Y = y_plain(yo, N) ? yo.y[0] : nullptr;
   p.N = N;
   p.K = pl.K;
   p.nch = pl.num_chunks;
@@ -1579,7 +1602,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   const int fill = rep ? 1 : (fill_env >= 0 ? fill_env : pl.tmem_fill);
   const unsigned threads = rep ? unsigned(kTmemRConsumers + 4) * 32 : unsigned(kTmemConsumers + (fill ? 4 : 1)) * 32;
   const unsigned grid = unsigned(nblocks);
-  const bool multi = !(yo.n == 1 && yo.ld == N && yo.col0 == 0);
+  const bool multi = !y_plain(yo, N);
   if (multi && fill != 1) return fail(SDNN_ERR_UNSUPPORTED, "multi-destination TMEM launch needs the filler-warp fill");
   if (KS > 1) {  // split-K slices (raw partial sums) + splitk_reduce_kernel
     if (multi || fill != 1 || !pool) return fail(SDNN_ERR_INTERNAL, "TMEM split-K needs one destination and a pool");
@@ -1687,7 +1710,7 @@ static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const Y
 static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo) {
   const sdnn_handle_s* a = h->alt;
   if (!a || h->plan.no_split_k || !h->ws_pool) return 0;
-  if (!(yo.n == 1 && yo.ld == N && yo.col0 == 0)) return 0;
+  if (!y_plain(yo, N)) return 0;
   if (!(N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))) return 0;
   static const int env = [] {
     const char* e = getenv("SDNN_TMEM_SPLIT_K");
@@ -1780,7 +1803,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
 
 // Fast-path call (aligned X / Y, one destination, N % 4 == 0) that sdnn_tune measured for this N.
 static bool tuned_for(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo, sdnn_handle_s::Tuned* t) {
-  if (!(yo.n == 1 && yo.ld == N && yo.col0 == 0) || N % 4 || reinterpret_cast<uintptr_t>(X) % 16 || !y_aligned16(yo))
+  if (!y_plain(yo, N) || N % 4 || reinterpret_cast<uintptr_t>(X) % 16 || !y_aligned16(yo))
     return false;
   std::lock_guard<std::mutex> lk(h->tune_mu);
   const auto it = h->tuned.find(N);
@@ -1843,7 +1866,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   p.X = X;
   p.bias = bias;
   p.yo = yo;
-  p.Y = (yo.n == 1 && yo.ld == N && yo.col0 == 0) ? yo.y[0] : nullptr;
+  p.Y = y_plain(yo, N) ? yo.y[0] : nullptr;
   p.N = N;
   p.K = pl.K;
   p.nch = pl.num_chunks;
@@ -2254,6 +2277,29 @@ sdnn_status sdnn_spmm_multi(sdnn_handle h, const float* X, int64_t N, const floa
     if (overlaps(Y_dsts[d], span, X, size_t(h->plan.K) * size_t(N) * 4) || overlaps(Y_dsts[d], span, bias, size_t(h->plan.M) * 4))
       return fail(SDNN_ERR_INVALID_ARGUMENT, "a destination overlaps X or bias");
   }
+  sdnn_status st = check_device(h);
+  if (st != SDNN_OK) return st;
+  return launch(h, X, N, bias, act, yo, static_cast<cudaStream_t>(stream));
+}
+
+sdnn_status sdnn_spmm_multicast(sdnn_handle h, const float* X, int64_t N, const float* bias, int32_t act, float* Y_mc,
+                                int64_t ldy, int64_t col0, void* stream) {
+  if (!h) return fail(SDNN_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->plan.kernel == 3) return fail(SDNN_ERR_UNSUPPORTED, "the codegen kernel has no multicast epilogue");
+  float* const dst[1] = {Y_mc};
+  // validation and launch as sdnn_spmm_multi with one destination, then flag it multicast
+  if (N < 0) return fail(SDNN_ERR_INVALID_ARGUMENT, "N < 0");
+  if (act != SDNN_ACT_NONE && act != SDNN_ACT_RELU) return fail(SDNN_ERR_INVALID_ARGUMENT, "unknown act");
+  if (!Y_mc) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL multicast destination");
+  if (col0 < 0 || ldy < col0 + N) return fail(SDNN_ERR_INVALID_ARGUMENT, "need col0 >= 0 and ldy >= col0 + N");
+  if (N == 0) return SDNN_OK;
+  if (!X) return fail(SDNN_ERR_INVALID_ARGUMENT, "X is NULL");
+  YOut yo{};
+  yo.n = 1;
+  yo.mc = 1;
+  yo.ld = ldy;
+  yo.col0 = col0;
+  yo.y[0] = dst[0];
   sdnn_status st = check_device(h);
   if (st != SDNN_OK) return st;
   return launch(h, X, N, bias, act, yo, static_cast<cudaStream_t>(stream));
