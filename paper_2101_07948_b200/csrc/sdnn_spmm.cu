@@ -1636,12 +1636,12 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   return SDNN_OK;
 }
 
-// The TMEM kernel runs one CTA per SM and pays once the call has at least half a wave of CTAs
-// (measured per config, profiles/r01_configs_v5.log: it wins from ~100 CTAs up — c2 3072×768,
-// c3 512² — while the row kernel, several CTAs per SM, wins on c3 256×128 (65 TMEM CTAs) and below).
+// The TMEM kernel runs one CTA per SM and pays once the call has at least a third of a wave of
+// CTAs (round 2, TMEM-R kernel: 3072×768 at N = 512, 52 CTAs, 38.1 → 32.9 µs against the row plan,
+// profiles/r02_tune_rules.log; round 1's kernel needed half a wave).
 static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const YOut& yo) {
   return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo) &&
-         2 * int64_t(a->plan.num_row_blocks) * ((N + tmem_tn(a->plan.kernel) - 1) / tmem_tn(a->plan.kernel)) >= a->sms;
+         3 * int64_t(a->plan.num_row_blocks) * ((N + tmem_tn(a->plan.kernel) - 1) / tmem_tn(a->plan.kernel)) >= a->sms;
 }
 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
@@ -1702,11 +1702,15 @@ static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const Y
   const int64_t ks = std::min<int64_t>({8, pl.num_chunks / 4, 16 * int64_t(h->sms) / warps});
   return ks >= 2 ? int(ks) : 1;
 }
-// TMEM plan with split-K: a call on the TMEM fast path whose grid is under half a wave (so
-// tmem_worth declined it) but whose K range is long: KS ≤ 8 slices (of ≥ 4 chunks, cut at even
-// chunks) bring the grid to about one wave, for N of at least one full TMEM tile
-// (profiles/r01_tmem_split_k.log: c2 768×3072 66 → 58 µs, 512×4096 N = 2048 116 → 85 µs; at
-// N = 256 half the tile's lanes idle and it lost).  SDNN_TMEM_SPLIT_K=0 disables it.
+// TMEM plan with split-K: a call on the TMEM fast path whose grid is under 0.9 of a wave runs over
+// KS ≤ 8 slices of K (cut at even chunks, ≥ 2 chunk pairs each), KS = ⌊SMs / grid⌋, then the
+// slice-ordered reduction — when K has ≥ 16 chunks (shorter ranges: the unsplit kernel or the row
+// plans), at a single N tile only for long K (≥ 48 chunks; ≥ 32 with ≥ 20 % nonzeros), and when the
+// split grid reaches a third of a wave.  Re-derived for the TMEM-R kernel from sdnn_tune over the
+// BASELINE configs and the round-1 shape grid (profiles/r02_tune_rules*.log): 4096² N = 512 146 →
+// 96 µs, 768×3072 N = 2048 95 → 67 µs, 512×4096 N = 2048 91 → 48 µs; 768×3072 / 512×4096 at N = 128
+// (4 / 3 row blocks) stay on the row plan's split-K (22.2 / 19.9 → 14.7 / 13.0 µs).
+// SDNN_TMEM_SPLIT_K=0 disables it.
 static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo) {
   const sdnn_handle_s* a = h->alt;
   if (!a || h->plan.no_split_k || !h->ws_pool) return 0;
@@ -1717,25 +1721,18 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
     return e ? atoi(e) : -1;
   }();
   if (env == 0) return 0;
-  const int64_t TN = tmem_tn(a->plan.kernel);
-  const int64_t grid = int64_t(a->plan.num_row_blocks) * ((N + TN - 1) / TN);
-  // a partial TMEM tile wastes lanes; at a single TMEM tile (N < 2·TN) only long K (≥ 48 chunks)
-  // beat the row / narrow plans (profiles/r01_tune_shapes*.log: 2048², 1024² at N = 512 lost;
-  // 512×4096, 1024×4096 at N = 512 and every N ≥ 1024 won)
-  // — unless the matrix is dense enough (≥ 20 % nonzeros) that a 32-chunk K range already pays
-  // (profiles/r01_tune_grid.log: 2048² at 70 / 80 %, N = 512: 113 → 88 µs, 81 → 71 µs)
   const Plan& ap = a->plan;
+  const int64_t TN = tmem_tn(ap.kernel);
+  const int64_t grid = int64_t(ap.num_row_blocks) * ((N + TN - 1) / TN);
+  if (10 * grid >= 9 * int64_t(h->sms) || ap.num_chunks < 16) return 0;
   const bool dense = 5 * ap.nnz >= int64_t(ap.M) * ap.K;
-  if (2 * grid > h->sms || N < TN || ap.num_chunks < (N >= 2 * TN ? 16 : dense ? 32 : 48)) return 0;
-  const int64_t ks = std::min<int64_t>({8, ap.num_chunks / 4, h->sms / grid});
-  // several TMEM tiles: the split CTAs must keep ≥ 3.5 MFLOP each, else the partial-sum round trip
-  // and the per-CTA fill start-up lose to the row plans (r01_tune_grid.log: 1024² at 80-95 % and
-  // 2048² at 95 %, N = 1024: 35-70 µs against 21-63 µs; c2 768×3072, N = 1024, 3.7 MFLOP, still wins)
-  // — unless the K range is long (≥ 32 chunks) and cut at least 4 ways, where the split is what
-  // fills the GPU (r01_tune_shapes_rules.log: 512×4096 at 95 %, N = 1024 / 2048, 1.5 MFLOP per CTA:
-  // 54 → 43 µs, 92 → 68 µs)
-  if (N >= 2 * TN && ap.nnz * N * 4 < int64_t(7000000) * grid * ks && !(ap.num_chunks >= 32 && ks >= 4)) return 0;
-  return ks >= 2 ? int(ks) : 0;
+  if (N < 2 * TN && ap.num_chunks < (dense ? 32 : 48)) return 0;
+  const int64_t pairs = (ap.num_chunks + 1) / 2;
+  // at most one CTA per SM in total: a second partial wave of split CTAs doubles the time (768×3072,
+  // N = 1024: 5 slices of 32 CTAs = 160 CTAs, 55 µs against 39 µs at 4 slices)
+  const int64_t ks = std::min<int64_t>({8, pairs / 2, int64_t(h->sms) / grid});
+  if (ks < 2 || 3 * grid * ks < h->sms) return 0;
+  return int(ks);
 }
 static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
   if (!h->narrow) return false;
@@ -1834,9 +1831,9 @@ static sdnn_status launch(sdnn_handle_s* h, const float* X, int64_t N, const flo
 // The built-in per-call rules (what an untuned call takes).
 static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                const YOut& yo, cudaStream_t stream) {
-  if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
   if (const int ks = tmem_split_for(h, X, N, yo); ks > 1)
     return launch_tmem(h->alt, X, N, bias, act, yo, stream, ks, h->ws_pool);
+  if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
   if (sdnn_handle_s* nw = narrow_pick(h, N)) return launch(nw, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
