@@ -110,7 +110,7 @@ def _csr(row_ptr, col_idx, vals):
     return rp, ci, v
 
 
-KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4, "tmem8": 5}
+KERNELS = {"auto": 0, "row": 1, "group": 2, "codegen": 3, "tmem": 4, "tmem8": 5, "tmemp": 6}
 
 
 FLAG_NO_ROW_SPLIT = 1

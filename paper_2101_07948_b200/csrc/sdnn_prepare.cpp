@@ -3,6 +3,7 @@
 // execution-ordered format the kernel reads sequentially (§3.2.2).  No CUDA here; the
 // upload lives in sdnn_spmm.cu.  Independent of oracle/ (shares no code with it).
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -98,6 +99,7 @@ struct Geometry {
   int32_t kernel, rw, wc, kc, nch, nrb, sb;
   int32_t tmem = 0;  // TMEM kernel variant of the row format (see emit_blocks)
   bool runs = true;  // TMEM V = 4: encode leading aligned 1×4 runs (block-clustered masks only)
+  bool pairs = false;  // kernel 6: Algorithm 1 row pairs, shared columns loaded once (emit_blocks)
 };
 struct EmitStats {
   int64_t entries = 0;    // row kernel: padded entries; group kernel: union entries
@@ -143,7 +145,71 @@ static void emit_blocks(const int32_t* csr_ptr, const int32_t* col_idx, const fl
       const int32_t lo = j * g.kc, hi = lo + g.kc;
       uint8_t* blk = out ? out + (*offs)[size_t(b) * g.nch + j] : nullptr;
       int64_t bytes = 0;
-      if (g.kernel == 1) {
+      if (g.pairs) {
+        // kernel 6 (TMEM, Algorithm 1 row pairs): per pair of slots (2i, 2i+1) of a warp, the chunk's
+        // entries of its two rows split three ways, each ascending: shared columns (16 bytes:
+        // {TMEM column, w_a, w_b, 0}, one load feeding both rows), then the first row's other
+        // columns and then the second row's ({TMEM column, w} pairs of 8 bytes, each list padded to
+        // whole pairs with weight-0 entries).  Headers: slot 2i = start << 16 | shared << 8 | a-only
+        // count, slot 2i+1 = start of its list << 16 | b-only count (entries of 8 bytes).
+        const int64_t hdr = align_up(int64_t(rcta) * 4, 16);
+        const uint32_t half = uint32_t(j & 1) * 256u;
+        int32_t e = 0;
+        std::vector<std::pair<int32_t, float>> ra, rb;
+        for (int32_t s = 0; s < rcta; s += 2) {
+          const uint32_t lane_base = uint32_t(32 * ((s / g.rw) & 3)) << 16;
+          for (int32_t t = 0; t < 2; ++t) {
+            auto& lst = t ? rb : ra;
+            lst.clear();
+            const int32_t orow = row_orig[size_t(b) * rcta + s + t];
+            if (orow < 0) continue;
+            int32_t& q = cur[s + t];
+            while (q < stop[s + t] && col_idx[q] < hi) {
+              lst.push_back({col_idx[q] - lo, vals ? vals[q] : 0.f});
+              ++q;
+            }
+          }
+          std::vector<std::array<float, 2>> sh;
+          std::vector<int32_t> shc;
+          std::vector<std::pair<int32_t, float>> ao, bo;
+          size_t ia = 0, ib = 0;
+          while (ia < ra.size() || ib < rb.size()) {
+            if (ib == rb.size() || (ia < ra.size() && ra[ia].first < rb[ib].first)) ao.push_back(ra[ia++]);
+            else if (ia == ra.size() || rb[ib].first < ra[ia].first) bo.push_back(rb[ib++]);
+            else {
+              shc.push_back(ra[ia].first);
+              sh.push_back({ra[ia].second, rb[ib].second});
+              ++ia, ++ib;
+            }
+          }
+          const int32_t na = int32_t(align_up(int64_t(ao.size()), 2)), nb = int32_t(align_up(int64_t(bo.size()), 2));
+          const int32_t ns = int32_t(sh.size());
+          if (blk) {
+            auto put = [&](int32_t at, uint32_t cl, float w) {
+              std::memcpy(blk + hdr + size_t(at) * 8, &cl, 4);
+              std::memcpy(blk + hdr + size_t(at) * 8 + 4, &w, 4);
+            };
+            for (int32_t i = 0; i < ns; ++i) {  // {column, w_a} {w_b, 0}
+              const uint32_t cl = (uint32_t(shc[i]) * 4u + half) | lane_base;
+              std::memcpy(blk + hdr + size_t(e + 2 * i) * 8, &cl, 4);
+              std::memcpy(blk + hdr + size_t(e + 2 * i) * 8 + 4, &sh[i][0], 4);
+              std::memcpy(blk + hdr + size_t(e + 2 * i + 1) * 8, &sh[i][1], 4);
+            }
+            const int32_t a0 = e + 2 * ns, b0 = a0 + na;
+            for (int32_t i = 0; i < na; ++i)
+              i < int32_t(ao.size()) ? put(a0 + i, (uint32_t(ao[i].first) * 4u + half) | lane_base, ao[i].second)
+                                     : put(a0 + i, half | lane_base, 0.f);
+            for (int32_t i = 0; i < nb; ++i)
+              i < int32_t(bo.size()) ? put(b0 + i, (uint32_t(bo[i].first) * 4u + half) | lane_base, bo[i].second)
+                                     : put(b0 + i, half | lane_base, 0.f);
+            reinterpret_cast<uint32_t*>(blk)[s] = (uint32_t(e) << 16) | (uint32_t(ns) << 8) | uint32_t(na);
+            reinterpret_cast<uint32_t*>(blk)[s + 1] = (uint32_t(b0) << 16) | uint32_t(nb);
+          }
+          e += 2 * ns + na + nb;
+        }
+        ent_total += e;
+        bytes = align_up(hdr + int64_t(e) * 8, 16);
+      } else if (g.kernel == 1) {
         // TMEM variant (g.tmem = V): the column field is the TMEM column offset of X[col] in the
         // chunk's TMEM half (V·col_local + 256·(j mod 2)) — for kernel 4 (g.wc = 24, replicated lane
         // quarters) with the TMEM lane base of the slot's warp, (32·(warp mod 4)) << 16, added — and
@@ -284,8 +350,8 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     if ((o.flags & SDNN_FLAG_PERMUTED_OUTPUT) && o.kernel == 3)
       return fail(SDNN_ERR_UNSUPPORTED, "SDNN_FLAG_PERMUTED_OUTPUT is not available with the codegen kernel");
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
-    if (o.kernel < 0 || o.kernel > 5) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..5");
-    if (o.kernel == 4 || o.kernel == 5) {
+    if (o.kernel < 0 || o.kernel > 6) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..6");
+    if (o.kernel == 4 || o.kernel == 5 || o.kernel == 6) {
       if (o.panel_rows_max != 0 || o.cta_panels != 0 || (o.k_chunk != 0 && o.k_chunk != tmem_kc(tmem_v(o.kernel))) ||
           o.group_sb != 0)
         return fail(SDNN_ERR_INVALID_ARGUMENT, "the TMEM kernel has a fixed geometry (leave the tiling options 0)");
@@ -367,7 +433,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     // the machine for the typical N.
     auto make_geo = [&](int32_t kernel, int32_t sb) {
       Geometry g{};
-      if (kernel == 4 || kernel == 5) {
+      if (kernel == 4 || kernel == 5 || kernel == 6) {
         // TMEM kernels (sdnn_spmm.cu): row-kernel format, tmem_rows(V)-row warp panels; kernel 4: 24
         // panels per CTA row block (one per consumer warp, replicated lane quarters), kernel 5: 6
         // (one per warp slot, shared by the 4 lane quarters); K chunk = one TMEM half.
@@ -376,7 +442,9 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
         g.rw = tmem_rows(g.tmem);
         // runs pay only on block-clustered masks: encode them when ≥ 1/4 of the nonzeros sit in aligned
         // 1×4 groups (a uniform 90 % mask has ~0.1 % by chance — then the kernel takes its run-free loop)
-        if (g.tmem == 4) {
+        if (g.pairs) {
+          g.runs = false;  // kernel 6: no x16 run loads (a run's four entries are ordinary entries)
+        } else if (g.tmem == 4) {
           int64_t in_runs = 0;
           for (int32_t r = 0; r < M; ++r)
             for (int32_t q = csr_ptr[r]; q + 3 < csr_ptr[r + 1]; ++q)
@@ -385,7 +453,8 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
         }
         // (rows per warp: 10 measured against 9 and 8 on c5 — 41.8 / 43.4 / 48.1 ms,
         // profiles/r02_tmemr_rows_per_warp.log: fewer rows per CTA cost more than the freed registers gain)
-        g.wc = kernel == 4 ? kTmemRWarps : kTmemPanels;
+        g.wc = (kernel == 4 || kernel == 6) ? kTmemRWarps : kTmemPanels;
+        g.pairs = kernel == 6;
         g.nrb = (M + g.rw * g.wc - 1) / (g.rw * g.wc);
         return g;
       }
@@ -425,6 +494,47 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       std::vector<int32_t> pos(M);
       for (int32_t i = 0; i < M; ++i) pos[plan.perm[i]] = i;
       auto nz = [&](int32_t r) { return csr_ptr[r + 1] - csr_ptr[r]; };
+      if (g.pairs) {
+        // kernel 6: rows go in pairs of consecutive Algorithm 1 positions (perm[2i], perm[2i+1]) —
+        // the rows with the most common columns — so a shared column is loaded once for
+        // both; pairs are dealt to warps by the LPT (weight = both rows' nonzeros), rw / 2 per warp,
+        // and keep their Algorithm 1 order inside a warp
+        const int32_t np = (M + 1) / 2, cap = g.rw / 2;
+        g.nrb = std::max(g.nrb, int32_t((int64_t(np) + int64_t(cap) * g.wc - 1) / (int64_t(cap) * g.wc)));
+        const int32_t nw = g.nrb * g.wc;
+        std::vector<std::pair<int64_t, int32_t>> items;
+        items.reserve(size_t(np));
+        for (int32_t i = 0; i < np; ++i)
+          items.push_back({nz(plan.perm[2 * i]) + (2 * i + 1 < M ? nz(plan.perm[2 * i + 1]) : 0), i});
+        std::stable_sort(items.begin(), items.end(),
+                         [](const std::pair<int64_t, int32_t>& a, const std::pair<int64_t, int32_t>& b) {
+                           return a.first > b.first;
+                         });
+        std::vector<std::pair<int64_t, int32_t>> heap;
+        for (int32_t w = 0; w < nw; ++w) heap.push_back({0, w});
+        auto cmp = [](const std::pair<int64_t, int32_t>& a, const std::pair<int64_t, int32_t>& b) { return a > b; };
+        std::vector<std::vector<int32_t>> prs(nw);
+        for (const auto& it : items) {
+          std::pop_heap(heap.begin(), heap.end(), cmp);
+          auto [load, w] = heap.back();
+          heap.pop_back();
+          prs[w].push_back(it.second);
+          if (int32_t(prs[w].size()) < cap) {
+            heap.push_back({load + it.first + 1, w});
+            std::push_heap(heap.begin(), heap.end(), cmp);
+          }
+        }
+        std::vector<int32_t> ro(size_t(nw) * g.rw, -1);
+        for (int32_t w = 0; w < nw; ++w) {
+          std::sort(prs[w].begin(), prs[w].end());
+          for (size_t j = 0; j < prs[w].size(); ++j) {
+            const int32_t i = prs[w][j];
+            ro[size_t(w) * g.rw + 2 * j] = plan.perm[2 * i];
+            if (2 * i + 1 < M) ro[size_t(w) * g.rw + 2 * j + 1] = plan.perm[2 * i + 1];
+          }
+        }
+        return ro;
+      }
       // items: whole rows (id = row) and pieces (id = −2 − piece); weight = nonzeros
       std::vector<std::pair<int64_t, int32_t>> items;
       items.reserve(size_t(M));
@@ -492,7 +602,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
         g.kc = c;
         g.nch = (K + c - 1) / c;
         emit_blocks(csr_ptr, col_idx, vals, ro, g, sizes, nullptr, nullptr, entries, &pcs);
-        if (g.tmem == 4)  // kernel 4: 8 KB TMA pieces × kTmemRPieces + two metadata slots
+        if (g.tmem == 4)  // kernels 4 / 6: 8 KB TMA pieces × kTmemRPieces + two metadata slots
           return int64_t(kTmemRPieces) * 8192 + 2 * align_up(max_of(sizes), 128) + 1024 <= kSmemBudget;
         const int32_t s = stages_for(c, max_of(sizes));
         if (s >= 3 || (s >= 2 && (o.k_chunk || c == 8))) return true;
@@ -523,7 +633,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     EmitStats stats;
     {
       std::vector<Geometry> cands;
-      if (o.kernel == 4 || o.kernel == 5) {
+      if (o.kernel == 4 || o.kernel == 5 || o.kernel == 6) {
         o.k_chunk = tmem_kc(tmem_v(o.kernel));
         cands.push_back(make_geo(o.kernel, 0));
       } else if (o.kernel != 2) {
@@ -553,7 +663,7 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       pcs = best_pcs;
       if (!found) return fail(SDNN_ERR_UNSUPPORTED, "no K chunk fits the shared-memory budget");
     }
-    plan.kernel = (o.kernel == 4 || o.kernel == 5) ? o.kernel : g.kernel;
+    plan.kernel = (o.kernel == 4 || o.kernel == 5 || o.kernel == 6) ? o.kernel : g.kernel;
     plan.panel_rows = g.rw;
     plan.cta_panels = g.wc;
     plan.num_row_blocks = g.nrb;

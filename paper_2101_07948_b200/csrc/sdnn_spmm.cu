@@ -225,6 +225,12 @@ struct KParamsY : KParams {
 };
 template <bool MULTI> using TmemParams = std::conditional_t<MULTI, KParamsY, KParams>;
 
+// acc[0..1] (4 columns of one row) += w · x
+__device__ __forceinline__ void fma4(float2 (&acc)[2], float w, const float4& x) {
+  const float2 w2 = make_float2(w, w);
+  acc[0] = __ffma2_rn(w2, make_float2(x.x, x.y), acc[0]);
+  acc[1] = __ffma2_rn(w2, make_float2(x.z, x.w), acc[1]);
+}
 // Consume one chunk: for each of the warp's RW rows, every (col, w) entry of the chunk:
 // acc[r] += w · X_stage[col][lane·4 .. +4] (and +128 for V = 8), ascending column order.
 // TF = log2 of the TMEM-kernel metadata scale (column field = 2^TF·col_local + 256·half; 0 = row format),
@@ -282,6 +288,31 @@ __device__ __forceinline__ void consume_chunk(float2 (&acc)[RW][V / 2], const fl
         }
       }
     }
+  }
+}
+
+// Generic fallback of a kernel-6 plan (Algorithm 1 row pairs, V = 4 tiles of 128 columns in the
+// stage): per pair of rows, the shared columns (one X slice feeding both) then each row's own, in the
+// order the TMEM kernel sums them.
+template <int RW>
+__device__ __forceinline__ void consume_pairs(float2 (&acc)[RW][2], const float* __restrict__ xs,
+                                              const uint8_t* __restrict__ ms, int warp, int lane, int hdr_bytes) {
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + warp * RW;
+  const float2* ent = reinterpret_cast<const float2*>(ms + hdr_bytes);  // {column field, weight}
+  const float* xl = xs + lane * 4;
+  auto xrow = [&](float cf) { return *reinterpret_cast<const float4*>(xl + ((__float_as_uint(cf) & 255u) >> 2) * 128); };
+#pragma unroll
+  for (int i = 0; i < RW / 2; ++i) {
+    const uint32_t ha = hdr[2 * i], hb = hdr[2 * i + 1];
+    const int ns = int((ha >> 8) & 0xffu), na = int(ha & 0xffu), nb = int(hb & 0xffu);
+    const float2* e = ent + (ha >> 16);
+    for (int k = 0; k < ns; ++k, e += 2) {
+      const float4 x = xrow(e[0].x);
+      fma4(acc[2 * i], e[0].y, x);
+      fma4(acc[2 * i + 1], e[1].x, x);
+    }
+    for (int k = 0; k < na; ++k, ++e) fma4(acc[2 * i], e->y, xrow(e->x));
+    for (int k = 0; k < nb; ++k, ++e) fma4(acc[2 * i + 1], e->y, xrow(e->x));
   }
 }
 
@@ -497,7 +528,7 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
 // Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
 // threads using bounds-checked loads (zero fill) and a block barrier instead of TMA/mbarriers.
 template <int KIND, int RW, int V, int SB = 0>
-__global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : KIND == 4 ? kTmemRWarps * 32 : 16 * 32, 1)
+__global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : (KIND == 4 || KIND == 6) ? kTmemRWarps * 32 : 16 * 32, 1)
     spmm_generic_kernel(const KParamsY p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TN = 32 * V;
@@ -529,8 +560,10 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : KIND == 4 ? 
     __syncthreads();
     if constexpr (KIND == 2)
       consume_group<V, SB>(acc, xs, ms, warp, lane);
+    else if constexpr (KIND == 6)
+      consume_pairs<RW>(acc, xs, ms, warp, lane, p.hdr_bytes);
     else
-      consume_chunk<RW, V, (KIND >= 4 ? KIND - 2 : 0)>(acc, xs, ms, warp, lane, p.hdr_bytes);
+      consume_chunk<RW, V, (KIND == 4 || KIND == 5 ? KIND - 2 : 0)>(acc, xs, ms, warp, lane, p.hdr_bytes);
   }
   epilogue<RW, V, false>(acc, p, rb * p.wc + warp, lane, n0);
 }
@@ -832,12 +865,6 @@ __device__ __forceinline__ void tmem_wait_ld(float4& a, float4& b, float4& c, fl
                  "+f"(c.x), "+f"(c.y), "+f"(c.z), "+f"(c.w), "+f"(d.x), "+f"(d.y), "+f"(d.z), "+f"(d.w)
                :
                : "memory");
-}
-// acc[0..1] (4 columns of one row) += w · x
-__device__ __forceinline__ void fma4(float2 (&acc)[2], float w, const float4& x) {
-  const float2 w2 = make_float2(w, w);
-  acc[0] = __ffma2_rn(w2, make_float2(x.x, x.y), acc[0]);
-  acc[1] = __ffma2_rn(w2, make_float2(x.z, x.w), acc[1]);
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float4 (&v)[4]) {
   asm volatile(
@@ -1250,7 +1277,7 @@ constexpr size_t tmemr_smem_bytes(int m_stage_bytes) {
   return size_t(kTmemRPieces) * kTmemRPieceBytes + size_t(kTmemRMetaSlots) * m_stage_bytes + 32 * 8 + 16;
 }
 
-template <bool MULTI, bool SPLIT, bool RUNS, int RW>
+template <bool MULTI, bool SPLIT, bool RUNS, int RW, bool PAIRS = false>
 __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& p, uint8_t* mring, uint64_t* mfull,
                                               uint64_t* mempty, uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0,
                                               int warp, int lane) {
@@ -1271,6 +1298,60 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
     // row ahead)
     uint32_t hn = hdr[0];
     const float4* e = reinterpret_cast<const float4*>(ms + p.hdr_bytes) + (hn >> 17);
+    if constexpr (PAIRS) {  // kernel 6: Algorithm 1 row pairs (rows 2i, 2i+1): shared columns, then each row's own
+#pragma unroll
+      for (int i = 0; i < RW / 2; ++i) {
+        const uint32_t ha = hdr[2 * i], hb = hdr[2 * i + 1];
+        int ns = int((ha >> 8) & 0xffu);
+        for (; ns >= 2; ns -= 2, e += 2) {  // two shared columns {col, w_a, w_b, 0}: one load feeds both rows
+          const float4 e0 = e[0], e1 = e[1];
+          float4 xa, xb;
+          tmem_ld4(__float_as_uint(e0.x), xa);
+          tmem_ld4(__float_as_uint(e1.x), xb);
+          tmem_wait_ld(xa, xb);
+          fma4(acc[2 * i], e0.y, xa);
+          fma4(acc[2 * i + 1], e0.z, xa);
+          fma4(acc[2 * i], e1.y, xb);
+          fma4(acc[2 * i + 1], e1.z, xb);
+        }
+        if (ns) {
+          const float4 e0 = e[0];
+          float4 xa;
+          tmem_ld4(__float_as_uint(e0.x), xa);
+          tmem_wait_ld(xa);
+          fma4(acc[2 * i], e0.y, xa);
+          fma4(acc[2 * i + 1], e0.z, xa);
+          ++e;
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {  // the first row's own columns, then the second row's
+          int n = int((t ? hb : ha) & 0xffu);
+          for (; n >= 4; n -= 4, e += 2) {
+            const float4 e0 = e[0], e1 = e[1];
+            float4 xa, xb, xc, xd;
+            tmem_ld4(__float_as_uint(e0.x), xa);
+            tmem_ld4(__float_as_uint(e0.z), xb);
+            tmem_ld4(__float_as_uint(e1.x), xc);
+            tmem_ld4(__float_as_uint(e1.z), xd);
+            tmem_wait_ld(xa, xb, xc, xd);
+            fma4(acc[2 * i + t], e0.y, xa);
+            fma4(acc[2 * i + t], e0.w, xb);
+            fma4(acc[2 * i + t], e1.y, xc);
+            fma4(acc[2 * i + t], e1.w, xd);
+          }
+          if (n) {
+            const float4 e0 = e[0];
+            float4 xa, xb;
+            tmem_ld4(__float_as_uint(e0.x), xa);
+            tmem_ld4(__float_as_uint(e0.z), xb);
+            tmem_wait_ld(xa, xb);
+            fma4(acc[2 * i + t], e0.y, xa);
+            fma4(acc[2 * i + t], e0.w, xb);
+            ++e;
+          }
+        }
+      }
+    } else
 #pragma unroll
     for (int r = 0; r < RW; ++r) {
       const uint32_t hh = hn;
@@ -1344,7 +1425,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
   }
 }
 
-template <bool MULTI = false, bool SPLIT = false, bool RUNS = true, int RW = tmem_rows(4)>
+template <bool MULTI = false, bool SPLIT = false, bool RUNS = true, int RW = tmem_rows(4), bool PAIRS = false>
 __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     spmm_tmemr_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI || SPLIT> p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1441,7 +1522,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     }
   } else {
     if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0 (addresses are absolute)
-    tmemr_consume<MULTI, SPLIT, RUNS, RW>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
+    tmemr_consume<MULTI, SPLIT, RUNS, RW, PAIRS>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -1533,7 +1614,8 @@ static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, c
 static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                const YOut& yo, cudaStream_t stream, int KS = 1, cudaMemPool_t pool = nullptr) {
   const Plan& pl = h->plan;
-  const bool rep = pl.kernel == 4;  // replicated-quarter kernel (V = 4, TN = 128); else V = 8 (TN = 1024)
+  const bool rep = pl.kernel == 4 || pl.kernel == 6;  // replicated-quarter kernels (V = 4, TN = 128); else V = 8
+  const bool prs = pl.kernel == 6;                      // Algorithm 1 row pairs
   const int V = tmem_v(pl.kernel), TN = tmem_tn(pl.kernel);
   const int64_t ntiles = (N + TN - 1) / TN;
   const int64_t nblocks = ntiles * pl.num_row_blocks;
@@ -1613,7 +1695,8 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     q.kws = kws;
     q.M = pl.M;
     const dim3 g2{grid, unsigned(KS)};
-    if (rep) spmm_tmemr_kernel<false, true><<<g2, threads, smem, stream>>>(tmap, q);
+    if (prs) spmm_tmemr_kernel<false, true, false, tmem_rows(4), true><<<g2, threads, smem, stream>>>(tmap, q);
+    else if (rep) spmm_tmemr_kernel<false, true><<<g2, threads, smem, stream>>>(tmap, q);
     else spmm_tmem_kernel<8, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
     cudaError_t le = cudaGetLastError();
     if (le == cudaSuccess) {
@@ -1625,7 +1708,10 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     if (le != cudaSuccess) return fail(SDNN_ERR_CUDA, std::string("TMEM split-K: ") + cudaGetErrorString(le));
     return SDNN_OK;
   }
-  if (rep && multi) spmm_tmemr_kernel<true, false><<<grid, threads, smem, stream>>>(tmap, p);
+  if (prs && multi) spmm_tmemr_kernel<true, false, false, tmem_rows(4), true><<<grid, threads, smem, stream>>>(tmap, p);
+  else if (prs)
+    spmm_tmemr_kernel<false, false, false, tmem_rows(4), true><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
+  else if (rep && multi) spmm_tmemr_kernel<true, false><<<grid, threads, smem, stream>>>(tmap, p);
   else if (rep && h->tmem_runs) spmm_tmemr_kernel<false, false, true><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
   else if (rep) spmm_tmemr_kernel<false, false, false><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
   else if (multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
@@ -1837,7 +1923,8 @@ static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, cons
   if (sdnn_handle_s* nw = narrow_pick(h, N)) return launch(nw, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
-  if ((pl.kernel == 4 || pl.kernel == 5) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))
+  if ((pl.kernel == 4 || pl.kernel == 5 || pl.kernel == 6) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+      y_aligned16(yo))
     return launch_tmem(h, X, N, bias, act, yo, stream);
   return launch_row(h, X, N, bias, act, yo, stream, -1);
 }
@@ -1850,7 +1937,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
   int V = row_tile_v_small(pl, N, h->sms);
   if (KS > 1 && pl.kernel == 1 && N > 64 && row_tile_v(pl, N) == 4) V = 4;  // split-K calls: see splitk_for
-  if (pl.kernel == 4 || pl.kernel == 5) V = 4;  // TMEM plan, ragged / unaligned call: generic kernel
+  if (pl.kernel == 4 || pl.kernel == 5 || pl.kernel == 6) V = 4;  // TMEM plan, ragged / unaligned call: generic kernel
   const int TN = 32 * V;
   const int64_t ntiles = (N + TN - 1) / TN;
   const int64_t nblocks = ntiles * pl.num_row_blocks;
@@ -1953,6 +2040,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
     else if (pl.kernel == 2) spmm_generic_kernel<2, 16, 4, 4><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 4) spmm_generic_kernel<4, tmem_rows(4), 4><<<grid, block, smem, stream>>>(p);
     else if (pl.kernel == 5) spmm_generic_kernel<5, tmem_rows(8), 4><<<grid, block, smem, stream>>>(p);
+    else if (pl.kernel == 6) spmm_generic_kernel<6, tmem_rows(4), 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 8) spmm_generic_kernel<1, 8, 8><<<grid, block, smem, stream>>>(p);
     else if (rw == 8 && V == 4) spmm_generic_kernel<1, 8, 4><<<grid, block, smem, stream>>>(p);
     else if (rw == 8) spmm_generic_kernel<1, 8, 2><<<grid, block, smem, stream>>>(p);
@@ -2025,6 +2113,18 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_generic_kernel<5, tmem_rows(8), 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_generic_kernel<6, tmem_rows(4), 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, false, tmem_rows(4), true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<true, false, false, tmem_rows(4), true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, true, false, tmem_rows(4), true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmem_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
@@ -2567,7 +2667,7 @@ sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const flo
   if (sdnn_handle_s* nw = narrow_pick(h, N)) return sdnn_spmm_kernel(nw, N, X, Y, kernel);
   const int k = h->plan.kernel;
   const bool tma = N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo);
-  *kernel = (k == 4 || k == 5) ? (N % 128 == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
+  *kernel = (k == 4 || k == 5 || k == 6) ? (N % 128 == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
   return SDNN_OK;
 }
 
@@ -2645,14 +2745,15 @@ sdnn_status plan_with_meta(const sdnn_handle_s* h, Plan& out) {
 }
 // Structural checks of a deserialized plan before it is uploaded and launched.
 bool plan_sane(const Plan& p, uint32_t role) {
-  if (p.M < 1 || p.K < 1 || p.kernel < 1 || p.kernel > 5 || p.kernel == 3) return false;
+  if (p.M < 1 || p.K < 1 || p.kernel < 1 || p.kernel > 6 || p.kernel == 3) return false;
   // plan kind per role: 0 main (row / group / TMEM), 1 TMEM alternative, 2-3 narrow row plans
-  if ((role == 1 && p.kernel != 4 && p.kernel != 5) || (role >= 2 && p.kernel != 1)) return false;
+  if ((role == 1 && p.kernel != 4 && p.kernel != 5 && p.kernel != 6) || (role >= 2 && p.kernel != 1)) return false;
   if (p.perm.size() != size_t(p.M) || p.num_row_blocks < 1 || p.num_chunks < 1 || p.k_chunk < 1) return false;
   if (p.num_chunks != (p.K + p.k_chunk - 1) / p.k_chunk) return false;
   // panel geometry the kernels are compiled for
   if (p.num_panels != int64_t(p.num_row_blocks) * p.cta_panels) return false;
-  if (p.kernel == 4 && (p.panel_rows != tmem_rows(4) || p.cta_panels != kTmemRWarps || p.k_chunk != tmem_kc(4)))
+  if ((p.kernel == 4 || p.kernel == 6) &&
+      (p.panel_rows != tmem_rows(4) || p.cta_panels != kTmemRWarps || p.k_chunk != tmem_kc(4)))
     return false;
   if (p.kernel == 5 && (p.panel_rows != tmem_rows(8) || p.cta_panels != kTmemPanels || p.k_chunk != tmem_kc(8)))
     return false;
@@ -2664,7 +2765,7 @@ bool plan_sane(const Plan& p, uint32_t role) {
   if (p.max_block_bytes < 16) return false;
   // the stage ring the launch sizes from max_block_bytes must fit shared memory
   const int mstage = int(align_up(p.max_block_bytes, 128));
-  if (p.kernel == 4 && tmemr_smem_bytes(mstage) > size_t(kSmemBudget) + 1024) return false;
+  if ((p.kernel == 4 || p.kernel == 6) && tmemr_smem_bytes(mstage) > size_t(kSmemBudget) + 1024) return false;
   if (p.kernel == 5 && tmem_smem_bytes(mstage) > size_t(kSmemBudget) + 1024) return false;
   if ((p.kernel == 1 || p.kernel == 2) && int64_t(p.k_chunk) * kMaxTN * 4 + mstage > kSmemBudget) return false;
   for (size_t i = 1; i < p.blk_off.size(); ++i)
@@ -2681,6 +2782,33 @@ bool plan_sane(const Plan& p, uint32_t role) {
       return false;
   for (int32_t r : p.row_orig)
     if (r >= p.M || (r <= -2 && size_t(-2 - int64_t(r)) >= p.piece_row.size())) return false;
+  // kernel 6 (row pairs): per slot pair, the shared (16-byte) entries and both own lists inside the
+  // block, contiguous, TMEM columns with the warp's lane base
+  if (p.kernel == 6) {
+    const int64_t rcta = int64_t(p.panel_rows) * p.cta_panels;
+    const int64_t hdr = align_up(rcta * 4, 16);
+    for (int64_t b = 0; b + 1 < int64_t(p.blk_off.size()); ++b) {
+      const int64_t bytes = p.blk_off[b + 1] - p.blk_off[b];
+      if (bytes < hdr) return false;
+      const uint8_t* blk = p.meta.data() + p.blk_off[b];
+      const int64_t nent = (bytes - hdr) / 8;
+      for (int64_t sl = 0; sl < rcta; sl += 2) {
+        uint32_t ha, hb;
+        std::memcpy(&ha, blk + sl * 4, 4);
+        std::memcpy(&hb, blk + sl * 4 + 4, 4);
+        const int64_t start = ha >> 16, ns = (ha >> 8) & 0xffu, na = ha & 0xffu, b0 = hb >> 16, nb = hb & 0xffu;
+        if (start % 2 || na % 2 || nb % 2 || b0 != start + 2 * ns + na || b0 + nb > nent) return false;
+        const uint32_t lb = uint32_t(32 * ((sl / p.panel_rows) & 3)) << 16;
+        for (int64_t e = start; e < b0 + nb; ++e) {
+          if (e < start + 2 * ns && (e - start) % 2) continue;  // second half of a shared entry {w_b, 0}
+          uint32_t c;
+          std::memcpy(&c, blk + hdr + e * 8, 4);
+          if ((c & ~0xffffu) != lb || (c & 0xffffu) >= 512u || (c & 0xffu) % 4u) return false;
+        }
+      }
+    }
+    return true;
+  }
   // row-format metadata (row / TMEM kernels): every slot's segment inside its block, columns inside
   // the chunk (the kernels index shared / tensor memory with them)
   if (p.kernel != 2) {
@@ -2815,7 +2943,7 @@ sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* 
   if (st != SDNN_OK) return st;
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   std::vector<sdnn_handle_s::Tuned> cands{{-1, 0}};  // the built-in rules first (ties keep them)
-  const bool has_tmem = (h->alt || h->plan.kernel == 4 || h->plan.kernel == 5) && N % 128 == 0;
+  const bool has_tmem = (h->alt || h->plan.kernel == 4 || h->plan.kernel == 5 || h->plan.kernel == 6) && N % 128 == 0;
   const bool row_ok = h->plan.kernel == 1 || h->plan.kernel == 2;
   // TMEM split-K slices are cut at even chunks and keep ≥ 2 chunk pairs each (launch_tmem caps KS):
   // candidates beyond that cap would repeat a smaller KS

@@ -46,6 +46,7 @@ CASES = [  # (problem, N, handle options)
     ("c1", 128, {}), ("c1", 100, {}), ("c1", 512, dict(kernel="tmem")), ("c1", 1024, dict(kernel="tmem8")),
     ("c1", 96, dict(kernel="tmem")), ("c1", 256, dict(kernel="group")), ("c1", 1000, dict(kernel="row", cta_panels=1)),
     ("lognormal", 64, dict(kernel="row")), ("splitk", 96, {}), ("block4", 512, dict(kernel="tmem")),
+    ("c1", 512, dict(kernel="tmemp")), ("c1", 96, dict(kernel="tmemp")),
     ("narrow", 128, {}), ("narrow", 68, {}),
 ]
 

@@ -60,7 +60,7 @@ def test_worked_example(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ BASELINE configs c1-c4 (full size)
-@pytest.mark.parametrize("kernel", ["auto", "row", "group1", "group2", "group4", "codegen", "tmem", "tmem8"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "group1", "group2", "group4", "codegen", "tmem", "tmem8", "tmemp"])
 @pytest.mark.parametrize("key", [k for k in synth.CONFIGS if k != "c5"])
 def test_config_parity(sdnn, oracle_mod, key, kernel):
     p = synth.config_problem(key)
@@ -75,7 +75,7 @@ def test_c2_no_act(sdnn, oracle_mod):
 
 
 # ------------------------------------------------------------------ desk grid
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8", "tmemp"])
 @pytest.mark.parametrize("g", list(synth.desk_grid()), ids=lambda g: f"{g['name']}_s{g['seed']}")
 def test_desk_grid(sdnn, oracle_mod, g, kernel):
     p = synth.make_problem(g["name"], g["M"], g["K"], g["N"], g["sparsity"], seed=g["seed"])
@@ -83,7 +83,7 @@ def test_desk_grid(sdnn, oracle_mod, g, kernel):
 
 
 # ------------------------------------------------------------------ c5 at full size, launch config of bench.py
-@pytest.mark.parametrize("kernel", ["auto", "row", "codegen", "tmem", "tmem8"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "codegen", "tmem", "tmem8", "tmemp"])
 def test_c5_full_size_sampled_columns(sdnn, oracle_mod, kernel):
     p = synth.config_problem("c5")
     h = sdnn.Handle.from_problem(p, kernel=kernel)
@@ -103,14 +103,14 @@ def test_c5_full_size_sampled_columns(sdnn, oracle_mod, kernel):
 
 
 # ------------------------------------------------------------------ edge cases
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8", "tmemp"])
 @pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 127, 128, 129, 256, 300, 384, 1000, 1024])
 def test_ragged_n(sdnn, oracle_mod, N, kernel):
     p = synth.make_problem("ragged", 200, 150, N, 0.9, mask="lognormal", seed=N)
     check(sdnn, oracle_mod, p, kernel=kernel)
 
 
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8", "tmemp"])
 def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     p = synth.make_problem("unal", 100, 90, 64, 0.8, seed=1)
     X = p.x()
@@ -125,7 +125,7 @@ def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     assert_parity(Yv.cpu().numpy(), Yo, S, "unaligned")
 
 
-@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8"])
+@pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8", "tmemp"])
 @pytest.mark.parametrize("M,K,N,dens", [(1, 1, 4, 1.0), (1, 500, 8, 0.3), (500, 1, 8, 0.5), (37, 65, 12, 1.0),
                                         (129, 257, 20, 0.0), (64, 64, 64, 1.0), (2100, 70, 40, 0.05),
                                         (1, 500, 128, 0.3), (500, 1, 256, 0.5), (129, 257, 384, 0.0),
@@ -415,7 +415,7 @@ except ImportError:  # pragma: no cover
     given = None
 
 if given is not None:
-    @pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "tmem8"])
+    @pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "tmem8", "tmemp"])
     @settings(max_examples=12, deadline=None, suppress_health_check=list(HealthCheck))
     @given(M=st.integers(1, 300), K=st.integers(1, 300), nq=st.integers(1, 6), ragged=st.booleans(),
            dens=st.sampled_from([0.0, 0.02, 0.1, 0.3, 1.0]), seed=st.integers(0, 2**31 - 1),
@@ -460,7 +460,7 @@ if given is not None:
         check(sdnn, oracle_mod, p, X=X, act=act, bias=b if bias else None)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "row", "tmem"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "tmemp"])
 def test_large_k_and_large_m(sdnn, oracle_mod, kernel):
     """K = 40 000 (625 TMEM chunks) and M = 20 000 (334 TMEM row blocks) at small N."""
     for M, K, N, dens in [(96, 40000, 256, 0.01), (20000, 64, 128, 0.05)]:
@@ -469,7 +469,7 @@ def test_large_k_and_large_m(sdnn, oracle_mod, kernel):
 
 
 # ------------------------------------------------------------------ fused all-gather form (sdnn_spmm_multi)
-@pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "tmem8"])
+@pytest.mark.parametrize("kernel", ["auto", "row", "tmem", "tmem8", "tmemp"])
 @pytest.mark.parametrize("key,N", [("c3_512x512", 1024), ("c3_512x512", 1000), ("c2_768x768", 512), ("c1", 128)])
 def test_spmm_multi_destinations(sdnn, key, N, kernel):
     """Y written to 3 buffers of leading dimension ldy at column offset col0 (the all-gather layout a

@@ -24,6 +24,7 @@ def sdnn():
     ("c3_512x512", dict(kernel="tmem"), (6272, 96)),       # explicit TMEM (+ its ragged fallback)
     ("c1", dict(kernel="group"), (128,)),
     ("c1", dict(kernel="tmem8", permuted_output=True), (1024,)),
+    ("c3_512x512", dict(kernel="tmemp"), (6272, 100)),          # Algorithm 1 row pairs (+ ragged fallback)
 ])
 def test_roundtrip_bitwise(sdnn, key, opts, Ns):
     p = synth.make_problem("ser_nw", 2048, 1024, 2048, 0.9) if key == "narrow" else synth.config_problem(key, N=max(Ns))

@@ -12,6 +12,8 @@ def decode(p, plan):
     info = plan.info()
     if info["kernel"] == 2:
         return decode_group(p, plan)
+    if info["kernel"] == 6:
+        return decode_pairs(p, plan)
     row_orig, blk_off, meta = plan.export()
     rw, wc, kc, nch, nrb = (info[k] for k in ("panel_rows", "cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
     V = {4: 4, 5: 8}.get(info["kernel"], 0)
@@ -91,6 +93,65 @@ def decode(p, plan):
     return info, row_orig, triples
 
 
+def decode_pairs(p, plan):
+    """Kernel 6 (TMEM, Algorithm 1 row pairs): per slot pair, shared columns {col, w_a, w_b, 0}, then
+    each row's own columns, each list ascending, with the warp's TMEM lane base in every column."""
+    info = plan.info()
+    row_orig, blk_off, meta = plan.export()
+    rw, wc, kc, nch, nrb = (info[k] for k in ("panel_rows", "cta_panels", "k_chunk", "num_chunks", "num_row_blocks"))
+    assert (rw, wc, kc) == (10, 24, 64)
+    rcta = rw * wc
+    hdr_bytes = (rcta * 4 + 15) // 16 * 16
+    assert blk_off[0] == 0 and blk_off[-1] == meta.size and np.all(blk_off % 16 == 0)
+    triples, shared = [], 0
+    perm = sdnn.permutation(p.row_ptr, p.col_idx, p.M, p.K) if info["permuted"] else np.arange(p.M)
+    decode_pairs.pos = np.empty(p.M, int)
+    decode_pairs.pos[perm] = np.arange(p.M)
+    for b in range(nrb):
+        for j in range(nch):
+            blk = meta[blk_off[b * nch + j]:blk_off[b * nch + j + 1]]
+            hdr = blk[:rcta * 4].view(np.uint32)
+            ent = blk[hdr_bytes:]
+
+            def entry(i):
+                cl = int(ent[i * 8:i * 8 + 4].view(np.uint32)[0])
+                lane_base = (32 * ((s // rw) % 4)) << 16
+                assert cl & ~0xFFFF == lane_base
+                cl &= 0xFFFF
+                half = 256 * (j & 1)
+                assert (cl - half) % 4 == 0 and 0 <= cl - half < 256
+                return (cl - half) // 4, ent[i * 8 + 4:i * 8 + 8].view(np.float32)[0]
+            for s in range(0, rcta, 2):
+                ha, hb = int(hdr[s]), int(hdr[s + 1])
+                start, ns, na, b0, nb = ha >> 16, (ha >> 8) & 0xFF, ha & 0xFF, hb >> 16, hb & 0xFF
+                assert start % 2 == 0 and na % 2 == 0 and nb % 2 == 0 and b0 == start + 2 * ns + na
+                ra, rb = int(row_orig[b * rcta + s]), int(row_orig[b * rcta + s + 1])
+                if ra >= 0 and rb >= 0:  # a pair = two consecutive Algorithm 1 positions (2i, 2i + 1)
+                    assert decode_pairs.pos[rb] == decode_pairs.pos[ra] + 1 and decode_pairs.pos[ra] % 2 == 0
+                cols_a, cols_b = [], []
+                for i in range(ns):
+                    c, wa = entry(start + 2 * i)
+                    wb = ent[(start + 2 * i + 1) * 8:(start + 2 * i + 1) * 8 + 4].view(np.float32)[0]
+                    assert ra >= 0 and rb >= 0
+                    triples += [(ra, j * kc + c, wa), (rb, j * kc + c, wb)]
+                    cols_a.append(c), cols_b.append(c)
+                    shared += 1
+                for r, n0, n in ((ra, start + 2 * ns, na), (rb, b0, nb)):
+                    own = []
+                    for i in range(n):
+                        c, w = entry(n0 + i)
+                        if w == 0:
+                            assert c == 0  # padding entry (column 0 of the half)
+                            continue
+                        assert r >= 0
+                        triples.append((r, j * kc + c, w))
+                        own.append(c)
+                    assert own == sorted(own)
+                assert cols_a == sorted(cols_a)
+    decode_pairs.shared = shared
+    return info, row_orig, triples
+
+
 def decode_group(p, plan):
     info = plan.info()
     row_orig, blk_off, meta = plan.export()
@@ -167,6 +228,8 @@ def test_c_alg1_equals_bruteforce_random(oracle_mod, seed):
     ("c4_512x2048_s80", dict(kernel="group", group_sb=4)),
     ("c1", dict(kernel="tmem")), ("c2_768x3072", dict(kernel="tmem")), ("c4_2048x512_s95", dict(kernel="tmem", permute=False)),
     ("c1", dict(kernel="tmem8")), ("c2_768x768", dict(kernel="tmem8")), ("c4_512x2048_s80", dict(kernel="tmem8")),
+    ("c1", dict(kernel="tmemp")), ("c2_768x3072", dict(kernel="tmemp")), ("c4_2048x512_s80", dict(kernel="tmemp")),
+    ("c3_512x512", dict(kernel="tmemp", permute=False)),
 ])
 def test_packing_invariants(oracle_mod, key, opts):
     p = synth.config_problem(key, N=4)
@@ -240,7 +303,7 @@ def test_degenerate_shapes():
         v = rng.standard_normal(ci.size).astype(np.float32)
         p = synth.Problem("d", M, K, 1, 0, "x", rp, ci, v, None, 0, 0)
         v[v == 0] = 1.0  # decode treats 0.0 weights as padding
-        for kernel, sb in (("row", 0), ("group", 1), ("group", 2), ("group", 4), ("tmem", 0), ("tmem8", 0)):
+        for kernel, sb in (("row", 0), ("group", 1), ("group", 2), ("group", 4), ("tmem", 0), ("tmem8", 0), ("tmemp", 0)):
             plan = sdnn.Plan(rp, ci, v, M, K, kernel=kernel, group_sb=sb)
             _, _, triples = decode(p, plan)
             assert sorted(triples) == csr_triples(p)
