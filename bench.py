@@ -212,7 +212,7 @@ def plan_geometry(p, info: dict, kid: int, kernel: str) -> dict:
 def tmem_operand_bytes(p, N: int, kc: int = 64) -> int:
     """TMEM → register bytes one launch of the TMEM kernel reads: every (row, K chunk) segment is
     padded to whole pairs of entries, and each entry is one 512-byte tcgen05.ld.32x32b.x4 per
-    128-column N tile (4 bytes per entry per column of N)."""
+    128-column N tile (4 bytes per entry per column of N; c5 encodes no 1×4 runs)."""
     rows = np.repeat(np.arange(p.M), np.diff(p.row_ptr))
     cnt = np.bincount(rows * ((p.K + kc - 1) // kc) + p.col_idx // kc, minlength=p.M * ((p.K + kc - 1) // kc))
     padded = int(((cnt + 1) // 2 * 2).sum())
