@@ -128,6 +128,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Timing perturbation for the pipeline-protocol tests (SDNN_JITTER=1 → KParams::dbg bit 8): a
+// pseudo-random 0-2 µs sleep at the mbarrier hand-off points of the TMA / TMEM pipelines, so that
+// producers, issuers and consumers interleave in orders the free-running kernel rarely produces; the
+// results must stay bitwise identical (tests/test_gpu_jitter.py).  One predictable branch otherwise.
+__device__ __forceinline__ void jitter(int32_t dbg, uint32_t salt) {
+  if (dbg & 256) {
+    uint32_t h = (salt ^ (blockIdx.x * 0x9E3779B9u) ^ (threadIdx.x >> 5) * 0x85EBCA6Bu) * 2654435761u;
+    h ^= h >> 15;
+    __nanosleep(h & 2047u);
+  }
+}
 // Same, but each try_wait may suspend the thread until the phase completes (time hint in ns), so a
 // warp that waits long (a filler ahead of the consumers) does not spin on issue slots.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -494,6 +505,7 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
       const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
       for (int j = j0; j < j1; ++j) {
         const int s = (j - j0) % S;
+        jitter(p.dbg, uint32_t(j));
         if (j - j0 >= S) mbar_wait(&empty[s], (((j - j0) / S) - 1) & 1);
         const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
         mbar_expect_tx(&full[s], uint32_t(p.x_stage_bytes) + mbytes);
@@ -518,6 +530,7 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
       consume_group<V, SB>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane);
     else
       consume_chunk<RW, V>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane, p.hdr_bytes);
+    jitter(p.dbg, uint32_t(j) * 7u + 1u);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -1498,6 +1511,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
         for (int j = 0; j < MS && j < jr.y; ++j) load_meta(j);
       for (int j = 0; j < jr.y; ++j) {
         const int h = j & 1, s = q + 4 * h;
+        jitter(p.dbg, uint32_t(j) * 5u + 3u);
         if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
           mbar_wait_sleep(&tfree[h], ((j >> 1) - 1) & 1);
           tc_fence_after();
@@ -1507,6 +1521,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
           load_meta(j);
         }
         mbar_wait(&slot_full[s], (j >> 1) & 1);
+        jitter(p.dbg, uint32_t(j) * 11u + 4u);
         const uint32_t src = smem_u32(xring + size_t(s) * kTmemRPieceBytes);
 #pragma unroll
         for (int kk = 0; kk < PK; ++kk)
@@ -1611,6 +1626,15 @@ static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, c
   return SDNN_OK;
 }
 
+// SDNN_JITTER=1: timing perturbation of the pipelines (tests only; see jitter())
+static int32_t jitter_flag() {
+  static const int32_t f = [] {
+    const char* e = getenv("SDNN_JITTER");
+    return (e && atoi(e) > 0) ? 256 : 0;
+  }();
+  return f;
+}
+
 static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                const YOut& yo, cudaStream_t stream, int KS = 1, cudaMemPool_t pool = nullptr) {
   const Plan& pl = h->plan;
@@ -1648,7 +1672,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
       const char* e = getenv("SDNN_DEBUG_TMEM");
       return e ? atoi(e) : 0;
     }();
-    p.dbg = dbg;
+    p.dbg = dbg | jitter_flag();
   }
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -1951,6 +1975,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   p.bias = bias;
   p.yo = yo;
   p.Y = y_plain(yo, N) ? yo.y[0] : nullptr;
+  p.dbg = jitter_flag();
   p.N = N;
   p.K = pl.K;
   p.nch = pl.num_chunks;
