@@ -111,6 +111,10 @@ constexpr int kTmemPieces = 4;        // kernel 5: smem ring depth (32 KB TMA pi
 constexpr int kTmemRPieces = 8;       // kernel 4: smem ring depth (8 KB TMA pieces: 16 K rows × 128 columns)
 inline int tmem_v(int kernel) { return kernel == 5 ? 8 : 4; }
 inline int tmem_tn(int kernel) { return kernel == 5 ? 1024 : 128; }  // N tile of a TMEM plan
+// N granularity of a TMEM plan's fast path: kernels 4 / 6 read X through a 2-D tensor map (any
+// N % 4 == 0: the last tile's columns past N are zero-filled by TMA and not stored); kernel 5's 3-D
+// map needs whole 128-column blocks
+inline int tmem_n_align(int kernel) { return kernel == 5 ? 128 : 4; }
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 

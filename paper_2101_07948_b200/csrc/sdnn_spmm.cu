@@ -1750,7 +1750,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
 // CTAs (round 2, TMEM-R kernel: 3072×768 at N = 512, 52 CTAs, 38.1 → 32.9 µs against the row plan,
 // profiles/r02_tune_rules.log; round 1's kernel needed half a wave).
 static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const YOut& yo) {
-  return a && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo) &&
+  return a && N % tmem_n_align(a->plan.kernel) == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo) &&
          3 * int64_t(a->plan.num_row_blocks) * ((N + tmem_tn(a->plan.kernel) - 1) / tmem_tn(a->plan.kernel)) >= a->sms;
 }
 
@@ -1825,7 +1825,7 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   const sdnn_handle_s* a = h->alt;
   if (!a || h->plan.no_split_k || !h->ws_pool) return 0;
   if (!y_plain(yo, N)) return 0;
-  if (!(N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))) return 0;
+  if (!(N % tmem_n_align(a->plan.kernel) == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo))) return 0;
   static const int env = [] {
     const char* e = getenv("SDNN_TMEM_SPLIT_K");
     return e ? atoi(e) : -1;
@@ -1947,7 +1947,8 @@ static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, cons
   if (sdnn_handle_s* nw = narrow_pick(h, N)) return launch(nw, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
-  if ((pl.kernel == 4 || pl.kernel == 5 || pl.kernel == 6) && N % 128 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+  if ((pl.kernel == 4 || pl.kernel == 5 || pl.kernel == 6) && N % tmem_n_align(pl.kernel) == 0 &&
+      reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
       y_aligned16(yo))
     return launch_tmem(h, X, N, bias, act, yo, stream);
   return launch_row(h, X, N, bias, act, yo, stream, -1);
@@ -2692,7 +2693,7 @@ sdnn_status sdnn_spmm_kernel(sdnn_handle h, int64_t N, const float* X, const flo
   if (sdnn_handle_s* nw = narrow_pick(h, N)) return sdnn_spmm_kernel(nw, N, X, Y, kernel);
   const int k = h->plan.kernel;
   const bool tma = N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 && y_aligned16(yo);
-  *kernel = (k == 4 || k == 5 || k == 6) ? (N % 128 == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
+  *kernel = (k == 4 || k == 5 || k == 6) ? (N % tmem_n_align(k) == 0 && tma ? k : -k) : (k == 3 || tma) ? k : -k;
   return SDNN_OK;
 }
 
@@ -2968,7 +2969,8 @@ sdnn_status sdnn_tune(sdnn_handle h, const float* X, int64_t N, float* Y, void* 
   if (st != SDNN_OK) return st;
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   std::vector<sdnn_handle_s::Tuned> cands{{-1, 0}};  // the built-in rules first (ties keep them)
-  const bool has_tmem = (h->alt || h->plan.kernel == 4 || h->plan.kernel == 5 || h->plan.kernel == 6) && N % 128 == 0;
+  const bool has_tmem = (h->alt || h->plan.kernel == 4 || h->plan.kernel == 5 || h->plan.kernel == 6) &&
+                        N % tmem_n_align(h->alt ? h->alt->plan.kernel : h->plan.kernel) == 0;
   const bool row_ok = h->plan.kernel == 1 || h->plan.kernel == 2;
   // TMEM split-K slices are cut at even chunks and keep ≥ 2 chunk pairs each (launch_tmem caps KS):
   // candidates beyond that cap would repeat a smaller KS

@@ -110,6 +110,24 @@ def test_ragged_n(sdnn, oracle_mod, N, kernel):
     check(sdnn, oracle_mod, p, kernel=kernel)
 
 
+@pytest.mark.parametrize("kernel", ["tmem", "tmemp"])
+@pytest.mark.parametrize("N", [4, 100, 132, 1000, 6276])
+def test_tmem_fast_path_partial_tiles(sdnn, oracle_mod, N, kernel):
+    """TMEM-R kernels (2-D tensor map) take any N % 4 == 0 on the fast path: the last 128-column
+    tile's columns past N are zero-filled by TMA and not stored — oracle parity, and bitwise equal to
+    the same columns of a call with N rounded up to whole tiles (column independence)."""
+    p = synth.make_problem("ptile", 600, 700, N, 0.9, seed=N)
+    h = sdnn.Handle.from_problem(p, kernel=kernel)
+    assert h.kernel_for(N, 256, 256) == (6 if kernel == "tmemp" else 4)
+    check(sdnn, oracle_mod, p, kernel=kernel)
+    Nr = (N + 127) // 128 * 128
+    X = np.zeros((p.K, Nr), np.float32)
+    X[:, :N] = p.x()
+    Y, _ = run_gpu(sdnn, p, np.ascontiguousarray(X[:, :N]), p.bias, 1, handle=h)
+    Yr, _ = run_gpu(sdnn, p, X, p.bias, 1, handle=h)
+    np.testing.assert_array_equal(Y, Yr[:, :N])
+
+
 @pytest.mark.parametrize("kernel", ["row", "group", "codegen", "tmem", "tmem8", "tmemp"])
 def test_unaligned_pointers(sdnn, oracle_mod, kernel):
     p = synth.make_problem("unal", 100, 90, 64, 0.8, seed=1)
