@@ -1290,19 +1290,23 @@ constexpr size_t tmemr_smem_bytes(int m_stage_bytes) {
   return size_t(kTmemRPieces) * kTmemRPieceBytes + size_t(kTmemRMetaSlots) * m_stage_bytes + 32 * 8 + 16;
 }
 
+// g0: global index of this item's first chunk in the CTA's chunk stream (persistent CTAs run several
+// (row block, N tile) items through one pipeline; 0 otherwise) — it fixes the TMEM half, the
+// metadata slot and the mbarrier phases of every chunk.
 template <bool MULTI, bool SPLIT, bool RUNS, int RW, bool PAIRS = false>
 __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& p, uint8_t* mring, uint64_t* mfull,
                                               uint64_t* mempty, uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0,
-                                              int warp, int lane) {
+                                              int warp, int lane, int g0 = 0) {
   constexpr int MS = kTmemRMetaSlots;
   float2 acc[RW][2];
 #pragma unroll
   for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
   const int nrel = tmem_chunks<SPLIT>(p.nch).y;
   for (int j = 0; j < nrel; ++j) {
-    const int h = j & 1, m = j % MS;
-    mbar_wait(&mfull[m], (j / MS) & 1);
-    mbar_wait(&tfull[h], (j >> 1) & 1);
+    const int g = g0 + j;
+    const int h = g & 1, m = g % MS;
+    mbar_wait(&mfull[m], (g / MS) & 1);
+    mbar_wait(&tfull[h], (g >> 1) & 1);
     tc_fence_after();
     const uint8_t* ms = mring + size_t(m) * p.m_stage_bytes;
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(ms) + warp * RW;
@@ -1438,7 +1442,12 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
   }
 }
 
-template <bool MULTI = false, bool SPLIT = false, bool RUNS = true, int RW = tmem_rows(4), bool PAIRS = false>
+// PERSIST: one CTA per SM runs the items (row block, N tile) blockIdx.x, blockIdx.x + gridDim.x, …
+// through one continuous chunk pipeline — the issuers fetch the next item's chunks while the
+// consumers finish the current item and store its Y — for short K ranges, where a CTA's pipeline
+// start-up and drain are a large part of its life.
+template <bool MULTI = false, bool SPLIT = false, bool RUNS = true, int RW = tmem_rows(4), bool PAIRS = false,
+          bool PERSIST = false>
 __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     spmm_tmemr_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI || SPLIT> p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1490,26 +1499,47 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     const int q = warp & 3;
     const int2 jr = tmem_chunks<SPLIT>(p.nch);
     if (lane == 0) {
-      const int64_t* off = p.blk_off + int64_t(rb) * p.nch + jr.x;
-      auto load_piece = [&](int j) {
-        const int s = q + 4 * (j & 1);
+      // chunk g of this CTA's stream → (row block, N tile, chunk); one item unless PERSIST
+      const int items = PERSIST ? (p.nrb * int((p.N + 127) / 128) - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x) : 1;
+      const int total = PERSIST ? items * p.nch : jr.y;
+      auto where = [&](int g, int& rb_, int64_t& n0_, int& j_) {
+        if constexpr (PERSIST) {
+          const int u = g / p.nch, id = int(blockIdx.x) + u * int(gridDim.x);
+          j_ = g - u * p.nch;
+          rb_ = id % p.nrb;
+          n0_ = int64_t(id / p.nrb) * 128;
+        } else {
+          j_ = jr.x + g;
+          rb_ = rb;
+          n0_ = n0;
+        }
+      };
+      auto load_piece = [&](int g) {
+        const int s = q + 4 * (g & 1);
         if (p.dbg & 1) {
           mbar_arrive(&slot_full[s]);
           return;
         }
+        int rb_, j_;
+        int64_t n0_;
+        where(g, rb_, n0_, j_);
         mbar_expect_tx(&slot_full[s], kTmemRPieceBytes);
-        tma_load_2d(xring + size_t(s) * kTmemRPieceBytes, &tmap, int32_t(n0), (jr.x + j) * 64 + q * PK, &slot_full[s]);
+        tma_load_2d(xring + size_t(s) * kTmemRPieceBytes, &tmap, int32_t(n0_), j_ * 64 + q * PK, &slot_full[s]);
       };
-      auto load_meta = [&](int j) {
-        const int m = j % MS;
-        const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
+      auto load_meta = [&](int g) {
+        const int m = g % MS;
+        int rb_, j_;
+        int64_t n0_;
+        where(g, rb_, n0_, j_);
+        const int64_t* off = p.blk_off + int64_t(rb_) * p.nch + j_;
+        const uint32_t mbytes = uint32_t(off[1] - off[0]);
         mbar_expect_tx(&mfull[m], mbytes);
-        bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[j], mbytes, &mfull[m]);
+        bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[0], mbytes, &mfull[m]);
       };
-      for (int j = 0; j < 2 && j < jr.y; ++j) load_piece(j);
+      for (int j = 0; j < 2 && j < total; ++j) load_piece(j);
       if (q == 0)
-        for (int j = 0; j < MS && j < jr.y; ++j) load_meta(j);
-      for (int j = 0; j < jr.y; ++j) {
+        for (int j = 0; j < MS && j < total; ++j) load_meta(j);
+      for (int j = 0; j < total; ++j) {
         const int h = j & 1, s = q + 4 * h;
         jitter(p.dbg, uint32_t(j) * 5u + 3u);
         if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
@@ -1529,7 +1559,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
                        "l"(cp_desc(src + uint32_t(kk) * 512)) : "memory");
         tc_commit(&slot_empty[s]);
         tc_commit(&tfull[h]);
-        if (j + 2 < jr.y) {
+        if (j + 2 < total) {
           mbar_wait(&slot_empty[s], (j >> 1) & 1);
           load_piece(j + 2);
         }
@@ -1537,7 +1567,14 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     }
   } else {
     if (tbase != 0) __trap();  // the 512-column allocation starts at lane 0, column 0 (addresses are absolute)
-    tmemr_consume<MULTI, SPLIT, RUNS, RW, PAIRS>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
+    if constexpr (PERSIST) {
+      const int W = p.nrb * int((p.N + 127) / 128);
+      for (int id = int(blockIdx.x), g0 = 0; id < W; id += int(gridDim.x), g0 += p.nch)
+        tmemr_consume<MULTI, SPLIT, RUNS, RW, PAIRS>(p, mring, mfull, mempty, tfull, tfree, id % p.nrb,
+                                                     int64_t(id / p.nrb) * 128, warp, lane, g0);
+    } else {
+      tmemr_consume<MULTI, SPLIT, RUNS, RW, PAIRS>(p, mring, mfull, mempty, tfull, tfree, rb, n0, warp, lane);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1730,6 +1767,26 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     }
     cudaFreeAsync(kws, stream);
     if (le != cudaSuccess) return fail(SDNN_ERR_CUDA, std::string("TMEM split-K: ") + cudaGetErrorString(le));
+    return SDNN_OK;
+  }
+  // persistent CTAs (one per SM, items round-robin through one chunk pipeline): opt-in experiment
+  // (SDNN_TMEM_PERSIST=1) — measured on the short-K BASELINE configs it gains on c4 2048×512 (+4-6 %)
+  // and loses on c3 512², c2 3072×768 and c4 512×2048 at 95 % (−5 to −9 %), c5 −4 %
+  // (profiles/r02_persist_ab.log), so the default keeps one CTA per item
+  static const int persist_env = [] {
+    const char* e = getenv("SDNN_TMEM_PERSIST");
+    return e ? atoi(e) : 0;
+  }();
+  const bool persist = rep && !prs && !multi && persist_env > 0;
+  if (persist) {
+    const unsigned pg = unsigned(std::min<int64_t>(nblocks, h->sms));
+    if (h->tmem_runs)
+      spmm_tmemr_kernel<false, false, true, tmem_rows(4), false, true><<<pg, threads, smem, stream>>>(
+          tmap, static_cast<const KParams&>(p));
+    else
+      spmm_tmemr_kernel<false, false, false, tmem_rows(4), false, true><<<pg, threads, smem, stream>>>(
+          tmap, static_cast<const KParams&>(p));
+    SDNN_CUDA_TRY(cudaGetLastError());
     return SDNN_OK;
   }
   if (prs && multi) spmm_tmemr_kernel<true, false, false, tmem_rows(4), true><<<grid, threads, smem, stream>>>(tmap, p);
@@ -2142,6 +2199,12 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_generic_kernel<6, tmem_rows(4), 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, true, tmem_rows(4), false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, false, tmem_rows(4), false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, false, tmem_rows(4), true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
