@@ -25,6 +25,7 @@ CASES = [  # (problem, N, handle options)
     ("c3_256x128", 128, dict(kernel="row")),                # row kernel, split-K
     ("c3_512x512", 6272, dict(kernel="tmem")),              # TMEM-R
     ("c4_2048x512_s95", 1024, dict(kernel="tmem")),         # TMEM-R with 1×4 runs
+    ("c3_1024x512", 6272, dict(kernel="tmem")),             # 245 items: several per CTA when persistent
     ("tsplit", 128, {}),                                    # TMEM-R split-K (4096², N = 128)
     ("c3_512x512", 1024, dict(kernel="tmemp")),             # row pairs
     ("c1", 1024, dict(kernel="tmem8")),                     # V = 8 TMEM kernel
@@ -74,3 +75,24 @@ def test_jittered_pipelines_bitwise(tmp_path):
         ref = h.spmm(X, torch.from_numpy(p.bias).cuda(), act=1).cpu().numpy()
         for rep in range(3):
             np.testing.assert_array_equal(got[f"{i}_{rep}"], ref, err_msg=f"{key} {opts} rep {rep}")
+
+
+def test_persistent_tmem_ctas_bitwise(tmp_path):
+    """SDNN_TMEM_PERSIST=1 (opt-in): one CTA per SM runs its (row block, N tile) items through one
+    chunk pipeline — same per-row order, so Y is bitwise the default launch's (TMEM-R cases only)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = tmp_path / "persist.npz"
+    env = dict(os.environ, SDNN_TMEM_PERSIST="1", PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(out)], env=env, capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    got = np.load(out)
+    sys.path.insert(0, ROOT)
+    import paper_2101_07948_b200 as sdnn
+    for i, (key, N, opts) in enumerate(CASES):
+        p = problem(key, N)
+        h = sdnn.Handle.from_problem(p, **opts)
+        X = torch.from_numpy(p.x_cols(0, N) if key == "tsplit" else p.x()[:, :N].copy()).cuda()
+        ref = h.spmm(X, torch.from_numpy(p.bias).cuda(), act=1).cpu().numpy()
+        np.testing.assert_array_equal(got[f"{i}_0"], ref, err_msg=f"{key} {opts}")
