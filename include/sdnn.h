@@ -58,18 +58,22 @@ typedef struct {
   uint32_t struct_size;
   int32_t permute;          /* 1 (default): Algorithm 1 greedy row reorder; 0: identity   */
   int32_t kernel;           /* 0 = auto: the row kernel's plan (or the group kernel's, by cost model)
-                               plus the TMEM kernel's plan; each sdnn_spmm call takes the TMEM
-                               kernel when N % 128 == 0, X/Y are 16-byte aligned and the call has
-                               2 · row blocks · N tiles ≥ SMs, else the row plan.
+                               plus the TMEM-R kernel's plan; each sdnn_spmm call takes the TMEM
+                               plan when N % 4 == 0, X/Y are 16-byte aligned and the call has at
+                               least a third of a wave of CTAs (or TMEM split-K fills one), else
+                               the row plan.
                                1 = row kernel (each nonzero reads its X row slice from shared
                                memory), 2 = group kernel (16-row groups: one X load feeds every
                                nonzero of the group in that column), 3 = codegen (per-panel
                                generated PTX with the weights as FFMA immediates, JIT-compiled
-                               during sdnn_prepare), 4 = TMEM kernel (X tile staged in
-                               tensor memory, 4 columns of N per TMEM lane, operands read by
-                               tcgen05.ld; 16-row warp panels), 5 = TMEM kernel with 8 columns per
-                               lane (8-row panels).  4 and 5 take their fast path when N % 128 == 0
-                               and X/Y are 16-byte aligned, else a generic kernel on the same plan. */
+                               during sdnn_prepare), 4 = TMEM-R kernel (a 128-column X
+                               tile replicated into all four TMEM lane quarters by tcgen05.cp,
+                               24 warps × 10-row panels, operands read by tcgen05.ld), 5 = TMEM
+                               kernel with 8 columns per lane (round 1's layout, 5-row panels),
+                               6 = TMEM-R with Algorithm 1 row pairs (columns two paired rows share
+                               are loaded once; per-row summation order differs from the others).
+                               4 and 6 take their fast path when N % 4 == 0 and X/Y are 16-byte
+                               aligned, 5 when N % 128 == 0; else a generic kernel on the same plan. */
   int32_t panel_rows_max;   /* row kernel: rows per warp panel, 0 = auto, else 4 or 8 (group: 16)   */
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
@@ -85,7 +89,7 @@ typedef struct {
   int64_t nnz;
   int32_t device;           /* CUDA ordinal, −1 for a host-only plan                                  */
   int32_t permuted;         /* 1 if Algorithm 1 was applied                                           */
-  int32_t kernel;           /* the primary plan's kernel: 1 row, 2 group, 3 codegen, 4/5 TMEM         */
+  int32_t kernel;           /* the primary plan's kernel: 1 row, 2 group, 3 codegen, 4/5/6 TMEM       */
   int32_t group_entries_per_nnz_x1000; /* group format: union entries per nonzero · 1000            */
   int32_t group_sb;         /* group kernel sub-block rows (0 for the row kernel)                     */
   int32_t group_subblocks_per_nnz_x1000; /* nonzero sub-blocks per nonzero · 1000                    */
@@ -295,8 +299,12 @@ SDNN_API const char* sdnn_last_error_message(void); /* thread-local; "" if none 
 SDNN_API int32_t sdnn_abi_version(void);
 
 /* Environment knobs read by libsdnn (diagnostics and experiments only; unset = the product path):
- *   SDNN_TMEM_FILL   TMEM kernels' fill path: 1 = filler warps with tcgen05.st (default), 0 = one
- *                    producer thread with tcgen05.cp, 2 = both (odd/even pieces)
+ *   SDNN_TMEM_FILL   kernel 5's fill path: 1 = filler warps with tcgen05.st (default), 0 = one
+ *                    producer thread with tcgen05.cp, 2 = both (odd/even pieces); kernels 4 / 6
+ *                    always fill with tcgen05.cp.32x128b.warpx4
+ *   SDNN_TMEM_PERSIST 1 = kernel 4 runs one CTA per SM over its (row block, N tile) items
+ *   SDNN_JITTER      1 = pseudo-random sleeps at the pipelines' mbarrier hand-offs (protocol tests;
+ *                    results unchanged, slower)
  *   SDNN_DEBUG_TMEM  bit mask, TMEM kernels: 1 skip the X loads (TMA), 2 skip the FMA loop, 4 skip the
  *                    smem -> TMEM fill — results are WRONG with any bit set (timing decomposition)
  *   SDNN_ROW_STAGES  upper bound on the row kernel's stage-ring depth
