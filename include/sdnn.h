@@ -234,9 +234,11 @@ SDNN_API sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle*
  * Tuning state is per handle, guarded by a mutex, and not serialized.  Codegen handles →
  * SDNN_ERR_UNSUPPORTED; N % 4 ≠ 0 or unaligned buffers → SDNN_ERR_INVALID_ARGUMENT. */
 /* sdnn_conv2d_tune: the same for sdnn_conv2d — times its tile choices for this geometry (the built-in
- * rules, then 2 / 4 output pixels per lane × 1 / 2 / 4 / 8 K slices) on the caller's DEVICE X / Y
- * (overwritten) and keeps the fastest (> 3 % better than the rules) for later calls with the same
- * {B, IC, H, W, FY, FX, pad, stride}.  choice_out = −1 (rules) or 16·pixels + slices. */
+ * rules, then 2 / 4 output pixels per lane × 1 / 2 / 4 / 8 K slices, and — handles with a TMEM plan —
+ * the explicit form: the virtual operand written out, then the TMEM-R SpMM) on the caller's DEVICE
+ * X / Y (overwritten) and keeps the fastest (> 3 % better than the rules) for later calls with the
+ * same {B, IC, H, W, FY, FX, pad, stride}.  choice_out = −1 (rules), −2 (explicit form) or
+ * 16·pixels + slices. */
 SDNN_API sdnn_status sdnn_conv2d_tune(sdnn_handle h, const float* X, int32_t B, int32_t IC, int32_t H, int32_t W,
                                       int32_t FY, int32_t FX, int32_t pad, int32_t stride, float* Y, void* stream,
                                       int32_t* choice_out, float* us_out);

@@ -237,7 +237,8 @@ class Handle:
         return cls(row_ptr, col_idx, vals, OC, IC * fyx, **opts)
 
     def conv2d_tune(self, X, FY: int = 3, FX: int = 3, pad: int = 1, stride: int = 1, stream=None) -> dict:
-        """sdnn_conv2d_tune for X's geometry: {"pixels": 2 | 4 | 0 (rules), "split_k": slices, "us": µs}."""
+        """sdnn_conv2d_tune for X's geometry: {"pixels": 2 | 4 | 0 (rules) | -2 (explicit form: virtual
+        operand written out + TMEM-R SpMM), "split_k": slices, "us": µs}."""
         import torch
         IC, B, H, W = X.shape
         Ho, Wo = (H + 2 * pad - FY) // stride + 1, (W + 2 * pad - FX) // stride + 1
@@ -246,6 +247,8 @@ class Handle:
         ch, us = _i32(0), ctypes.c_float(0)
         _check(_lib.sdnn_conv2d_tune(self._h, X.data_ptr(), B, IC, H, W, FY, FX, pad, stride, out.data_ptr(),
                                      s.cuda_stream, ctypes.byref(ch), ctypes.byref(us)), "sdnn_conv2d_tune")
+        if ch.value == -2:  # the explicit form (virtual operand written out, TMEM-R SpMM)
+            return {"pixels": -2, "split_k": 0, "us": us.value}
         if ch.value < 0:
             return {"pixels": 0, "split_k": 0, "us": us.value}
         return {"pixels": ch.value // 16, "split_k": ch.value % 16, "us": us.value}

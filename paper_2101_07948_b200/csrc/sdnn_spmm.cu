@@ -593,6 +593,21 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : (KIND == 4 |
 struct ConvGeom {
   int32_t B, IC, H, W, Ho, Wo, FY, FX, pad, stride;
 };
+// The convolution's virtual operand written out: Xv[k][n] = X[ic][b][oy·s + fy − pad][ox·s + fx − pad]
+// (0 outside the image), k = (ic·FY + fy)·FX + fx, n = (b·Ho + oy)·Wo + ox — the K × N matrix the
+// TMEM-R SpMM then multiplies (sdnn_conv2d's explicit form for deep, wide layers).  One thread per
+// element of a row segment: coalesced stores along n, the loads stride `s` along the image row.
+__global__ void im2col_kernel(const float* __restrict__ X, float* __restrict__ Xv, const ConvGeom c, int64_t N) {
+  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int32_t k = int32_t(blockIdx.y);
+  if (n >= N) return;
+  const int32_t fx = k % c.FX, fy = (k / c.FX) % c.FY, ic = k / (c.FX * c.FY);
+  const int32_t ox = int32_t(n % c.Wo), oy = int32_t((n / c.Wo) % c.Ho), b = int32_t(n / (int64_t(c.Wo) * c.Ho));
+  const int32_t y = oy * c.stride + fy - c.pad, x = ox * c.stride + fx - c.pad;
+  float v = 0.f;
+  if (y >= 0 && y < c.H && x >= 0 && x < c.W) v = X[((int64_t(ic) * c.B + b) * c.H + y) * c.W + x];
+  Xv[int64_t(k) * N + n] = v;
+}
 __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
                : "memory");
@@ -2542,6 +2557,42 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
     return fail(SDNN_ERR_INVALID_ARGUMENT, "Y overlaps X or bias");
   sdnn_status st = check_device(h);
   if (st != SDNN_OK) return st;
+  // explicit form: write the virtual operand Xv (K × N) once, then the TMEM-R SpMM of the handle's
+  // TMEM plan.  On the paper's suite (OC ≤ 256, profiles/r02_conv_forms.log) it wins only at 256
+  // channels, 14-28 px, 90 % (−8 %, −7 %) and loses up to 1.7× elsewhere: with ≤ 256 filters the
+  // 240-row TMEM row blocks run half empty.  So by default only layers with ≥ 480 filters (two full row
+  // blocks) and ≥ 8 nonzeros per virtual row take it when the TMEM kernel takes the call;
+  // sdnn_conv2d_tune times it as a candidate (px_force = -2), SDNN_CONV_IM2COL=0|1 forces it off / on.
+  {
+    static const int exp_env = [] {  // SDNN_CONV_IM2COL=0|1 (experiments)
+      const char* e = getenv("SDNN_CONV_IM2COL");
+      return e ? atoi(e) : -1;
+    }();
+    const YOut yo1 = y_single(Y, N);
+    const bool aligned = N % 4 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0;
+    const bool tmem_takes = h->alt && aligned && (tmem_worth(h->alt, reinterpret_cast<const float*>(uintptr_t(256)), N, yo1) ||
+                                                  tmem_split_for(h, reinterpret_cast<const float*>(uintptr_t(256)), N, yo1) > 1);
+    const bool want = px_force == -2 || (px_force <= 0 && ks_force <= 0 &&
+                                         (exp_env >= 0 ? exp_env > 0 : pl.M >= 480 && pl.nnz >= 8 * int64_t(pl.K)));
+    if (want && tmem_takes && h->ws_pool) {
+      float* xv = nullptr;
+      SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&xv), size_t(pl.K) * size_t(N) * 4, h->ws_pool,
+                                            static_cast<cudaStream_t>(stream)));
+      const ConvGeom cg{B, IC, H, W, Ho, Wo, FY, FX, pad, stride};
+      im2col_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(pl.K)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+          X, xv, cg, N);
+      cudaError_t le = cudaGetLastError();
+      sdnn_status st2 = le == cudaSuccess ? SDNN_OK : fail(SDNN_ERR_CUDA, std::string("im2col: ") + cudaGetErrorString(le));
+      if (st2 == SDNN_OK) {
+        if (const int ks = tmem_split_for(h, xv, N, yo1); ks > 1)
+          st2 = launch_tmem(h->alt, xv, N, bias, act, yo1, static_cast<cudaStream_t>(stream), ks, h->ws_pool);
+        else
+          st2 = launch_tmem(h->alt, xv, N, bias, act, yo1, static_cast<cudaStream_t>(stream));
+      }
+      cudaFreeAsync(xv, static_cast<cudaStream_t>(stream));
+      return st2;
+    }
+  }
   constexpr int TN = 128;
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   const int64_t nblocks = int64_t(pl.num_row_blocks) * ((N + TN - 1) / TN);
@@ -3103,6 +3154,7 @@ sdnn_status sdnn_conv2d_tune(sdnn_handle h, const float* X, int32_t B, int32_t I
   for (int px : {4, 2})
     for (int ks : {1, 2, 4, 8})
       if (ks == 1 || !h->plan.no_split_k) cands.emplace_back(px, ks);  // SDNN_FLAG_NO_SPLIT_K: never split
+  if (h->alt) cands.emplace_back(-2, 0);  // the explicit form: virtual operand written out + TMEM-R SpMM
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   SDNN_CUDA_TRY(cudaEventCreate(&e0));
   SDNN_CUDA_TRY(cudaEventCreate(&e1));
@@ -3137,7 +3189,7 @@ sdnn_status sdnn_conv2d_tune(sdnn_handle h, const float* X, int32_t B, int32_t I
     std::lock_guard<std::mutex> lk(h->tune_mu);
     h->conv_tuned[{B, IC, H, W, FY, FX, pad, stride}] = pick;
   }
-  if (choice_out) *choice_out = pick.first < 0 ? -1 : pick.first * 16 + pick.second;
+  if (choice_out) *choice_out = pick.first == -2 ? -2 : pick.first < 0 ? -1 : pick.first * 16 + pick.second;
   if (us_out) *us_out = best * 1000.f / 5.f;
   return SDNN_OK;
 }

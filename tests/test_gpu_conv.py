@@ -96,3 +96,19 @@ def test_conv_tune(sdnn, C, HW):
     err = np.abs(Y.astype(np.float64) - Yo) / np.where(S == 0, 1.0, S)
     assert float(err.max()) <= TOL
 
+
+
+@pytest.mark.parametrize("OC,IC,HW,B,sp", [(512, 128, 14, 8, 0.9), (480, 64, 28, 2, 0.8), (256, 256, 14, 8, 0.9)])
+def test_conv_explicit_form(sdnn, OC, IC, HW, B, sp):
+    """Layers with ≥ 480 filters take the explicit form (Xv = the virtual operand written out by
+    im2col_kernel, then the TMEM-R SpMM of the handle's TMEM plan); smaller ones can get it from the
+    tuner: oracle parity either way."""
+    p = synth.make_conv_problem(f"ex{OC}_{IC}_{HW}", OC, IC, HW, HW, B, sp)
+    Y, h = run(sdnn, p)
+    X = torch.from_numpy(p.x()).cuda()
+    r = h.conv2d_tune(X, p.FY, p.FX, p.pad, p.stride)
+    assert r["pixels"] in (-2, 0, 2, 4)
+    run_again = h.conv2d(X, p.FY, p.FX, p.pad, p.stride, torch.from_numpy(p.bias).cuda(), act=p.act).cpu().numpy()
+    Yo, S = oconv.conv2d(p.row_ptr, p.col_idx, p.vals, p.OC, p.IC, p.FY, p.FX, p.x(), p.pad, p.stride, p.bias, p.act)
+    err = np.abs(run_again.astype(np.float64) - Yo) / np.where(S == 0, 1.0, S)
+    assert float(err.max()) <= TOL
