@@ -128,6 +128,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Programmatic dependent launch (PDL): the row, TMEM-R and reduction kernels are launched with
+// programmatic stream serialization (launch_k), so a call's grid is scheduled while the previous
+// kernel on the stream drains and runs its prologue (mbarrier init, TMEM allocation, the first
+// metadata copies: plan memory, immutable after sdnn_prepare) in that kernel's shadow.
+// pdl_wait() blocks until every prerequisite grid has completed and its writes are visible — every
+// thread calls it before its first access to caller memory (X, bias, Y) or a workspace; without a
+// programmatic prerequisite it returns at once.  pdl_trigger() lets the next grid launch as soon as
+// every CTA of this one has started (it still waits for this grid's completion in its pdl_wait).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Timing perturbation for the pipeline-protocol tests (SDNN_JITTER=1 → KParams::dbg bit 8): a
 // pseudo-random 0-2 µs sleep at the mbarrier hand-off points of the TMA / TMEM pipelines, so that
 // producers, issuers and consumers interleave in orders the free-running kernel rarely produces; the
@@ -441,6 +452,8 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
 // column; blockIdx.y = split row.  split = {rows[ns], first piece[ns], piece count[ns]}.
 __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t* __restrict__ split, int32_t ns,
                                     const float* __restrict__ bias, int32_t act, const YOut yo, int64_t N) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (n >= N) return;
   for (int32_t sr = int32_t(blockIdx.y); sr < ns; sr += int32_t(gridDim.y)) {  // gridDim.y ≤ 65535
@@ -459,6 +472,8 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t*
 // column; blockIdx.y = row.
 __global__ void splitk_reduce_kernel(const float* __restrict__ kws, int32_t KS, int32_t M, const float* __restrict__ bias,
                                      int32_t act, const YOut yo, int64_t N) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (n >= N) return;
   const int64_t slice = int64_t(M) * N;
@@ -497,16 +512,27 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_trigger();
 
   // split-K (gridDim.y > 1): this CTA's K chunks [j0, j1)
   const int j0 = int(blockIdx.y) * p.nch / int(gridDim.y), j1 = (int(blockIdx.y) + 1) * p.nch / int(gridDim.y);
   if (warp == p.wc) {  // producer
     if (lane == 0) {
       const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
-      for (int j = j0; j < j1; ++j) {
+      // the first stages' metadata (plan memory) before the dependency wait, their X tiles after it
+      const int pre = S < j1 - j0 ? S : j1 - j0;
+      for (int t = 0; t < pre; ++t) {
+        const uint32_t mbytes = uint32_t(off[j0 + t + 1] - off[j0 + t]);
+        mbar_expect_tx(&full[t], uint32_t(p.x_stage_bytes) + mbytes);
+        bulk_load(mstage + size_t(t) * p.m_stage_bytes, p.meta + off[j0 + t], mbytes, &full[t]);
+      }
+      pdl_wait();
+      for (int t = 0; t < pre; ++t)
+        tma_load_2d(xstage + size_t(t) * p.x_stage_bytes, &tmap, int32_t(n0), (j0 + t) * p.kc, &full[t]);
+      for (int j = j0 + pre; j < j1; ++j) {
         const int s = (j - j0) % S;
         jitter(p.dbg, uint32_t(j));
-        if (j - j0 >= S) mbar_wait(&empty[s], (((j - j0) / S) - 1) & 1);
+        mbar_wait(&empty[s], (((j - j0) / S) - 1) & 1);
         const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
         mbar_expect_tx(&full[s], uint32_t(p.x_stage_bytes) + mbytes);
         tma_load_2d(xstage + size_t(s) * p.x_stage_bytes, &tmap, int32_t(n0), j * p.kc, &full[s]);
@@ -535,6 +561,7 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   (void)TN;
+  pdl_wait();  // bias, Y / workspace (an empty K range never waited on a stage)
   epilogue<RW, V, true>(acc, p, rb * p.wc + warp, lane, n0);
 }
 
@@ -1433,6 +1460,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
     }
   }
   // epilogue: panel rb·24 + warp; lane columns n0 + 4·lane
+  pdl_wait();  // bias, Y / workspace
   const int64_t n = n0 + lane * 4;
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
@@ -1503,6 +1531,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
   const uint32_t tbase = *tbase_s;
 
   if (warp >= kTmemRConsumers) {
@@ -1551,9 +1580,11 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
         mbar_expect_tx(&mfull[m], mbytes);
         bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[0], mbytes, &mfull[m]);
       };
-      for (int j = 0; j < 2 && j < total; ++j) load_piece(j);
+      // the first chunks' metadata (plan memory) before the dependency wait, X after it
       if (q == 0)
         for (int j = 0; j < MS && j < total; ++j) load_meta(j);
+      pdl_wait();
+      for (int j = 0; j < 2 && j < total; ++j) load_piece(j);
       for (int j = 0; j < total; ++j) {
         const int h = j & 1, s = q + 4 * h;
         jitter(p.dbg, uint32_t(j) * 5u + 3u);
@@ -1645,6 +1676,34 @@ static int occupancy(const void* fn, int threads, size_t smem) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) n = 1;
   cache.emplace_back(key, n);
   return n;
+}
+
+// Launch with programmatic stream serialization (see pdl_wait / pdl_trigger): the kernel may be
+// scheduled while the previous kernel on the stream drains.  SDNN_PDL=0 launches plainly (A/B runs).
+static bool pdl_on() {
+  static const bool on = [] {
+    const char* e = getenv("SDNN_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+static cudaLaunchConfig_t pdl_cfg(dim3 grid, dim3 block, size_t smem, cudaStream_t st, cudaLaunchAttribute* at) {
+  at->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at->val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cfg;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchAttribute at;
+  const cudaLaunchConfig_t cfg = pdl_cfg(grid, block, smem, st, &at);
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
@@ -1771,12 +1830,12 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     q.kws = kws;
     q.M = pl.M;
     const dim3 g2{grid, unsigned(KS)};
-    if (prs) spmm_tmemr_kernel<false, true, false, tmem_rows(4), true><<<g2, threads, smem, stream>>>(tmap, q);
-    else if (rep) spmm_tmemr_kernel<false, true><<<g2, threads, smem, stream>>>(tmap, q);
+    if (prs) launch_k(spmm_tmemr_kernel<false, true, false, tmem_rows(4), true>, g2, threads, smem, stream, tmap, q);
+    else if (rep) launch_k(spmm_tmemr_kernel<false, true>, g2, threads, smem, stream, tmap, q);
     else spmm_tmem_kernel<8, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
     cudaError_t le = cudaGetLastError();
     if (le == cudaSuccess) {
-      splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, stream>>>(kws, KS, pl.M, bias, act,
+      launch_k(splitk_reduce_kernel, dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, stream, kws, KS, pl.M, bias, act,
                                                                                                  yo, N);
       le = cudaGetLastError();
     }
@@ -1796,20 +1855,20 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   if (persist) {
     const unsigned pg = unsigned(std::min<int64_t>(nblocks, h->sms));
     if (h->tmem_runs)
-      spmm_tmemr_kernel<false, false, true, tmem_rows(4), false, true><<<pg, threads, smem, stream>>>(
+      launch_k(spmm_tmemr_kernel<false, false, true, tmem_rows(4), false, true>, pg, threads, smem, stream, 
           tmap, static_cast<const KParams&>(p));
     else
-      spmm_tmemr_kernel<false, false, false, tmem_rows(4), false, true><<<pg, threads, smem, stream>>>(
+      launch_k(spmm_tmemr_kernel<false, false, false, tmem_rows(4), false, true>, pg, threads, smem, stream, 
           tmap, static_cast<const KParams&>(p));
     SDNN_CUDA_TRY(cudaGetLastError());
     return SDNN_OK;
   }
-  if (prs && multi) spmm_tmemr_kernel<true, false, false, tmem_rows(4), true><<<grid, threads, smem, stream>>>(tmap, p);
+  if (prs && multi) launch_k(spmm_tmemr_kernel<true, false, false, tmem_rows(4), true>, grid, threads, smem, stream, tmap, p);
   else if (prs)
-    spmm_tmemr_kernel<false, false, false, tmem_rows(4), true><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
-  else if (rep && multi) spmm_tmemr_kernel<true, false><<<grid, threads, smem, stream>>>(tmap, p);
-  else if (rep && h->tmem_runs) spmm_tmemr_kernel<false, false, true><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
-  else if (rep) spmm_tmemr_kernel<false, false, false><<<grid, threads, smem, stream>>>(tmap, static_cast<const KParams&>(p));
+    launch_k(spmm_tmemr_kernel<false, false, false, tmem_rows(4), true>, grid, threads, smem, stream, tmap, static_cast<const KParams&>(p));
+  else if (rep && multi) launch_k(spmm_tmemr_kernel<true, false>, grid, threads, smem, stream, tmap, p);
+  else if (rep && h->tmem_runs) launch_k(spmm_tmemr_kernel<false, false, true>, grid, threads, smem, stream, tmap, static_cast<const KParams&>(p));
+  else if (rep) launch_k(spmm_tmemr_kernel<false, false, false>, grid, threads, smem, stream, tmap, static_cast<const KParams&>(p));
   else if (multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
   else if (fill == 2) spmm_tmem_kernel<8, 2><<<grid, threads, smem, stream>>>(tmap, p);
   else if (fill == 1) spmm_tmem_kernel<8, 1><<<grid, threads, smem, stream>>>(tmap, p);
@@ -1962,7 +2021,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   if (KS > 1) {
     if (st == SDNN_OK) {
       const dim3 grid{unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))};
-      splitk_reduce_kernel<<<grid, 256, 0, stream>>>(kws, KS, pl.M, bias, act, yo, N);
+      launch_k(splitk_reduce_kernel, grid, 256, 0, stream, kws, KS, pl.M, bias, act, yo, N);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("splitk_reduce_kernel: ") + cudaGetErrorString(le));
     }
@@ -1971,7 +2030,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   if (ns > 0) {
     if (st == SDNN_OK) {
       const dim3 grid{unsigned((N + 255) / 256), unsigned(std::min(ns, 65535))};
-      split_reduce_kernel<<<grid, 256, 0, stream>>>(ws, h->d_split, ns, bias, act, yo, N);
+      launch_k(split_reduce_kernel, grid, 256, 0, stream, ws, h->d_split, ns, bias, act, yo, N);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("split_reduce_kernel: ") + cudaGetErrorString(le));
     }
@@ -2123,7 +2182,9 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SDNN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
     void* args[] = {&tmap, &p};
-    SDNN_CUDA_TRY(cudaLaunchKernel(fn, dim3(unsigned(nblocks), unsigned(KS)), dim3(unsigned(threads)), args, smem, stream));
+    cudaLaunchAttribute at;
+    const cudaLaunchConfig_t cfg = pdl_cfg(dim3(unsigned(nblocks), unsigned(KS)), dim3(unsigned(threads)), smem, stream, &at);
+    SDNN_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
   } else {
     if (KS > 1) return fail(SDNN_ERR_INTERNAL, "split-K outside the row kernel's fast path");
     p.stages = 1;
@@ -2677,7 +2738,7 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
       cudaError_t le = cudaLaunchKernel(fn2, dim3(unsigned(nb2), unsigned(KS)), dim3(unsigned(wc * 32)), args2,
                                         smem2, st_);
       if (le == cudaSuccess && KS > 1) {
-        splitk_reduce_kernel<<<dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, st_>>>(kws, KS, pl.M, bias, act,
+        launch_k(splitk_reduce_kernel, dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, st_, kws, KS, pl.M, bias, act,
                                                                                                 y_single(Y, N), N);
         le = cudaGetLastError();
       }
