@@ -376,17 +376,34 @@ template <int KIND> struct AccSel { using type = float2; };
 template <> struct AccSel<2> { using type = uint64_t; };
 template <int KIND> using AccT = typename AccSel<KIND>::type;
 
+// A warp's output rows (row_orig: plan memory) and their biases, loaded ahead of the epilogue (the row
+// kernel: at its start, so the global-load latency overlaps the K loop).  Bias: caller memory — after
+// pdl_wait.
+template <int RW> struct RowPre {
+  int32_t orow[RW];
+  float b[RW];
+};
+template <int RW>
+__device__ __forceinline__ RowPre<RW> row_pre(const KParamsY& p, int panel) {
+  RowPre<RW> q;
+#pragma unroll
+  for (int r = 0; r < RW; ++r) q.orow[r] = p.row_orig[panel * RW + r];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) q.b[r] = (q.orow[r] >= 0 && p.bias && !p.kws) ? p.bias[q.orow[r]] : 0.f;
+  return q;
+}
+
 template <int RW, int V, bool VEC, typename A>
-__device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParamsY& p, int panel, int lane,
-                                         int64_t n0) {
+__device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParamsY& p, const RowPre<RW>& pre,
+                                         int lane, int64_t n0) {
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
-    const int32_t orow = p.row_orig[panel * RW + r];
+    const int32_t orow = pre.orow[r];
     if (orow == -1) continue;
     // a piece of a split row (row_orig = −2 − piece): its raw partial sums go to workspace row
     // `piece`; split_reduce_kernel adds the pieces, the bias and the activation
     const bool piece = orow <= -2 || p.kws;  // raw partial sums: a split row's piece or a split-K slice
-    const float b = (piece || !p.bias) ? 0.f : p.bias[orow];
+    const float b = pre.b[r];
     if constexpr (V == 2) {
       const int64_t n = n0 + lane * 2;
       const float2 a0 = as_f2(acc[r][0]);
@@ -519,24 +536,44 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
   if (warp == p.wc) {  // producer
     if (lane == 0) {
       const int64_t* off = p.blk_off + int64_t(rb) * p.nch;
-      // the first stages' metadata (plan memory) before the dependency wait, their X tiles after it
+      // the first stages' metadata (plan memory) before the dependency wait, their X tiles after it;
+      // the chunk offsets are loaded together (S ≤ 4), then one chunk ahead of their use — a small
+      // call's start-up is otherwise a chain of dependent global loads
       const int pre = S < j1 - j0 ? S : j1 - j0;
-      for (int t = 0; t < pre; ++t) {
-        const uint32_t mbytes = uint32_t(off[j0 + t + 1] - off[j0 + t]);
-        mbar_expect_tx(&full[t], uint32_t(p.x_stage_bytes) + mbytes);
-        bulk_load(mstage + size_t(t) * p.m_stage_bytes, p.meta + off[j0 + t], mbytes, &full[t]);
+      int64_t o[5];
+#pragma unroll
+      for (int t = 0; t < 5; ++t) o[t] = t <= pre ? off[j0 + t] : 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t < pre) {
+          const uint32_t mbytes = uint32_t(o[t + 1] - o[t]);
+          mbar_expect_tx(&full[t], uint32_t(p.x_stage_bytes) + mbytes);
+          bulk_load(mstage + size_t(t) * p.m_stage_bytes, p.meta + o[t], mbytes, &full[t]);
+        }
       }
       pdl_wait();
       for (int t = 0; t < pre; ++t)
         tma_load_2d(xstage + size_t(t) * p.x_stage_bytes, &tmap, int32_t(n0), (j0 + t) * p.kc, &full[t]);
+      int64_t lo = 0, hi = 0;
+#pragma unroll
+      for (int t = 0; t < 5; ++t)
+        if (t == pre) lo = o[t];
+      if (j0 + pre < j1) hi = off[j0 + pre + 1];
+      int s = pre % S, ph = 0;  // stage and the phase of its empty barrier to wait for
       for (int j = j0 + pre; j < j1; ++j) {
-        const int s = (j - j0) % S;
+        const int64_t nxt = j + 1 < j1 ? off[j + 2] : 0;
         jitter(p.dbg, uint32_t(j));
-        mbar_wait(&empty[s], (((j - j0) / S) - 1) & 1);
-        const uint32_t mbytes = uint32_t(off[j + 1] - off[j]);
+        mbar_wait(&empty[s], ph);
+        const uint32_t mbytes = uint32_t(hi - lo);
         mbar_expect_tx(&full[s], uint32_t(p.x_stage_bytes) + mbytes);
         tma_load_2d(xstage + size_t(s) * p.x_stage_bytes, &tmap, int32_t(n0), j * p.kc, &full[s]);
-        bulk_load(mstage + size_t(s) * p.m_stage_bytes, p.meta + off[j], mbytes, &full[s]);
+        bulk_load(mstage + size_t(s) * p.m_stage_bytes, p.meta + lo, mbytes, &full[s]);
+        lo = hi;
+        hi = nxt;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
     return;
@@ -547,10 +584,11 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
   for (int r = 0; r < RW; ++r)
 #pragma unroll
     for (int q = 0; q < V / 2; ++q) acc[r][q] = AccT<KIND>{};
+  pdl_wait();  // bias (prefetched now), Y / workspace in the epilogue
+  const RowPre<RW> pre = row_pre<RW>(p, rb * p.wc + warp);
 
-  for (int j = j0; j < j1; ++j) {
-    const int s = (j - j0) % S;
-    mbar_wait(&full[s], ((j - j0) / S) & 1);
+  for (int j = j0, s = 0, ph = 0; j < j1; ++j) {
+    mbar_wait(&full[s], ph);
     const float* xs = reinterpret_cast<const float*>(xstage + size_t(s) * p.x_stage_bytes);
     if constexpr (KIND == 2)
       consume_group<V, SB>(acc, xs, mstage + size_t(s) * p.m_stage_bytes, warp, lane);
@@ -559,10 +597,13 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
     jitter(p.dbg, uint32_t(j) * 7u + 1u);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
+    }
   }
   (void)TN;
-  pdl_wait();  // bias, Y / workspace (an empty K range never waited on a stage)
-  epilogue<RW, V, true>(acc, p, rb * p.wc + warp, lane, n0);
+  epilogue<RW, V, true>(acc, p, pre, lane, n0);
 }
 
 // Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
@@ -605,7 +646,7 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : (KIND == 4 |
     else
       consume_chunk<RW, V, (KIND == 4 || KIND == 5 ? KIND - 2 : 0)>(acc, xs, ms, warp, lane, p.hdr_bytes);
   }
-  epilogue<RW, V, false>(acc, p, rb * p.wc + warp, lane, n0);
+  epilogue<RW, V, false>(acc, p, row_pre<RW>(p, rb * p.wc + warp), lane, n0);
 }
 
 
@@ -710,7 +751,7 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
     consume_chunk<RW, V>(acc, xs_of(j & 1), ms_of(j & 1), warp, lane, p.hdr_bytes);
     __syncthreads();
   }
-  epilogue<RW, V, VEC>(acc, p, rb * p.wc + warp, lane, n0);
+  epilogue<RW, V, VEC>(acc, p, row_pre<RW>(p, rb * p.wc + warp), lane, n0);
 }
 
 // Patch form (the default): per K chunk the CTA stages the *input* rows its tile needs — the window
@@ -1580,9 +1621,22 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
         mbar_expect_tx(&mfull[m], mbytes);
         bulk_load(mring + size_t(m) * p.m_stage_bytes, p.meta + off[0], mbytes, &mfull[m]);
       };
-      // the first chunks' metadata (plan memory) before the dependency wait, X after it
-      if (q == 0)
-        for (int j = 0; j < MS && j < total; ++j) load_meta(j);
+      // the first chunks' metadata (plan memory) before the dependency wait, X after it; one item:
+      // their offsets loaded together (a short K range's start-up is otherwise a chain of loads)
+      if (q == 0) {
+        if constexpr (!PERSIST) {
+          static_assert(MS == 2, "prologue offsets for two metadata slots");
+          const int64_t* off = p.blk_off + int64_t(rb) * p.nch + jr.x;
+          const int64_t o0 = off[0], o1 = off[1], o2 = total > 1 ? off[2] : 0;
+          for (int j = 0; j < MS && j < total; ++j) {
+            const int64_t lo = j ? o1 : o0, hi = j ? o2 : o1;
+            mbar_expect_tx(&mfull[j], uint32_t(hi - lo));
+            bulk_load(mring + size_t(j) * p.m_stage_bytes, p.meta + lo, uint32_t(hi - lo), &mfull[j]);
+          }
+        } else {
+          for (int j = 0; j < MS && j < total; ++j) load_meta(j);
+        }
+      }
       pdl_wait();
       for (int j = 0; j < 2 && j < total; ++j) load_piece(j);
       for (int j = 0; j < total; ++j) {
