@@ -541,10 +541,15 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       const bool split = out && g.kernel == 1 && g.tmem == 0 && !(o.flags & SDNN_FLAG_NO_ROW_SPLIT);
       const int32_t nw0 = g.nrb * g.wc;
       const int64_t T = std::max<int64_t>(64, (nnz + nw0 - 1) / std::max(nw0, 1));
+      // split rows: [first piece, piece count) per heavy row, heaviest first
+      std::vector<std::pair<int64_t, std::pair<int32_t, int32_t>>> groups;
       for (int32_t r = 0; r < M; ++r) {
         const int64_t n = nz(r);
         if (split && n > T) {
-          const int32_t P = int32_t((n + T - 1) / T);
+          // at most one piece per warp of a CTA: the pieces of a row share a row block, so the row
+          // kernel adds them in shared memory at its end (no workspace, no reduction kernel)
+          const int32_t P = int32_t(std::min<int64_t>((n + T - 1) / T, g.wc));
+          groups.push_back({n, {int32_t(out->row.size()), P}});
           for (int32_t q = 0; q < P; ++q) {  // piece q: entries q, q + P, q + 2P, … of the row
             items.push_back({(n - q + P - 1) / P, -2 - int32_t(out->row.size())});
             out->row.push_back(r);
@@ -566,20 +571,74 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
                        [&](const std::pair<int64_t, int32_t>& a, const std::pair<int64_t, int32_t>& b) {
                          return a.first > b.first;
                        });
-      // min-heap of (load, warp); warps with full slots leave the heap
+      std::vector<int32_t> fill(nw, 0);
+      std::vector<int64_t> load(nw, 0);
+      std::vector<std::vector<int32_t>> rows(nw);
+      // 1. the split rows' pieces, heaviest row first: the row block whose least-loaded free warps
+      //    take the pieces with the smallest resulting maximum load (lowest block on ties), one piece
+      //    per warp.  Bounded work (groups × blocks); beyond it, or if no block has room, the pieces
+      //    go through the LPT below like rows (anywhere: workspace + reduction kernel instead).
+      bool local = !groups.empty() && int64_t(groups.size()) * g.nrb <= 4000000;
+      std::stable_sort(groups.begin(), groups.end(),
+                       [](const auto& a, const auto& b) { return a.first > b.first; });
+      std::vector<char> placed(out ? out->row.size() : 0, 0);
+      for (size_t gi = 0; local && gi < groups.size(); ++gi) {
+        const int32_t first = groups[gi].second.first, P = groups[gi].second.second;
+        std::vector<int64_t> wt(P);
+        for (int32_t q = 0; q < P; ++q) {
+          const int64_t n = (out->end[size_t(first + q)] - out->begin[size_t(first + q)] + P - 1) / P;
+          wt[size_t(q)] = n;
+        }
+        int32_t best_b = -1;
+        int64_t best_c = 0;
+        std::vector<int32_t> best_w, cand;
+        for (int32_t b = 0; b < g.nrb; ++b) {
+          cand.clear();
+          for (int32_t w = b * g.wc; w < (b + 1) * g.wc; ++w)
+            if (fill[w] < g.rw) cand.push_back(w);
+          if (int32_t(cand.size()) < P) continue;
+          std::stable_sort(cand.begin(), cand.end(), [&](int32_t x, int32_t y) { return load[x] < load[y]; });
+          int64_t c = 0;
+          for (int32_t q = 0; q < P; ++q) c = std::max(c, load[cand[size_t(q)]] + wt[size_t(q)] + 1);
+          if (best_b < 0 || c < best_c) {
+            best_b = b;
+            best_c = c;
+            best_w.assign(cand.begin(), cand.begin() + P);
+          }
+        }
+        if (best_b < 0) {
+          local = false;
+          break;
+        }
+        for (int32_t q = 0; q < P; ++q) {
+          const int32_t w = best_w[size_t(q)];
+          rows[w].push_back(-2 - (first + q));
+          load[w] += wt[size_t(q)] + 1;
+          ++fill[w];
+          placed[size_t(first + q)] = 1;
+        }
+      }
+      if (!local) {  // undo: every item through the LPT
+        std::fill(fill.begin(), fill.end(), 0);
+        std::fill(load.begin(), load.end(), 0);
+        for (auto& v : rows) v.clear();
+        std::fill(placed.begin(), placed.end(), 0);
+      }
+      // 2. LPT: min-heap of (load, warp); warps with full slots leave the heap
       std::vector<std::pair<int64_t, int32_t>> heap;
       heap.reserve(nw);
-      for (int32_t w = 0; w < nw; ++w) heap.push_back({0, w});
-      std::vector<int32_t> fill(nw, 0);
-      std::vector<std::vector<int32_t>> rows(nw);
+      for (int32_t w = 0; w < nw; ++w)
+        if (fill[w] < g.rw) heap.push_back({load[w], w});
       auto cmp = [](const std::pair<int64_t, int32_t>& a, const std::pair<int64_t, int32_t>& b) { return a > b; };
+      std::make_heap(heap.begin(), heap.end(), cmp);
       for (const auto& it : items) {
+        if (it.second <= -2 && placed[size_t(-2 - it.second)]) continue;
         std::pop_heap(heap.begin(), heap.end(), cmp);
-        auto [load, w] = heap.back();
+        auto [ld, w] = heap.back();
         heap.pop_back();
         rows[w].push_back(it.second);
         if (++fill[w] < g.rw) {
-          heap.push_back({load + it.first + 1, w});
+          heap.push_back({ld + it.first + 1, w});
           std::push_heap(heap.begin(), heap.end(), cmp);
         }
       }

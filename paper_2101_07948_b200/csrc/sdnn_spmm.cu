@@ -71,6 +71,10 @@ struct sdnn_handle_s {
   int64_t* d_blk_off = nullptr;
   int32_t* d_row_orig = nullptr;
   int32_t* d_split = nullptr;  // split-row table {rows, first piece, count} (row plan)
+  // split rows whose pieces all sit in one row block: per slot {pk, target row} (row_pre), so the row
+  // kernel adds the pieces in shared memory; null when some row's pieces span row blocks
+  int2* d_slotpk = nullptr;
+  int32_t pieces_per_cta = 0;  // most pieces in one row block (shared-memory slots the sum needs)
   cudaMemPool_t ws_pool = nullptr;  // split-row workspaces: stream-ordered, memory kept between calls
   // codegen kernel: one JIT module per panel, one stream per panel (all panels run concurrently)
   std::vector<CUmodule> cg_mods;
@@ -242,6 +246,8 @@ struct KParams {
 // __launch_bounds__) shifts with the parameter block size and a larger block measured 8 % slower on c5.
 struct KParamsY : KParams {
   float* kws;   // split-K (row kernel): raw partial sums, slice blockIdx.y at kws + blockIdx.y·M·N, else NULL
+  const int2* slotpk;  // row kernel, CTA-local split rows: per slot {pk, target row} (pieces summed in
+                       // shared memory at the kernel's end); NULL: pieces go to the workspace p.ws
   int32_t M;
   YOut yo;  // every destination (sdnn_spmm_multi); p.Y = yo.y[0] when there is just one of ld = N, col0 = 0
 };
@@ -393,17 +399,91 @@ __device__ __forceinline__ RowPre<RW> row_pre(const KParamsY& p, int panel) {
   return q;
 }
 
+// Stores of one lane's output values of row `row` (columns n .. n + NV − 1) to every destination.
+template <int NV, bool VEC>
+__device__ __forceinline__ void y_store_row(const KParamsY& p, int32_t row, int64_t n, const float (&v)[NV]) {
+  const bool single = p.Y != nullptr;
+  for (int d = 0; d < (single ? 1 : p.yo.n); ++d) {
+    float* yrow = single ? p.Y + int64_t(row) * p.N : p.yo.y[d] + int64_t(row) * p.yo.ld + p.yo.col0;
+    const bool mc = !single && p.yo.mc;
+    if (VEC && NV == 4) {
+      if (n < p.N) y_st4(yrow + n, v[0], v[1], v[2], v[3], mc);
+    } else if (VEC && NV == 2) {
+      if (n < p.N) y_st2(yrow + n, v[0], v[1], mc);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        if (n + q < p.N) y_st1(yrow + n + q, v[q], mc);
+    }
+  }
+}
+
+// CTA-local split rows (row kernel, p.slotpk set; CTA-uniform): after the K loop every piece's raw
+// partial sums go to shared-memory slot L (the stage ring, idle by then), and the warp holding a row's
+// first piece adds the row's pieces in piece order, then the bias and the activation — the same
+// operations, in the same order, as split_reduce_kernel over the workspace.  Consumer warps only
+// (named barrier 1; the producer warp has exited).
+// Per slot of p.slotpk: pk = L | cnt << 8 | is_first << 16 (L: the piece's shared-memory slot, a
+// row's pieces consecutive) and the row's target Y row.
 template <int RW, int V, bool VEC, typename A>
-__device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParamsY& p, const RowPre<RW>& pre,
-                                         int lane, int64_t n0) {
+__device__ __forceinline__ void combine_pieces(const A (&acc)[RW][V / 2], const KParamsY& p, float* ps, int panel,
+                                               int lane, int64_t n0) {
+  constexpr int TN = 32 * V, NV = V == 2 ? 2 : 4;
+  int2 pc[RW];  // {pk, target}; pk = 0 for whole rows and empty slots (no piece: nothing to do)
+#pragma unroll
+  for (int r = 0; r < RW; ++r) pc[r] = p.slotpk[panel * RW + r];
+  asm volatile("bar.sync 1, %0;" ::"r"(p.wc * 32) : "memory");  // every warp is done with the ring
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
-    const int32_t orow = pre.orow[r];
-    if (orow == -1) continue;
+    if (!(pc[r].x & 0x1ff00)) continue;  // not a piece (a piece has cnt ≥ 1)
+    float* d = ps + (pc[r].x & 255) * TN + lane * NV;
+#pragma unroll
+    for (int h = 0; h < (V == 2 ? 1 : V / 4); ++h) {
+      if constexpr (V == 2) {
+        *reinterpret_cast<float2*>(d) = as_f2(acc[r][0]);
+      } else {
+        const float2 a0 = as_f2(acc[r][2 * h]), a1 = as_f2(acc[r][2 * h + 1]);
+        *reinterpret_cast<float4*>(d + h * 128) = make_float4(a0.x, a0.y, a1.x, a1.y);
+      }
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(p.wc * 32) : "memory");
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    if (!((pc[r].x >> 16) & 1)) continue;
+    const int L0 = pc[r].x & 255, cnt = (pc[r].x >> 8) & 255;
+    const float b = p.bias ? p.bias[pc[r].y] : 0.f;
+#pragma unroll
+    for (int h = 0; h < (V == 2 ? 1 : V / 4); ++h) {
+      const float* s0 = ps + L0 * TN + lane * NV + h * 128;
+      float v[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) v[q] = s0[q];
+      for (int k = 1; k < cnt; ++k)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] += s0[k * TN + q];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        if (p.bias) v[q] += b;
+        if (p.act == SDNN_ACT_RELU) v[q] = v[q] > 0.f ? v[q] : 0.f;
+      }
+      y_store_row<NV, VEC>(p, pc[r].y, n0 + h * 128 + lane * NV, v);
+    }
+  }
+}
+
+// pre: the rows and biases loaded ahead (row_pre), or NULL: loaded here, row by row (fewer live registers)
+template <int RW, int V, bool VEC, typename A>
+__device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParamsY& p, const RowPre<RW>* pre,
+                                         int panel, int lane, int64_t n0) {
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int32_t orow = pre ? pre->orow[r] : p.row_orig[panel * RW + r];
+    if (orow == -1 || (orow <= -2 && p.slotpk)) continue;  // CTA-local pieces: combine_pieces
     // a piece of a split row (row_orig = −2 − piece): its raw partial sums go to workspace row
     // `piece`; split_reduce_kernel adds the pieces, the bias and the activation
     const bool piece = orow <= -2 || p.kws;  // raw partial sums: a split row's piece or a split-K slice
-    const float b = pre.b[r];
+    const float b = pre ? pre->b[r] : (piece || !p.bias) ? 0.f : p.bias[orow];
     if constexpr (V == 2) {
       const int64_t n = n0 + lane * 2;
       const float2 a0 = as_f2(acc[r][0]);
@@ -585,7 +665,11 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
 #pragma unroll
     for (int q = 0; q < V / 2; ++q) acc[r][q] = AccT<KIND>{};
   pdl_wait();  // bias (prefetched now), Y / workspace in the epilogue
-  const RowPre<RW> pre = row_pre<RW>(p, rb * p.wc + warp);
+  // output rows and biases loaded before the K loop where the registers allow (≤ 16 accumulators; the
+  // 8-row / V = 8 tiles would spill), else after it
+  constexpr bool PRE = RW * V <= 16;
+  RowPre<RW> pre;
+  if constexpr (PRE) pre = row_pre<RW>(p, rb * p.wc + warp);
 
   for (int j = j0, s = 0, ph = 0; j < j1; ++j) {
     mbar_wait(&full[s], ph);
@@ -603,7 +687,9 @@ __global__ void __launch_bounds__(KIND == 2 ? (kMaxGroupWarps + 1) * 32 : 17 * 3
     }
   }
   (void)TN;
-  epilogue<RW, V, true>(acc, p, pre, lane, n0);
+  epilogue<RW, V, true>(acc, p, PRE ? &pre : nullptr, rb * p.wc + warp, lane, n0);
+  if constexpr (KIND == 1)
+    if (p.slotpk) combine_pieces<RW, V, true>(acc, p, reinterpret_cast<float*>(xstage), rb * p.wc + warp, lane, n0);
 }
 
 // Generic path (N % 4 != 0 or unaligned X/Y): the same consumption, with the stage filled by all
@@ -646,7 +732,7 @@ __global__ void __launch_bounds__(KIND == 2 ? kMaxGroupWarps * 32 : (KIND == 4 |
     else
       consume_chunk<RW, V, (KIND == 4 || KIND == 5 ? KIND - 2 : 0)>(acc, xs, ms, warp, lane, p.hdr_bytes);
   }
-  epilogue<RW, V, false>(acc, p, row_pre<RW>(p, rb * p.wc + warp), lane, n0);
+  epilogue<RW, V, false>(acc, p, static_cast<const RowPre<RW>*>(nullptr), rb * p.wc + warp, lane, n0);
 }
 
 
@@ -751,7 +837,7 @@ __global__ void __launch_bounds__(16 * 32, 1) spmm_conv_kernel(const KParamsY p,
     consume_chunk<RW, V>(acc, xs_of(j & 1), ms_of(j & 1), warp, lane, p.hdr_bytes);
     __syncthreads();
   }
-  epilogue<RW, V, VEC>(acc, p, row_pre<RW>(p, rb * p.wc + warp), lane, n0);
+  epilogue<RW, V, VEC>(acc, p, static_cast<const RowPre<RW>*>(nullptr), rb * p.wc + warp, lane, n0);
 }
 
 // Patch form (the default): per K chunk the CTA stages the *input* rows its tile needs — the window
@@ -1940,7 +2026,22 @@ static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const 
 }
 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                               const YOut& yo, float* ws, cudaStream_t stream, float* kws = nullptr, int KS = 1);
+                               const YOut& yo, float* ws, cudaStream_t stream, float* kws = nullptr, int KS = 1,
+                               bool local = false);
+static int row_tile_v_small(const Plan& pl, int64_t N, int sms);
+// Split rows summed inside the row kernel (combine_pieces): the plan's pieces are CTA-local
+// (d_slotpk), the call takes the fast path (TMA row kernel), and the block's pieces fit the stage
+// ring at the call's N tile (checked again in launch_main against the chosen stage depth).
+// SDNN_LOCAL_PIECES=0 keeps the workspace + split_reduce_kernel form (A/B runs).
+static bool row_pieces_local(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo) {
+  static const bool env_off = [] {
+    const char* e = getenv("SDNN_LOCAL_PIECES");
+    return e && atoi(e) == 0;
+  }();
+  const Plan& pl = h->plan;
+  return !env_off && h->d_slotpk && pl.kernel == 1 && N % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+         y_aligned16(yo) && int64_t(h->pieces_per_cta) <= int64_t(pl.k_chunk);
+}
 
 // N-tile width of the row / group kernels for a call: V = 8 floats per lane (TN = 256) when that
 // still gives ≥ 2 CTAs per SM worth of work units, else V = 4 (TN = 128).
@@ -2059,7 +2160,10 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   // split rows (row plan): a stream-ordered workspace for the pieces' partial sums, reduced after
   // the main kernel (no host synchronisation; allocation nodes under CUDA-graph capture)
   float* ws = nullptr;
-  const int32_t ns = int32_t(pl.split_row.size());
+  int32_t ns = int32_t(pl.split_row.size());
+  // CTA-local split rows on the row kernel's fast path: summed in shared memory by the kernel itself
+  const bool local = ns > 0 && row_pieces_local(h, X, N, yo);
+  if (local) ns = 0;
   if (ns > 0) {
     SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ws), pl.piece_row.size() * size_t(N) * 4,
                                           h->ws_pool, stream));
@@ -2071,7 +2175,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   if (KS > 1)
     SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws), size_t(KS) * pl.M * size_t(N) * 4,
                                           h->ws_pool, stream));
-  sdnn_status st = launch_main(h, X, N, bias, act, yo, ws, stream, kws, KS);
+  sdnn_status st = launch_main(h, X, N, bias, act, yo, ws, stream, kws, KS, local);
   if (KS > 1) {
     if (st == SDNN_OK) {
       const dim3 grid{unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))};
@@ -2141,7 +2245,7 @@ static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, cons
 
 // The row / group / generic kernels of a plan (everything but TMEM and codegen).
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
-                               const YOut& yo, float* ws, cudaStream_t stream, float* kws, int KS) {
+                               const YOut& yo, float* ws, cudaStream_t stream, float* kws, int KS, bool local) {
   const Plan& pl = h->plan;
   const int rw = pl.panel_rows, wc = pl.cta_panels;
   // V: widest N tile that still gives >= 2 CTAs per SM worth of work units.
@@ -2175,6 +2279,8 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
   p.ws = ws;
   p.kws = kws;
   p.M = pl.M;
+  // one stage holds k_chunk K rows of the N tile: ≥ pieces_per_cta slots of TN floats (row_pieces_local)
+  p.slotpk = local ? h->d_slotpk : nullptr;
 
   const bool fast = (N % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) && y_aligned16(yo) && pl.kernel < 4;
   if (fast) {
@@ -2241,6 +2347,7 @@ static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, cons
     SDNN_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
   } else {
     if (KS > 1) return fail(SDNN_ERR_INTERNAL, "split-K outside the row kernel's fast path");
+    if (p.slotpk) return fail(SDNN_ERR_INTERNAL, "CTA-local split rows outside the row kernel's fast path");
     p.stages = 1;
     const size_t smem = size_t(p.x_stage_bytes) + p.m_stage_bytes;
     const dim3 grid{unsigned(nblocks)}, block{unsigned(wc * 32)};
@@ -2375,6 +2482,7 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     cudaFree(h->d_blk_off);
     cudaFree(h->d_row_orig);
     cudaFree(h->d_split);
+    cudaFree(h->d_slotpk);
     if (h->ws_pool) cudaMemPoolDestroy(h->ws_pool);
     delete h;
     return fail(s, m);
@@ -2411,6 +2519,43 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
     tab.insert(tab.end(), pl.split_count.begin(), pl.split_count.end());
     e = cudaMalloc(&h->d_split, tab.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_split, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
+  }
+  // CTA-local split rows (row plans whose pieces of each row share a row block): per slot
+  // pk = L | cnt << 8 | is_first << 16 (L = the piece's index among its block's pieces, in piece-id
+  // order — a row's pieces are consecutive) and the target row (the first piece sums the group)
+  if (e == cudaSuccess && !pl.split_row.empty() && pl.kernel == 1) {
+    const int64_t rcta = int64_t(pl.panel_rows) * pl.cta_panels;
+    const size_t np = pl.piece_row.size();
+    std::vector<int64_t> slot_of(np, -1);
+    for (size_t sl = 0; sl < pl.row_orig.size(); ++sl)
+      if (pl.row_orig[sl] <= -2 && size_t(-2 - pl.row_orig[sl]) < np) slot_of[size_t(-2 - pl.row_orig[sl])] = int64_t(sl);
+    bool local = true;
+    std::vector<int32_t> srow(np, -1), cnt(np, 0), firstp(np, 0);
+    for (size_t i = 0; i < pl.split_row.size(); ++i)
+      for (int32_t k = 0; k < pl.split_count[i]; ++k) {
+        const size_t pid = size_t(pl.split_first[i] + k);
+        srow[pid] = pl.split_row[i];
+        cnt[pid] = pl.split_count[i];
+        firstp[pid] = pl.split_first[i];
+        if (slot_of[pid] < 0 || slot_of[pid] / rcta != slot_of[size_t(pl.split_first[i])] / rcta) local = false;
+      }
+    for (size_t pid = 0; pid < np && local; ++pid)
+      if (srow[pid] < 0 || cnt[pid] > 255) local = false;
+    if (local) {
+      std::vector<int2> tab(pl.row_orig.size(), make_int2(0, 0));
+      std::vector<int32_t> nblk(size_t(pl.num_row_blocks), 0);
+      // L: rank among the block's pieces by id (pieces are visited in id order)
+      for (size_t pid = 0; pid < np; ++pid) {
+        const int64_t sl = slot_of[pid];
+        const int32_t L = nblk[size_t(sl / rcta)]++;
+        tab[size_t(sl)] = make_int2(L | (cnt[pid] << 8) | (int32_t(firstp[pid]) == int32_t(pid) ? 1 << 16 : 0), srow[pid]);
+      }
+      for (int32_t v : nblk) h->pieces_per_cta = std::max(h->pieces_per_cta, v);
+      if (h->pieces_per_cta <= 255) {
+        e = cudaMalloc(&h->d_slotpk, tab.size() * sizeof(int2));
+        if (e == cudaSuccess) e = cudaMemcpy(h->d_slotpk, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice);
+      }
+    }
   }
   // workspace pool of the split-row pieces and the split-K slices (row and TMEM plans)
   if (e == cudaSuccess && pl.kernel != 3) {
@@ -2542,6 +2687,7 @@ sdnn_status sdnn_destroy(sdnn_handle h) {
   cudaFree(h->d_blk_off);
   cudaFree(h->d_row_orig);
   cudaFree(h->d_split);
+  cudaFree(h->d_slotpk);
   if (h->ws_pool) {
     cudaDeviceSynchronize();
     cudaMemPoolDestroy(h->ws_pool);

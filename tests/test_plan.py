@@ -283,6 +283,29 @@ def test_split_rows_balance():
         assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="row").info()["num_pieces"] == 0
 
 
+def test_split_row_pieces_share_a_row_block():
+    """The pieces of a split row sit on distinct warps of ONE row block (so the row kernel adds them in
+    shared memory at its end), at most one piece per warp of the block, consecutive piece ids."""
+    for key in ("c2_768x768", "c2_768x3072", "c2_3072x768"):
+        p = synth.config_problem(key, N=4)
+        plan = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="row")
+        info = plan.info()
+        rw, wc = info["panel_rows"], info["cta_panels"]
+        row_orig = plan.export()[0]
+        prow = plan.export_pieces()[0]
+        where = {}
+        for sl, o in enumerate(row_orig):
+            if o <= -2:
+                where[-2 - int(o)] = (sl // (rw * wc), sl // rw)
+        assert sorted(where) == list(range(len(prow)))
+        for r in np.unique(prow):
+            pids = np.flatnonzero(prow == r)
+            assert np.all(np.diff(pids) == 1) and 2 <= len(pids) <= wc
+            blocks = {where[int(i)][0] for i in pids}
+            warps = {where[int(i)][1] for i in pids}
+            assert len(blocks) == 1 and len(warps) == len(pids), (key, r)
+
+
 def test_auto_kernel_choice_and_alg1_benefit():
     """The cost model picks the group kernel where 16-row unions are small, and Algorithm 1 shrinks
     the unions on structured masks (the paper's reason for the permutation)."""

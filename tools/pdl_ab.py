@@ -61,7 +61,7 @@ def main():
         Y = torch.full_like(Y0, float("nan"))
         us = graph_time(lambda: h.spmm(X, b, act=1, out=Y), args.reps)
         ok = bool(torch.equal(Y, Y0))
-        print(json.dumps({"pdl": pdl, "config": key, "kernel": h.kernel_for(p.N, X.data_ptr(), Y.data_ptr()),
+        print(json.dumps({"pdl": pdl, "local_pieces": os.environ.get("SDNN_LOCAL_PIECES", "1"), "config": key, "kernel": h.kernel_for(p.N, X.data_ptr(), Y.data_ptr()),
                           "us": round(us, 2), "bitwise_eq_eager": ok}), flush=True)
     # dependent chain: Y1 = relu(W1 X + b1) (3072×768), Y2 = relu(W2 Y1 + b2) (768×3072)
     p1 = synth.config_problem("c2_3072x768")
@@ -82,7 +82,7 @@ def main():
         Y1.fill_(float("nan"))  # a third kernel writes Y1 after layer 2 read it (WAR across PDL launches)
 
     us = graph_time(chain, args.reps, launches=10)  # Y2 as the graph's last layer 2 wrote it
-    print(json.dumps({"pdl": pdl, "config": "ffn_chain_3072x768_768x3072", "us_per_pair": round(us, 2),
+    print(json.dumps({"pdl": pdl, "local_pieces": os.environ.get("SDNN_LOCAL_PIECES", "1"), "config": "ffn_chain_3072x768_768x3072", "us_per_pair": round(us, 2),
                       "bitwise_eq_eager": bool(torch.equal(Y2, Y2e))}), flush=True)
 
 
