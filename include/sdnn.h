@@ -103,9 +103,10 @@ typedef struct {
   int32_t max_block_bytes;  /* largest (row block, chunk) metadata block, bytes                       */
   int32_t alt_kernel;       /* auto handles: kernel of the second (TMEM) plan, else 0                 */
   int64_t max_panel_nnz;
-  int32_t num_split_rows;   /* row plan: rows split into pieces (their pieces are summed by a second
-                               small kernel, in piece order, before the bias: deterministic, but not
-                               bitwise equal to the unsplit summation order)                          */
+  int32_t num_split_rows;   /* row plan: rows split into pieces (≤ one per warp of ONE row block; the
+                               row kernel adds them in shared memory at its end — the generic path
+                               through a workspace and a second kernel — in piece order, before the
+                               bias: deterministic, but not bitwise equal to the unsplit order)      */
   int32_t num_pieces;       /* total pieces of the split rows                                         */
   int32_t narrow_row_blocks; /* auto handles: row blocks of the narrow row plan (4-row panels) taken by
                                row-plan calls whose grid is under one wave; 0 = none                 */
@@ -154,7 +155,11 @@ SDNN_API sdnn_status sdnn_destroy(sdnn_handle h);
  *   Y     device, M×N row-major fp32, written in ORIGINAL row order (the permutation is invisible);
  *         must not overlap X or bias
  *   stream cudaStream_t (NULL = legacy default stream).  The call enqueues and returns without a
- *         host synchronisation; device faults surface at the caller's next sync.
+ *         host synchronisation; device faults surface at the caller's next sync.  Kernels are
+ *         launched with programmatic dependent launch: a call's grid may start its prologue (barrier
+ *         setup, TMEM allocation, plan-metadata copies) while the previous kernel on `stream`
+ *         drains, and reads X / bias and writes Y only after that kernel has completed (stream
+ *         order is unchanged for the caller).
  * Fast path: X and Y 16-byte aligned and N % 4 == 0 (TMA tiles); otherwise a slower correct path.
  * Errors: INVALID_ARGUMENT (NULL handle/X/Y, N < 0, bad act, Y overlapping X or bias),
  * DEVICE_MISMATCH (current device ≠ handle device), CUDA (launch failure). */
@@ -317,6 +322,9 @@ SDNN_API int32_t sdnn_abi_version(void);
  *                    choice is between the two (small grids, no split-K)
  *   SDNN_TMEM_SPLIT_K 0 = never split the TMEM plan's K range
  *   SDNN_CONV_PX, SDNN_CONV_KS  sdnn_conv2d: force 2 | 4 output pixels per lane / this many K slices
+ *   SDNN_PDL         0 = launch without programmatic dependent launch (A/B runs)
+ *   SDNN_LOCAL_PIECES 0 = split rows through the workspace + reduction kernel even where the row
+ *                    kernel could add them in shared memory (A/B runs; bitwise the same Y)
  * (and, at build time, -DSDNN_DIAG=1|2: TMEM consumer without tcgen05.ld / without FFMA2). */
 
 #ifdef __cplusplus
