@@ -2170,7 +2170,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   }
   // split-K (row kernel, small grids): KS CTAs per (row block, N tile), each over a K-chunk range,
   // raw partial sums to a stream-ordered workspace, summed in slice order by splitk_reduce_kernel
-  const int KS = ns > 0 || pl.no_split_k ? 1 : (ks_force > 0 ? std::min(ks_force, pl.num_chunks) : splitk_for(h, N, X, yo));
+  const int KS = !pl.split_row.empty() || pl.no_split_k ? 1 : (ks_force > 0 ? std::min(ks_force, pl.num_chunks) : splitk_for(h, N, X, yo));
   float* kws = nullptr;
   if (KS > 1)
     SDNN_CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&kws), size_t(KS) * pl.M * size_t(N) * 4,
