@@ -209,14 +209,19 @@ def plan_geometry(p, info: dict, kid: int, kernel: str) -> dict:
             "num_row_blocks": info["num_row_blocks"]}
 
 
-def tmem_operand_bytes(p, N: int, kc: int = 64) -> int:
-    """TMEM → register bytes one launch of the TMEM kernel reads: every (row, K chunk) segment is
-    padded to whole pairs of entries, and each entry is one 512-byte tcgen05.ld.32x32b.x4 per
-    128-column N tile (4 bytes per entry per column of N; c5 encodes no 1×4 runs)."""
-    rows = np.repeat(np.arange(p.M), np.diff(p.row_ptr))
-    cnt = np.bincount(rows * ((p.K + kc - 1) // kc) + p.col_idx // kc, minlength=p.M * ((p.K + kc - 1) // kc))
-    padded = int(((cnt + 1) // 2 * 2).sum())
-    return padded * 4 * N
+def tmem_operand_bytes(p, N: int) -> int:
+    """TMEM → register bytes one launch of the TMEM kernel reads: one 512-byte tcgen05.ld.32x32b.x4
+    per 128-column N tile for every entry of the plan's metadata stream — the nonzeros plus the
+    zero-weight padding (4 bytes per entry per column of N; a 1×4 run's x16 load reads the same bytes
+    as its four entries).  Counted from the TMEM plan itself (host-side sdnn.Plan, the same arrays as
+    the handle's): every (row, K chunk) segment is padded to whole pairs."""
+    import paper_2101_07948_b200 as sdnn
+    plan = sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem")
+    info = plan.info()
+    _, blk_off, _ = plan.export()
+    hdr = (info["panel_rows"] * info["cta_panels"] * 4 + 15) // 16 * 16
+    entries = int(np.sum((np.diff(blk_off) - hdr) // 8))
+    return entries * 4 * N
 
 
 def bench_configs(sdnn, torch, dev, fp32_peak_tf: float, hbm_peak_gbs: float, with_parity: bool):
@@ -508,7 +513,7 @@ def run_product(args, rank: int, world: int, local_rank: int, dist):
     alg_bytes = p.nnz * 8 + (p.K + p.M) * Nr * 4
     hbm_gbs = alg_bytes / (ms_rank * 1e-3) / 1e9
     # design ceiling of the TMEM kernel: its operand path, tcgen05.ld.32x32b.x4 at 201.7 B/clk/SM
-    # (24 warps, profiles/r01_tmem_bw.log) over the padded entries it loads
+    # (24 warps, profiles/r01_tmem_bw.log) over the entries (nonzeros + padding) it loads
     design = None
     if abs(kid) == 4:
         tb = tmem_operand_bytes(p, Nr)
