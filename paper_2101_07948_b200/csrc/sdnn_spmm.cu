@@ -1586,14 +1586,18 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
       mbar_arrive(&mempty[m]);
     }
   }
-  // epilogue: panel rb·24 + warp; lane columns n0 + 4·lane
+  // epilogue: panel rb·24 + warp; lane columns n0 + 4·lane.  Lane r < RW loads row r's output row and
+  // bias (two global round trips for the warp instead of two per row: the loads of one row could not
+  // pass the previous row's store), then each row takes them by shuffle.
   pdl_wait();  // bias, Y / workspace
   const int64_t n = n0 + lane * 4;
+  const int32_t orow_l = lane < RW ? p.row_orig[(rb * kTmemRConsumers + warp) * RW + lane] : -1;
+  const float b_l = (p.bias && !SPLIT && orow_l >= 0) ? p.bias[orow_l] : 0.f;
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
-    const int32_t orow = p.row_orig[(rb * kTmemRConsumers + warp) * RW + r];
+    const int32_t orow = __shfl_sync(0xffffffffu, orow_l, r);
+    const float b = __shfl_sync(0xffffffffu, b_l, r);
     if (orow < 0) continue;
-    const float b = (p.bias && !SPLIT) ? p.bias[orow] : 0.f;
     float v[4] = {acc[r][0].x + b, acc[r][0].y + b, acc[r][1].x + b, acc[r][1].y + b};
     if (p.act == SDNN_ACT_RELU && !SPLIT) {
 #pragma unroll
