@@ -472,18 +472,27 @@ __device__ __forceinline__ void combine_pieces(const A (&acc)[RW][V / 2], const 
   }
 }
 
-// pre: the rows and biases loaded ahead (row_pre), or NULL: loaded here, row by row (fewer live registers)
+// pre: the rows and biases loaded ahead (row_pre), or NULL: loaded here — by lanes 0 .. RW − 1 at
+// once and shuffled to the warp per row (loads placed between the rows' stores would be serialised
+// behind them: two global round trips per row instead of two per warp).
 template <int RW, int V, bool VEC, typename A>
 __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParamsY& p, const RowPre<RW>* pre,
                                          int panel, int lane, int64_t n0) {
+  static_assert(RW <= 32, "one lane per row");
+  int32_t orow_l = -1;
+  float b_l = 0.f;
+  if (!pre) {
+    orow_l = lane < RW ? p.row_orig[panel * RW + lane] : -1;
+    b_l = (orow_l >= 0 && p.bias && !p.kws) ? p.bias[orow_l] : 0.f;
+  }
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
-    const int32_t orow = pre ? pre->orow[r] : p.row_orig[panel * RW + r];
+    const int32_t orow = pre ? pre->orow[r] : __shfl_sync(0xffffffffu, orow_l, r);
+    const float b = pre ? pre->b[r] : __shfl_sync(0xffffffffu, b_l, r);
     if (orow == -1 || (orow <= -2 && p.slotpk)) continue;  // CTA-local pieces: combine_pieces
     // a piece of a split row (row_orig = −2 − piece): its raw partial sums go to workspace row
     // `piece`; split_reduce_kernel adds the pieces, the bias and the activation
     const bool piece = orow <= -2 || p.kws;  // raw partial sums: a split row's piece or a split-K slice
-    const float b = pre ? pre->b[r] : (piece || !p.bias) ? 0.f : p.bias[orow];
     if constexpr (V == 2) {
       const int64_t n = n0 + lane * 2;
       const float2 a0 = as_f2(acc[r][0]);
@@ -1713,16 +1722,19 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
       };
       // the first chunks' metadata (plan memory) before the dependency wait, X after it; one item:
       // their offsets loaded together (a short K range's start-up is otherwise a chain of loads)
+      // one item: later chunks' offsets are read one chunk ahead, before the wait for a free slot
+      const int64_t* moff = p.blk_off + int64_t(rb) * p.nch + jr.x;
+      int64_t mlo = 0;  // the next metadata block's start offset (one item)
       if (q == 0) {
         if constexpr (!PERSIST) {
           static_assert(MS == 2, "prologue offsets for two metadata slots");
-          const int64_t* off = p.blk_off + int64_t(rb) * p.nch + jr.x;
-          const int64_t o0 = off[0], o1 = off[1], o2 = total > 1 ? off[2] : 0;
+          const int64_t o0 = moff[0], o1 = moff[1], o2 = total > 1 ? moff[2] : 0;
           for (int j = 0; j < MS && j < total; ++j) {
             const int64_t lo = j ? o1 : o0, hi = j ? o2 : o1;
             mbar_expect_tx(&mfull[j], uint32_t(hi - lo));
             bulk_load(mring + size_t(j) * p.m_stage_bytes, p.meta + lo, uint32_t(hi - lo), &mfull[j]);
           }
+          mlo = o2;
         } else {
           for (int j = 0; j < MS && j < total; ++j) load_meta(j);
         }
@@ -1737,8 +1749,16 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
           tc_fence_after();
         }
         if (q == 0 && j >= MS) {
-          mbar_wait(&mempty[j % MS], ((j / MS) - 1) & 1);
-          load_meta(j);
+          if constexpr (!PERSIST) {
+            const int64_t mhi = moff[j + 1];  // in flight during the wait
+            mbar_wait(&mempty[j % MS], ((j / MS) - 1) & 1);
+            mbar_expect_tx(&mfull[j % MS], uint32_t(mhi - mlo));
+            bulk_load(mring + size_t(j % MS) * p.m_stage_bytes, p.meta + mlo, uint32_t(mhi - mlo), &mfull[j % MS]);
+            mlo = mhi;
+          } else {
+            mbar_wait(&mempty[j % MS], ((j / MS) - 1) & 1);
+            load_meta(j);
+          }
         }
         mbar_wait(&slot_full[s], (j >> 1) & 1);
         jitter(p.dbg, uint32_t(j) * 11u + 4u);
