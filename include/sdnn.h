@@ -309,7 +309,8 @@ SDNN_API int32_t sdnn_abi_version(void);
  *   SDNN_TMEM_FILL   kernel 5's fill path: 1 = filler warps with tcgen05.st (default), 0 = one
  *                    producer thread with tcgen05.cp, 2 = both (odd/even pieces); kernels 4 / 6
  *                    always fill with tcgen05.cp.32x128b.warpx4
- *   SDNN_TMEM_PERSIST 1 = kernel 4 runs one CTA per SM over its (row block, N tile) items
+ *   SDNN_TMEM_PERSIST 1 / 0 = kernel 4 runs one CTA per SM over its (row block, N tile) items
+ *                    always / never (default: when K has ≤ 8 chunks and there are ≥ 4 items per SM)
  *   SDNN_JITTER      1 = pseudo-random sleeps at the pipelines' mbarrier hand-offs (protocol tests;
  *                    results unchanged, slower)
  *   SDNN_DEBUG_TMEM  bit mask, TMEM kernels: 1 skip the X loads (TMA), 2 skip the FMA loop, 4 skip the

@@ -2007,15 +2007,19 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     if (le != cudaSuccess) return fail(SDNN_ERR_CUDA, std::string("TMEM split-K: ") + cudaGetErrorString(le));
     return SDNN_OK;
   }
-  // persistent CTAs (one per SM, items round-robin through one chunk pipeline): opt-in experiment
-  // (SDNN_TMEM_PERSIST=1) — measured on the short-K BASELINE configs it gains on c4 2048×512 (+4-6 %)
-  // and loses on c3 512², c2 3072×768 and c4 512×2048 at 95 % (−5 to −9 %), c5 −4 %
-  // (profiles/r02_persist_ab.log), so the default keeps one CTA per item
+  // persistent CTAs (one per SM, items round-robin through one chunk pipeline): the next item's first
+  // chunks are fetched while the current item drains and stores its Y, and the CTA set-up (TMEM
+  // allocation, barriers) is paid once — worth it for short K ranges (≤ 8 chunks) over many items
+  // (≥ 4 per SM): c4 2048×512 at 80 / 95 % 197 → 188 µs, 103 → 99 µs; with fewer or longer items the
+  // static round-robin loses to the hardware's CTA scheduling (c3 512², c2 3072×768 +5 %, c4 512×2048
+  // at 95 % +13 %, c5 −4 %: profiles/r02_persist2_ab.log, r02_persist_ab.log).
+  // SDNN_TMEM_PERSIST=0 / 1 forces it off / on.
   static const int persist_env = [] {
     const char* e = getenv("SDNN_TMEM_PERSIST");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : -1;
   }();
-  const bool persist = rep && !prs && !multi && persist_env > 0;
+  const bool persist_auto = nblocks >= 4 * int64_t(h->sms) && pl.num_chunks <= 8;
+  const bool persist = rep && !prs && !multi && (persist_env > 0 || (persist_env < 0 && persist_auto));
   if (persist) {
     const unsigned pg = unsigned(std::min<int64_t>(nblocks, h->sms));
     if (h->tmem_runs)

@@ -31,6 +31,7 @@ CASES = [  # (problem, N, handle options)
     ("tsplit", 128, {}),                                    # TMEM-R split-K (4096², N = 128)
     ("c3_512x512", 1024, dict(kernel="tmemp")),             # row pairs
     ("c1", 1024, dict(kernel="tmem8")),                     # V = 8 TMEM kernel
+    ("c4_2048x512_s80", 12544, dict(kernel="tmem")),        # TMEM-R, persistent by default (882 items, 8 chunks)
 ]
 
 SCRIPT = r'''
@@ -80,8 +81,9 @@ def test_jittered_pipelines_bitwise(tmp_path):
 
 
 def test_persistent_tmem_ctas_bitwise(tmp_path):
-    """SDNN_TMEM_PERSIST=1 (opt-in): one CTA per SM runs its (row block, N tile) items through one
-    chunk pipeline — same per-row order, so Y is bitwise the default launch's (TMEM-R cases only)."""
+    """SDNN_TMEM_PERSIST=1 (forced; by default only short K ranges over ≥ 4 items per SM): one CTA per
+    SM runs its (row block, N tile) items through one chunk pipeline — same per-row order, so Y is
+    bitwise the default launch's (TMEM-R cases only)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     out = tmp_path / "persist.npz"
