@@ -85,11 +85,12 @@ def test_conv_split_k(sdnn):
 
 @pytest.mark.parametrize("C,HW", [(128, 14), (64, 7)])
 def test_conv_tune(sdnn, C, HW):
-    """sdnn_conv2d_tune keeps a tile choice per geometry; tuned results match the oracle."""
+    """sdnn_conv2d_tune keeps a choice per geometry (pixels per lane of the patch form, or −2: the
+    explicit form, im2col + TMEM-R SpMM); tuned results match the oracle."""
     p = synth.make_conv_problem(f"ctn{C}_{HW}", C, C, HW, HW, 4, 0.9)
     h = sdnn.Handle.for_conv(p.row_ptr, p.col_idx, p.vals, p.OC, p.IC, 3, 3)
     r = h.conv2d_tune(torch.from_numpy(p.x()).cuda())
-    assert r["pixels"] in (0, 2, 4) and r["us"] > 0
+    assert r["pixels"] in (-2, 0, 2, 4) and r["us"] > 0
     Xc = p.x()
     Y = h.conv2d(torch.from_numpy(Xc).cuda(), 3, 3, 1, 1, torch.from_numpy(p.bias).cuda(), act=1).cpu().numpy()
     Yo, S = oconv.conv2d(p.row_ptr, p.col_idx, p.vals, p.OC, p.IC, 3, 3, Xc, 1, 1, p.bias, 1)
