@@ -574,23 +574,43 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, const int32_t*
   }
 }
 
-// Split-K (row kernel): Y[row] = act(Σ_{s < KS} kws[s][row] (slice order) + b[row]).  One thread per
-// column; blockIdx.y = row.
+// Split-K (row / TMEM / conv kernels): Y[row] = act(Σ_{s < KS} kws[s][row] (slice order) + b[row]).
+// One thread per column (C = 1) or per 4 columns (C = 4: N % 4 == 0, 16-byte aligned destinations —
+// float4 loads and stores, the same additions in the same order); blockIdx.y = row.
+template <int C>
 __global__ void splitk_reduce_kernel(const float* __restrict__ kws, int32_t KS, int32_t M, const float* __restrict__ bias,
                                      int32_t act, const YOut yo, int64_t N) {
   pdl_trigger();
   pdl_wait();
-  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * C;
   if (n >= N) return;
   const int64_t slice = int64_t(M) * N;
   for (int32_t row = int32_t(blockIdx.y); row < M; row += int32_t(gridDim.y)) {  // gridDim.y ≤ 65535
-    float v = kws[int64_t(row) * N + n];
-    for (int32_t s = 1; s < KS; ++s) v += kws[s * slice + int64_t(row) * N + n];
-    if (bias) v += bias[row];
-    if (act == SDNN_ACT_RELU) v = v > 0.f ? v : 0.f;
+    float v[C];
+    const float* src = kws + int64_t(row) * N + n;
+    if constexpr (C == 4) {
+      const float4 a = *reinterpret_cast<const float4*>(src);
+      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+      for (int32_t s = 1; s < KS; ++s) {
+        const float4 b = *reinterpret_cast<const float4*>(src + s * slice);
+        v[0] += b.x, v[1] += b.y, v[2] += b.z, v[3] += b.w;
+      }
+    } else {
+      v[0] = src[0];
+      for (int32_t s = 1; s < KS; ++s) v[0] += src[s * slice];
+    }
 #pragma unroll
-    for (int d = 0; d < kMaxDst; ++d)  // static indices: yo stays in the parameter bank (no local copy)
-      if (d < yo.n) y_st1(yo.y[d] + int64_t(row) * yo.ld + yo.col0 + n, v, yo.mc);
+    for (int c = 0; c < C; ++c) {
+      if (bias) v[c] += bias[row];
+      if (act == SDNN_ACT_RELU) v[c] = v[c] > 0.f ? v[c] : 0.f;
+    }
+#pragma unroll
+    for (int d = 0; d < kMaxDst; ++d) {  // static indices: yo stays in the parameter bank (no local copy)
+      if (d >= yo.n) continue;
+      float* dst = yo.y[d] + int64_t(row) * yo.ld + yo.col0 + n;
+      if constexpr (C == 4) y_st4(dst, v[0], v[1], v[2], v[3], yo.mc);
+      else y_st1(dst, v[0], yo.mc);
+    }
   }
 }
 
@@ -1870,6 +1890,18 @@ static cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
+// The split-K reduction of a call (raw slices kws[0..KS) of M × N each): the float4 form when N % 4 == 0
+// and every destination is 16-byte aligned (the split paths' workspace always is).
+static cudaError_t launch_splitk_reduce(const float* kws, int32_t KS, int32_t M, const float* bias, int32_t act,
+                                        const YOut& yo, int64_t N, cudaStream_t st) {
+  const unsigned rows = unsigned(std::min(M, 65535));
+  if (N % 4 == 0 && y_aligned16(yo))
+    return launch_k(splitk_reduce_kernel<4>, dim3(unsigned((N / 4 + 255) / 256), rows), 256, 0, st, kws, KS, M, bias,
+                    act, yo, N);
+  return launch_k(splitk_reduce_kernel<1>, dim3(unsigned((N + 255) / 256), rows), 256, 0, st, kws, KS, M, bias, act,
+                  yo, N);
+}
+
 static sdnn_status launch_codegen(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                   const YOut& yo, cudaStream_t stream) {
   const Plan& pl = h->plan;
@@ -1999,8 +2031,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     else spmm_tmem_kernel<8, 1, false, true><<<g2, threads, smem, stream>>>(tmap, q);
     cudaError_t le = cudaGetLastError();
     if (le == cudaSuccess) {
-      launch_k(splitk_reduce_kernel, dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, stream, kws, KS, pl.M, bias, act,
-                                                                                                 yo, N);
+      launch_splitk_reduce(kws, KS, pl.M, bias, act, yo, N, stream);
       le = cudaGetLastError();
     }
     cudaFreeAsync(kws, stream);
@@ -2206,8 +2237,7 @@ static sdnn_status launch_row(sdnn_handle_s* h, const float* X, int64_t N, const
   sdnn_status st = launch_main(h, X, N, bias, act, yo, ws, stream, kws, KS, local);
   if (KS > 1) {
     if (st == SDNN_OK) {
-      const dim3 grid{unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))};
-      launch_k(splitk_reduce_kernel, grid, 256, 0, stream, kws, KS, pl.M, bias, act, yo, N);
+      launch_splitk_reduce(kws, KS, pl.M, bias, act, yo, N, stream);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) st = fail(SDNN_ERR_CUDA, std::string("splitk_reduce_kernel: ") + cudaGetErrorString(le));
     }
@@ -2966,8 +2996,7 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
       cudaError_t le = cudaLaunchKernel(fn2, dim3(unsigned(nb2), unsigned(KS)), dim3(unsigned(wc * 32)), args2,
                                         smem2, st_);
       if (le == cudaSuccess && KS > 1) {
-        launch_k(splitk_reduce_kernel, dim3(unsigned((N + 255) / 256), unsigned(std::min(pl.M, 65535))), 256, 0, st_, kws, KS, pl.M, bias, act,
-                                                                                                y_single(Y, N), N);
+        launch_splitk_reduce(kws, KS, pl.M, bias, act, y_single(Y, N), N, st_);
         le = cudaGetLastError();
       }
       if (KS > 1) cudaFreeAsync(kws, st_);
