@@ -512,7 +512,9 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
                       : single ? p.Y + int64_t(orow) * p.N
                                : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
         const bool mc = !single && !p.kws && p.yo.mc;
-        if (VEC) {
+        if (VEC && piece) {  // raw partial sums: plain stores, kept in L2 for the reduction kernel
+          if (n < p.N) *reinterpret_cast<float2*>(yrow + n) = make_float2(v[0], v[1]);
+        } else if (VEC) {
           if (n < p.N) y_st2(yrow + n, v[0], v[1], mc);
         } else {
           if (n < p.N) y_st1(yrow + n, v[0], mc);
@@ -542,7 +544,9 @@ __device__ __forceinline__ void epilogue(const A (&acc)[RW][V / 2], const KParam
                       : single ? p.Y + int64_t(orow) * p.N
                                : p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0;
         const bool mc = !single && !p.kws && p.yo.mc;
-        if (VEC) {
+        if (VEC && piece) {  // raw partial sums: plain stores, kept in L2 for the reduction kernel
+          if (n < p.N) *reinterpret_cast<float4*>(yrow + n) = make_float4(v[0], v[1], v[2], v[3]);
+        } else if (VEC) {
           if (n < p.N) y_st4(yrow + n, v[0], v[1], v[2], v[3], mc);
         } else {
 #pragma unroll
@@ -1029,7 +1033,10 @@ __global__ void __launch_bounds__(16 * 32, 2) spmm_conv2_kernel(const KParamsY p
     for (int q = 0; q < PX; ++q) {
       const int64_t n = n0 + lane + 32 * q;
       const float y = (p.act == SDNN_ACT_RELU && !p.kws) ? (v[q] > 0.f ? v[q] : 0.f) : v[q];
-      if (n < p.N) __stcs(yrow + n, y);
+      if (n < p.N) {
+        if (p.kws) yrow[n] = y;  // split-K slice: kept in L2 for the reduction kernel
+        else __stcs(yrow + n, y);
+      }
     }
   }
 }
@@ -1255,8 +1262,8 @@ __device__ __forceinline__ void tmem_consume(const TmemParams<MULTI || SPLIT>& p
       }
       if constexpr (SPLIT) {  // split-K slice: raw partial sums (splitk_reduce_kernel adds bias, act)
         if (n < p.N)
-          __stcs(reinterpret_cast<float4*>(p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N + n),
-                 make_float4(v[0], v[1], v[2], v[3]));
+          *reinterpret_cast<float4*>(p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N + n) =
+              make_float4(v[0], v[1], v[2], v[3]);  // L2-resident for the reduction (no streaming hint)
       } else if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
         if (n < p.N)
           for (int d = 0; d < p.yo.n; ++d)
@@ -1634,8 +1641,8 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
     }
     if (n >= p.N) continue;
     if constexpr (SPLIT) {  // split-K slice: raw partial sums (splitk_reduce_kernel adds bias, act)
-      __stcs(reinterpret_cast<float4*>(p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N + n),
-             make_float4(v[0], v[1], v[2], v[3]));
+      // plain store: the slices stay in L2 for splitk_reduce_kernel (a streaming store sent them to DRAM)
+      *reinterpret_cast<float4*>(p.kws + (int64_t(blockIdx.y) * p.M + orow) * p.N + n) = make_float4(v[0], v[1], v[2], v[3]);
     } else if constexpr (MULTI) {  // sdnn_spmm_multi: every destination, leading dimension ld, offset col0
       for (int d = 0; d < p.yo.n; ++d)
         y_st4(p.yo.y[d] + int64_t(orow) * p.yo.ld + p.yo.col0 + n, v[0], v[1], v[2], v[3], p.yo.mc);
