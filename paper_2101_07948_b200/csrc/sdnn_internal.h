@@ -108,7 +108,13 @@ SDNN_HD constexpr int tmem_pad(int V) { return 2; }  // row segments padded to w
 constexpr int kTmemPanels = 6;        // kernel 5: warp slots per lane quarter
 constexpr int kTmemRWarps = 24;       // kernel 4: consumer warps (= panels per row block)
 constexpr int kTmemPieces = 4;        // kernel 5: smem ring depth (32 KB TMA pieces)
-constexpr int kTmemRPieces = 8;       // kernel 4: smem ring depth (8 KB TMA pieces: 16 K rows × 128 columns)
+#ifndef SDNN_TMEMR_PIECES
+#define SDNN_TMEMR_PIECES 8
+#endif
+// kernel 4: smem ring depth (8 KB TMA pieces: 16 K rows × 128 columns; 4 per K chunk, one per issuer):
+// two K chunks of X in flight; four (16 pieces) measured 0.3-1.5 % slower on every config
+// (profiles/r02_ring_depth_ab.log) — the TMEM double buffer, not the TMA latency, paces the fill
+constexpr int kTmemRPieces = SDNN_TMEMR_PIECES;
 inline int tmem_v(int kernel) { return kernel == 5 ? 8 : 4; }
 inline int tmem_tn(int kernel) { return kernel == 5 ? 1024 : 128; }  // N tile of a TMEM plan
 // N granularity of a TMEM plan's fast path: kernels 4 / 6 read X through a 2-D tensor map (any

@@ -1664,6 +1664,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
   constexpr int PK = 16;          // K rows per TMA piece
   constexpr int PPC = 64 / PK;    // pieces per K chunk
   constexpr int S = kTmemRPieces, MS = kTmemRMetaSlots;
+  constexpr int D = kTmemRPieces / 4;  // K chunks of X in flight in shared memory (4 issuers × D slots)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = blockIdx.x % p.nrb;
   const int64_t n0 = int64_t(blockIdx.x / p.nrb) * 128;
@@ -1726,7 +1727,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
         }
       };
       auto load_piece = [&](int g) {
-        const int s = q + 4 * (g & 1);
+        const int s = q + 4 * (g % D);
         if (p.dbg & 1) {
           mbar_arrive(&slot_full[s]);
           return;
@@ -1767,9 +1768,9 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
         }
       }
       pdl_wait();
-      for (int j = 0; j < 2 && j < total; ++j) load_piece(j);
+      for (int j = 0; j < D && j < total; ++j) load_piece(j);
       for (int j = 0; j < total; ++j) {
-        const int h = j & 1, s = q + 4 * h;
+        const int h = j & 1, s = q + 4 * (j % D);
         jitter(p.dbg, uint32_t(j) * 5u + 3u);
         if (j >= 2) {  // half h held chunk j−2: wait until every consumer is done with it
           mbar_wait_sleep(&tfree[h], ((j >> 1) - 1) & 1);
@@ -1787,7 +1788,7 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
             load_meta(j);
           }
         }
-        mbar_wait(&slot_full[s], (j >> 1) & 1);
+        mbar_wait(&slot_full[s], (j / D) & 1);
         jitter(p.dbg, uint32_t(j) * 11u + 4u);
         const uint32_t src = smem_u32(xring + size_t(s) * kTmemRPieceBytes);
 #pragma unroll
@@ -1796,9 +1797,9 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
                        "l"(cp_desc(src + uint32_t(kk) * 512)) : "memory");
         tc_commit(&slot_empty[s]);
         tc_commit(&tfull[h]);
-        if (j + 2 < total) {
-          mbar_wait(&slot_empty[s], (j >> 1) & 1);
-          load_piece(j + 2);
+        if (j + D < total) {  // this slot's next chunk (its copies above must have read it first)
+          mbar_wait(&slot_empty[s], (j / D) & 1);
+          load_piece(j + D);
         }
       }
     }
