@@ -41,7 +41,8 @@
 #include "group_entry.inc"
 
 #ifndef SDNN_DIAG
-#define SDNN_DIAG 0  // diagnostics builds only (1: no TMEM loads, 2: no FFMA2); never set in the product
+#define SDNN_DIAG 0  // diagnostics builds only (kernel 5: 1 no TMEM loads, 2 no FFMA2; TMEM-R: 3 no consumer
+                     // entry loop, 4 no tcgen05.cp fill); never set in the product
 #endif
 
 namespace sdnn {
@@ -1520,6 +1521,10 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
     // row ahead)
     uint32_t hn = hdr[0];
     const float4* e = reinterpret_cast<const float4*>(ms + p.hdr_bytes) + (hn >> 17);
+#if SDNN_DIAG == 3  // diagnostics build: consumers skip their entry streams (barrier hand-offs only)
+    if (true) {
+    } else
+#endif
     if constexpr (PAIRS) {  // kernel 6: Algorithm 1 row pairs (rows 2i, 2i+1): shared columns, then each row's own
 #pragma unroll
       for (int i = 0; i < RW / 2; ++i) {
@@ -1791,10 +1796,12 @@ __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
         mbar_wait(&slot_full[s], (j / D) & 1);
         jitter(p.dbg, uint32_t(j) * 11u + 4u);
         const uint32_t src = smem_u32(xring + size_t(s) * kTmemRPieceBytes);
+#if SDNN_DIAG != 4  // diagnostics build 4: no smem → TMEM copies (commits only)
 #pragma unroll
         for (int kk = 0; kk < PK; ++kk)
           asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tbase + uint32_t(h * 256 + (q * PK + kk) * 4)),
                        "l"(cp_desc(src + uint32_t(kk) * 512)) : "memory");
+#endif
         tc_commit(&slot_empty[s]);
         tc_commit(&tfull[h]);
         if (j + D < total) {  // this slot's next chunk (its copies above must have read it first)
