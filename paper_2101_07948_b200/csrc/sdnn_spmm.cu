@@ -105,6 +105,7 @@ struct sdnn_handle_s {
   mutable std::mutex tune_mu;
   int32_t sms = 148;
   bool tmem_runs = true;  // kernel 4 plan with aligned 1×4 runs in its metadata (else the run-free consumer)
+  bool tmem_runs_only = false;  // ... and nothing else (every row segment is whole runs)
   HostStage hs;         // sdnn_spmm_host staging (created on first use)
   std::mutex host_mu;
 };
@@ -1499,7 +1500,8 @@ constexpr size_t tmemr_smem_bytes(int m_stage_bytes) {
 // g0: global index of this item's first chunk in the CTA's chunk stream (persistent CTAs run several
 // (row block, N tile) items through one pipeline; 0 otherwise) — it fixes the TMEM half, the
 // metadata slot and the mbarrier phases of every chunk.
-template <bool MULTI, bool SPLIT, bool RUNS, int RW, bool PAIRS = false>
+// RUNS: 0 no 1×4 runs in the plan, 1 leading runs then ordinary entries, 2 every entry in a run
+template <bool MULTI, bool SPLIT, int RUNS, int RW, bool PAIRS = false>
 __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& p, uint8_t* mring, uint64_t* mfull,
                                               uint64_t* mempty, uint64_t* tfull, uint64_t* tfree, int rb, int64_t n0,
                                               int warp, int lane, int g0 = 0) {
@@ -1596,6 +1598,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
           fma4(acc[r], e1.w, xd);
         }
       }
+      if constexpr (RUNS == 2) continue;  // every entry was in a run (no per-row tail checks)
       for (; n >= 4; n -= 4, e += 2) {  // two pairs: four loads in flight
         const float4 e0 = e[0], e1 = e[1];
         float4 xa, xb, xc, xd;
@@ -1661,7 +1664,7 @@ __device__ __forceinline__ void tmemr_consume(const TmemParams<MULTI || SPLIT>& 
 // through one continuous chunk pipeline — the issuers fetch the next item's chunks while the
 // consumers finish the current item and store its Y — for short K ranges, where a CTA's pipeline
 // start-up and drain are a large part of its life.
-template <bool MULTI = false, bool SPLIT = false, bool RUNS = true, int RW = tmem_rows(4), bool PAIRS = false,
+template <bool MULTI = false, bool SPLIT = false, int RUNS = 1, int RW = tmem_rows(4), bool PAIRS = false,
           bool PERSIST = false>
 __global__ void __launch_bounds__((kTmemRConsumers + 4) * 32, 1)
     spmm_tmemr_kernel(const __grid_constant__ CUtensorMap tmap, const TmemParams<MULTI || SPLIT> p) {
@@ -2068,7 +2071,10 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   const bool persist = rep && !prs && !multi && (persist_env > 0 || (persist_env < 0 && persist_auto));
   if (persist) {
     const unsigned pg = unsigned(std::min<int64_t>(nblocks, h->sms));
-    if (h->tmem_runs)
+    if (h->tmem_runs_only)
+      launch_k(spmm_tmemr_kernel<false, false, 2, tmem_rows(4), false, true>, pg, threads, smem, stream,
+               tmap, static_cast<const KParams&>(p));
+    else if (h->tmem_runs)
       launch_k(spmm_tmemr_kernel<false, false, true, tmem_rows(4), false, true>, pg, threads, smem, stream, 
           tmap, static_cast<const KParams&>(p));
     else
@@ -2081,6 +2087,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   else if (prs)
     launch_k(spmm_tmemr_kernel<false, false, false, tmem_rows(4), true>, grid, threads, smem, stream, tmap, static_cast<const KParams&>(p));
   else if (rep && multi) launch_k(spmm_tmemr_kernel<true, false>, grid, threads, smem, stream, tmap, p);
+  else if (rep && h->tmem_runs_only) launch_k(spmm_tmemr_kernel<false, false, 2>, grid, threads, smem, stream, tmap, static_cast<const KParams&>(p));
   else if (rep && h->tmem_runs) launch_k(spmm_tmemr_kernel<false, false, true>, grid, threads, smem, stream, tmap, static_cast<const KParams&>(p));
   else if (rep) launch_k(spmm_tmemr_kernel<false, false, false>, grid, threads, smem, stream, tmap, static_cast<const KParams&>(p));
   else if (multi) spmm_tmem_kernel<8, 1, true><<<grid, threads, smem, stream>>>(tmap, p);
@@ -2530,6 +2537,12 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
       ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
     if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget + 1024);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, 2, tmem_rows(4), false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+    if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(spmm_tmemr_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBudget + 1024);
 
@@ -2569,18 +2582,20 @@ static sdnn_status prepare_one(const int32_t* csr_ptr, const int32_t* col_idx, c
   if (e != cudaSuccess)
     return cleanup(e == cudaErrorMemoryAllocation ? SDNN_ERR_OUT_OF_MEMORY : SDNN_ERR_CUDA,
                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
-  if (pl.kernel == 4) {  // any aligned 1×4 runs (header bits 8..15)?  else launches take the run-free consumer
+  if (pl.kernel == 4) {  // any aligned 1×4 runs (header bits 8..15)?  else launches take the run-free consumer;
+    // runs only (every segment = its runs: block-clustered masks) → the consumer without tail checks
     h->tmem_runs = false;
+    h->tmem_runs_only = true;
     const int64_t rcta = int64_t(pl.panel_rows) * pl.cta_panels;
-    for (size_t b = 0; b + 1 < pl.blk_off.size() && !h->tmem_runs; ++b)
+    for (size_t b = 0; b + 1 < pl.blk_off.size(); ++b)
       for (int64_t sl = 0; sl < rcta; ++sl) {
         uint32_t hw;
         std::memcpy(&hw, pl.meta.data() + pl.blk_off[b] + sl * 4, 4);
-        if ((hw >> 8) & 0xffu) {
-          h->tmem_runs = true;
-          break;
-        }
+        const uint32_t runs = (hw >> 8) & 0xffu, cnt = hw & 0xffu;
+        h->tmem_runs |= runs != 0;
+        h->tmem_runs_only &= cnt == 4 * runs;
       }
+    h->tmem_runs_only &= h->tmem_runs;
   }
   if (!pl.meta.empty()) e = cudaMemcpy(h->d_meta, pl.meta.data(), pl.meta.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(h->d_blk_off, pl.blk_off.data(), pl.blk_off.size() * 8, cudaMemcpyHostToDevice);
