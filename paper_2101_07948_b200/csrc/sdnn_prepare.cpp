@@ -576,9 +576,9 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
       std::vector<std::vector<int32_t>> rows(nw);
       // 1. the split rows' pieces, heaviest row first: the row block whose least-loaded free warps
       //    take the pieces with the smallest resulting maximum load (lowest block on ties), one piece
-      //    per warp.  Bounded work (groups × blocks); beyond it, or if no block has room, the pieces
+      //    per warp.  Bounded work (groups × warps); beyond it, or if no block has room, the pieces
       //    go through the LPT below like rows (anywhere: workspace + reduction kernel instead).
-      bool local = !groups.empty() && int64_t(groups.size()) * g.nrb <= 4000000;
+      bool local = !groups.empty() && int64_t(groups.size()) * g.nrb * g.wc <= 8000000;
       std::stable_sort(groups.begin(), groups.end(),
                        [](const auto& a, const auto& b) { return a.first > b.first; });
       std::vector<char> placed(out ? out->row.size() : 0, 0);
