@@ -352,9 +352,12 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
     if (o.permute != 0 && o.permute != 1) return fail(SDNN_ERR_INVALID_ARGUMENT, "permute must be 0 or 1");
     if (o.kernel < 0 || o.kernel > 6) return fail(SDNN_ERR_INVALID_ARGUMENT, "kernel must be 0..6");
     if (o.kernel == 4 || o.kernel == 5 || o.kernel == 6) {
-      if (o.panel_rows_max != 0 || o.cta_panels != 0 || (o.k_chunk != 0 && o.k_chunk != tmem_kc(tmem_v(o.kernel))) ||
+      // kernel 4 alone takes panel_rows_max = 1..10: about that many rows per warp (more row blocks)
+      const bool rows_ok = o.panel_rows_max == 0 || (o.kernel == 4 && o.panel_rows_max >= 1 && o.panel_rows_max <= tmem_rows(4));
+      if (!rows_ok || o.cta_panels != 0 || (o.k_chunk != 0 && o.k_chunk != tmem_kc(tmem_v(o.kernel))) ||
           o.group_sb != 0)
-        return fail(SDNN_ERR_INVALID_ARGUMENT, "the TMEM kernel has a fixed geometry (leave the tiling options 0)");
+        return fail(SDNN_ERR_INVALID_ARGUMENT,
+                    "the TMEM kernels have a fixed geometry (tiling options 0; kernel 4: panel_rows_max 1..10)");
     } else if (o.kernel == 3) {
       if (o.panel_rows_max < 0 || o.panel_rows_max > kCgMaxRows)
         return fail(SDNN_ERR_INVALID_ARGUMENT, "panel_rows_max must be 0..128 with the codegen kernel");
@@ -456,6 +459,11 @@ sdnn_status build_plan(const int32_t* csr_ptr, const int32_t* col_idx, const flo
         g.wc = (kernel == 4 || kernel == 6) ? kTmemRWarps : kTmemPanels;
         g.pairs = kernel == 6;
         g.nrb = (M + g.rw * g.wc - 1) / (g.rw * g.wc);
+        // kernel 4 with panel_rows_max = r < 10: row blocks for ~r rows per warp (the panels' slots
+        // partly empty) — more, lighter CTAs for calls whose grid would fill its last wave badly
+        if (kernel == 4 && o.panel_rows_max > 0 && o.panel_rows_max < g.rw)
+          g.nrb = std::max(g.nrb, int32_t((int64_t(M) + int64_t(o.panel_rows_max) * g.wc - 1) /
+                                          (int64_t(o.panel_rows_max) * g.wc)));
         return g;
       }
       g.kernel = kernel;

@@ -88,6 +88,9 @@ struct sdnn_handle_s {
   // auto handles (kernel = 0): the TMEM plan prepared beside the row plan; sdnn_spmm takes it when
   // the call fits its fast path and fills at least one wave of CTAs (tmem_worth)
   sdnn_handle_s* alt = nullptr;
+  // auto handles, small M: the same TMEM plan with ~8 rows per warp (more row blocks) — taken per call
+  // when its grid fills the GPU's waves better (tmem_pick); not serialized (rebuilt plans use alt)
+  sdnn_handle_s* alt8 = nullptr;
   // auto handles: a row plan with more, smaller row blocks, for row-plan calls whose grid on the
   // main row plan is under one wave (small N: one or two N tiles)
   sdnn_handle_s* narrow = nullptr;
@@ -2109,6 +2112,24 @@ static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                const YOut& yo, float* ws, cudaStream_t stream, float* kws = nullptr, int KS = 1,
                                bool local = false);
+// The TMEM plan of an auto call: the 10-rows-per-warp plan or, where the handle has one, the ~8-row plan
+// with more row blocks — whichever gives the smaller waves × (rows per warp + 1.5) for this N (one CTA
+// per SM; the 1.5 rows stand for a CTA's fixed fill and set-up).  Graph-timed with the 8-row plan
+// forced (profiles/r02_tmem_rows_ab.log): c2 3072×768 30.7 → 27.4 µs (104 → 128 CTAs, one wave),
+// c3 1024×512 50.3 → 44.9 µs (245 → 294 CTAs, two waves either way); c5 34.3 → 36.5 ms and c4
+// 2048×512 at 80 % 174 → 197 µs (more waves) — which the estimate rejects.
+static sdnn_handle_s* tmem_pick(sdnn_handle_s* h, int64_t N) {
+  sdnn_handle_s* a = h->alt;
+  sdnn_handle_s* b = h->alt8;
+  if (!a || !b) return a;
+  const int64_t T = (N + tmem_tn(a->plan.kernel) - 1) / tmem_tn(a->plan.kernel);
+  auto est = [&](const sdnn_handle_s* x) {
+    const int64_t nrb = x->plan.num_row_blocks;
+    const double waves = double((nrb * T + h->sms - 1) / h->sms);
+    return waves * (double(x->plan.M) / double(nrb * kTmemRWarps) + 1.5);
+  };
+  return est(b) < est(a) ? b : a;
+}
 static int row_tile_v_small(const Plan& pl, int64_t N, int sms);
 // Split rows summed inside the row kernel (combine_pieces): the plan's pieces are CTA-local
 // (d_slotpk), the call takes the fast path (TMA row kernel), and the block's pieces fit the stage
@@ -2312,7 +2333,7 @@ static sdnn_status launch_auto(sdnn_handle_s* h, const float* X, int64_t N, cons
                                const YOut& yo, cudaStream_t stream) {
   if (const int ks = tmem_split_for(h, X, N, yo); ks > 1)
     return launch_tmem(h->alt, X, N, bias, act, yo, stream, ks, h->ws_pool);
-  if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(h->alt, X, N, bias, act, yo, stream);
+  if (tmem_worth(h->alt, X, N, yo)) return launch_tmem(tmem_pick(h, N), X, N, bias, act, yo, stream);
   if (sdnn_handle_s* nw = narrow_pick(h, N)) return launch(nw, X, N, bias, act, yo, stream);
   const Plan& pl = h->plan;
   if (pl.kernel == 3) return launch_codegen(h, X, N, bias, act, yo, stream);
@@ -2710,6 +2731,13 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
     return fail(st, m);
   }
   (*out)->alt = alt;
+  // the ~8-rows-per-warp TMEM plan, when it has more row blocks than the 10-row one
+  if (alt && int64_t(alt->plan.num_row_blocks) < (int64_t(M) + 8 * kTmemRWarps - 1) / (8 * kTmemRWarps)) {
+    sdnn_perm_opts o8 = o;
+    o8.panel_rows_max = 8;
+    sdnn_handle alt8 = nullptr;
+    if (prepare_one(csr_ptr, col_idx, vals, M, K, &o8, &alt8, perm) == SDNN_OK) (*out)->alt8 = alt8;
+  }
   // and, when the row plan has few row blocks, a row plan of 4-row panels with ≥ 64 row blocks for
   // the calls whose grid would not fill the GPU (launch: narrow_worth)
   const Plan& wide = (*out)->plan;
@@ -2752,6 +2780,7 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
 sdnn_status sdnn_destroy(sdnn_handle h) {
   if (!h) return SDNN_OK;
   if (h->alt) sdnn_destroy(h->alt);
+  if (h->alt8) sdnn_destroy(h->alt8);
   if (h->narrow) sdnn_destroy(h->narrow);
   if (h->narrow4) sdnn_destroy(h->narrow4);
   int cur = -1;
@@ -2936,7 +2965,7 @@ static sdnn_status conv2d_impl(sdnn_handle h, const float* X, int32_t B, int32_t
         if (const int ks = tmem_split_for(h, xv, N, yo1); ks > 1)
           st2 = launch_tmem(h->alt, xv, N, bias, act, yo1, static_cast<cudaStream_t>(stream), ks, h->ws_pool);
         else
-          st2 = launch_tmem(h->alt, xv, N, bias, act, yo1, static_cast<cudaStream_t>(stream));
+          st2 = launch_tmem(tmem_pick(h, N), xv, N, bias, act, yo1, static_cast<cudaStream_t>(stream));
       }
       cudaFreeAsync(xv, static_cast<cudaStream_t>(stream));
       return st2;

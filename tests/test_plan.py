@@ -347,7 +347,16 @@ def test_tmem_runs_marked_on_block_clustered_masks():
 def test_tmem_plan_options():
     p = synth.config_problem("c1", N=4)
     with pytest.raises(sdnn.SdnnError):
-        sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem", panel_rows=8)
+        sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem", panel_rows=11)
+    with pytest.raises(sdnn.SdnnError):
+        sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem8", panel_rows=4)
+    # kernel 4, panel_rows = r: about r rows per warp (more row blocks of 24 ten-slot panels)
+    q = synth.config_problem("c2_3072x768", N=4)
+    i10 = sdnn.Plan(q.row_ptr, q.col_idx, q.vals, q.M, q.K, kernel="tmem").info()
+    i8 = sdnn.Plan(q.row_ptr, q.col_idx, q.vals, q.M, q.K, kernel="tmem", panel_rows=8).info()
+    assert (i10["num_row_blocks"], i8["num_row_blocks"]) == (13, 16) and i8["panel_rows"] == 10
+    plan8 = sdnn.Plan(q.row_ptr, q.col_idx, q.vals, q.M, q.K, kernel="tmem", panel_rows=8)
+    assert sorted(decode(q, plan8)[2]) == csr_triples(q)
     with pytest.raises(sdnn.SdnnError):
         sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem8", k_chunk=64)
     assert sdnn.Plan(p.row_ptr, p.col_idx, p.vals, p.M, p.K, kernel="tmem8", k_chunk=32).info()["kernel"] == 5
