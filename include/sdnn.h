@@ -77,9 +77,9 @@ typedef struct {
   int32_t panel_rows_max;   /* row kernel: rows per warp panel, 0 = auto, else 4 or 8 (group: 16);
                                kernel 4: 1..10 = about that many rows per warp (more row blocks of
                                the fixed 24 × 10-slot geometry; 0 = 10).  Auto handles keep a
-                               second TMEM plan at 8 rows per warp when it has more row blocks and
-                               take it per call where its grid fills the waves better (not
-                               serialized: a deserialized handle uses the 10-row plan)            */
+                               second TMEM plan with ~25 % more row blocks and take it per call
+                               where its grid fills the waves better (not serialized: a
+                               deserialized handle uses the 10-row plan)                         */
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
                                multiple of 8                                                        */

@@ -88,9 +88,9 @@ struct sdnn_handle_s {
   // auto handles (kernel = 0): the TMEM plan prepared beside the row plan; sdnn_spmm takes it when
   // the call fits its fast path and fills at least one wave of CTAs (tmem_worth)
   sdnn_handle_s* alt = nullptr;
-  // auto handles, small M: the same TMEM plan with ~8 rows per warp (more row blocks) — taken per call
+  // auto handles: the same TMEM plan with ~25 % more row blocks (fewer rows per warp) — taken per call
   // when its grid fills the GPU's waves better (tmem_pick); not serialized (rebuilt plans use alt)
-  sdnn_handle_s* alt8 = nullptr;
+  sdnn_handle_s* alt2 = nullptr;
   // auto handles: a row plan with more, smaller row blocks, for row-plan calls whose grid on the
   // main row plan is under one wave (small N: one or two N tiles)
   sdnn_handle_s* narrow = nullptr;
@@ -2112,15 +2112,16 @@ static bool tmem_worth(const sdnn_handle_s* a, const float* X, int64_t N, const 
 static sdnn_status launch_main(sdnn_handle_s* h, const float* X, int64_t N, const float* bias, int32_t act,
                                const YOut& yo, float* ws, cudaStream_t stream, float* kws = nullptr, int KS = 1,
                                bool local = false);
-// The TMEM plan of an auto call: the 10-rows-per-warp plan or, where the handle has one, the ~8-row plan
-// with more row blocks — whichever gives the smaller waves × (rows per warp + 1.5) for this N (one CTA
-// per SM; the 1.5 rows stand for a CTA's fixed fill and set-up).  Graph-timed with the 8-row plan
-// forced (profiles/r02_tmem_rows_ab.log): c2 3072×768 30.7 → 27.4 µs (104 → 128 CTAs, one wave),
-// c3 1024×512 50.3 → 44.9 µs (245 → 294 CTAs, two waves either way); c5 34.3 → 36.5 ms and c4
-// 2048×512 at 80 % 174 → 197 µs (more waves) — which the estimate rejects.
+// The TMEM plan of an auto call: the 10-rows-per-warp plan or, where the handle has one, the second
+// plan with ~25 % more row blocks — whichever gives the smaller waves × (rows per warp + 1.5) for this
+// N (one CTA per SM; the 1.5 rows stand for a CTA's fixed fill and set-up).  Graph-timed with 8 rows
+// per warp forced (profiles/r02_tmem_rows_ab.log): c2 3072×768 30.7 → 27.4 µs (104 → 128 CTAs, one
+// wave), c3 1024×512 50.3 → 44.9 µs (245 → 294 CTAs, two waves either way); c5 34.3 → 36.5 ms and c4
+// 2048×512 at 80 % 174 → 197 µs (more waves) — which the estimate rejects; c3 256×128 at 4 rows per
+// warp 7.8 → 7.2 µs (98 → 147 CTAs, profiles/r02_tmem_rows_probe.log).
 static sdnn_handle_s* tmem_pick(sdnn_handle_s* h, int64_t N) {
   sdnn_handle_s* a = h->alt;
-  sdnn_handle_s* b = h->alt8;
+  sdnn_handle_s* b = h->alt2;
   if (!a || !b) return a;
   const int64_t T = (N + tmem_tn(a->plan.kernel) - 1) / tmem_tn(a->plan.kernel);
   auto est = [&](const sdnn_handle_s* x) {
@@ -2731,12 +2732,16 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
     return fail(st, m);
   }
   (*out)->alt = alt;
-  // the ~8-rows-per-warp TMEM plan, when it has more row blocks than the 10-row one
-  if (alt && int64_t(alt->plan.num_row_blocks) < (int64_t(M) + 8 * kTmemRWarps - 1) / (8 * kTmemRWarps)) {
-    sdnn_perm_opts o8 = o;
-    o8.panel_rows_max = 8;
-    sdnn_handle alt8 = nullptr;
-    if (prepare_one(csr_ptr, col_idx, vals, M, K, &o8, &alt8, perm) == SDNN_OK) (*out)->alt8 = alt8;
+  // the second TMEM plan: ~25 % more row blocks (at least one), r = ⌈M / (24 · blocks)⌉ rows per warp
+  if (alt) {
+    const int64_t nrb1 = alt->plan.num_row_blocks, nrb2 = nrb1 + std::max<int64_t>(1, nrb1 / 4);
+    const int64_t r = (int64_t(M) + kTmemRWarps * nrb2 - 1) / (kTmemRWarps * nrb2);
+    if (r >= 1 && r < tmem_rows(4) && (int64_t(M) + kTmemRWarps * r - 1) / (kTmemRWarps * r) > nrb1) {
+      sdnn_perm_opts o2 = o;
+      o2.panel_rows_max = int32_t(r);
+      sdnn_handle alt2 = nullptr;
+      if (prepare_one(csr_ptr, col_idx, vals, M, K, &o2, &alt2, perm) == SDNN_OK) (*out)->alt2 = alt2;
+    }
   }
   // and, when the row plan has few row blocks, a row plan of 4-row panels with ≥ 64 row blocks for
   // the calls whose grid would not fill the GPU (launch: narrow_worth)
@@ -2780,7 +2785,7 @@ sdnn_status sdnn_prepare(const int32_t* csr_ptr, const int32_t* col_idx, const f
 sdnn_status sdnn_destroy(sdnn_handle h) {
   if (!h) return SDNN_OK;
   if (h->alt) sdnn_destroy(h->alt);
-  if (h->alt8) sdnn_destroy(h->alt8);
+  if (h->alt2) sdnn_destroy(h->alt2);
   if (h->narrow) sdnn_destroy(h->narrow);
   if (h->narrow4) sdnn_destroy(h->narrow4);
   int cur = -1;
