@@ -38,7 +38,10 @@ constexpr int RW = 10, NCW = 24, NFW = 4;
 
 // per chunk block: header RW words per warp (groups of 4 entries per row), then per warp a stream
 // start (16-byte units) in word [NCW * RW + warp]; streams laid out per mode
-template <int MODE>
+// SYNC > 0: the consumer warps meet at a named barrier every SYNC chunks (the product's TMEM halves
+// let a warp run at most about one chunk ahead of the slowest: per-chunk load imbalance between
+// warps then costs time)
+template <int MODE, int SYNC = 0>
 __global__ void __launch_bounds__((NCW + NFW) * 32, 1)
     meta_kernel(const uint4* __restrict__ meta_g, int blk_u4, int nblk, int chunks, float* out, long long* cyc) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -73,6 +76,7 @@ __global__ void __launch_bounds__((NCW + NFW) * 32, 1)
 #pragma unroll
     for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
     for (int j = 0; j < chunks; ++j) {
+      if (SYNC && j % SYNC == 0) asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
       const uint4* blk = ms + size_t(j % nblk) * blk_u4;
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(blk) + warp * RW;
       const uint4* e = blk + __shfl_sync(0xffffffffu, reinterpret_cast<const uint32_t*>(blk)[NCW * RW + warp], 0);
@@ -200,9 +204,8 @@ static Meta make_meta(int mode, int nblk, double density, unsigned seed) {
   return m;
 }
 
-template <int MODE>
-static void run(const char* name, int chunks) {
-  const int nblk = 8;
+template <int MODE, int SYNC = 0>
+static void run(const char* name, int chunks, int nblk = 8) {
   Meta m = make_meta(MODE, nblk, 0.1, 777);
   int sms;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -213,7 +216,7 @@ static void run(const char* name, int chunks) {
   CK(cudaMemcpy(mg, m.words.data(), m.words.size() * sizeof(uint4), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&out, sizeof(float) * sms * 1024));
   CK(cudaMalloc(&cyc, sizeof(long long) * sms * 32));
-  auto kern = meta_kernel<MODE>;
+  auto kern = meta_kernel<MODE, SYNC>;
   const size_t smem = m.words.size() * sizeof(uint4);
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   cudaFuncAttributes fa;
@@ -249,6 +252,9 @@ int main(int argc, char** argv) {
     run<0>("MODE 0 LDS.128 {c,w,c,w} /2 (product)", chunks);
     run<1>("MODE 1 LDS.128 {c0..c3} /4, const w", chunks);
     run<2>("MODE 2 LDS.128 {w0..w3} + LDS.64 16-bit cols /4", chunks);
+    run<0, 0>("MODE 0, 12 distinct blocks, no sync", chunks, 12);
+    run<0, 1>("MODE 0, 12 distinct blocks, barrier every chunk", chunks, 12);
+    run<0, 2>("MODE 0, 12 distinct blocks, barrier every 2 chunks", chunks, 12);
   }
   return 0;
 }
