@@ -6,6 +6,10 @@
 //   MODE 1  LDS.128 {c0, c1, c2, c3} per 4 entries, weight a constant        (0.25 LDS, 128 B / nz)  [timing only]
 //   MODE 2  LDS.128 {w0..w3} + LDS.64 {c0|c1, c2|c3} (16-bit TMEM columns, the
 //           warp's lane base added in the kernel) per 4 entries (32 B of smem) (0.5 LDS, 192 B / nz)
+//   MODE 4  lane-distributed metadata: one coalesced LDS.64 per 32 entries (lane l keeps entry l), each
+//           entry's col and w broadcast through the uniform datapath (SEL + REDUX.OR -> UR): no
+//           broadcast load writes the register file                          (1/32 LDS, 8 B / nz)
+//   MODE 5  columns as in MODE 4 (REDUX), weights by one broadcast LDS.128 per 4 entries  (128 B / nz) [timing only]
 // Rows padded to multiples of 4 entries in every mode; rates are per padded entry.  No fill, no TMA.
 #include <cstdint>
 #include <cstdio>
@@ -75,7 +79,10 @@ __global__ void __launch_bounds__((NCW + NFW) * 32, 1)
     float2 acc[RW][2];
 #pragma unroll
     for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+    uint2 ent = make_uint2(0u, 0u);  // MODE 4 / 5: this lane's entry of the current 32-entry window
+    int pos = 32;
     for (int j = 0; j < chunks; ++j) {
+      if (MODE >= 4) pos = 32;  // a new chunk's stream starts elsewhere: reload the window
       if (SYNC && j % SYNC == 0) asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
       const uint4* blk = ms + size_t(j % nblk) * blk_u4;
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(blk) + warp * RW;
@@ -110,6 +117,30 @@ __global__ void __launch_bounds__((NCW + NFW) * 32, 1)
             tld4(lb | (c.y & 0xffffu), xc);
             tld4(lb | (c.y >> 16), xd);
             w0 = wv.x; w1 = wv.y; w2 = wv.z; w3 = wv.w;
+            e += 2;
+          } else if constexpr (MODE == 4 || MODE == 5) {
+            if (pos == 32) {
+              ent = reinterpret_cast<const uint2*>(e)[lane];
+              pos = 0;
+            }
+            const uint32_t c0 = __reduce_or_sync(0xffffffffu, lane == pos ? ent.x : 0u);
+            const uint32_t c1 = __reduce_or_sync(0xffffffffu, lane == pos + 1 ? ent.x : 0u);
+            const uint32_t c2 = __reduce_or_sync(0xffffffffu, lane == pos + 2 ? ent.x : 0u);
+            const uint32_t c3 = __reduce_or_sync(0xffffffffu, lane == pos + 3 ? ent.x : 0u);
+            tld4(c0, xa);
+            tld4(c1, xb);
+            tld4(c2, xc);
+            tld4(c3, xd);
+            if constexpr (MODE == 4) {
+              w0 = __uint_as_float(__reduce_or_sync(0xffffffffu, lane == pos ? ent.y : 0u));
+              w1 = __uint_as_float(__reduce_or_sync(0xffffffffu, lane == pos + 1 ? ent.y : 0u));
+              w2 = __uint_as_float(__reduce_or_sync(0xffffffffu, lane == pos + 2 ? ent.y : 0u));
+              w3 = __uint_as_float(__reduce_or_sync(0xffffffffu, lane == pos + 3 ? ent.y : 0u));
+            } else {
+              const float4 wv = reinterpret_cast<const float4*>(e)[0];
+              w0 = wv.x; w1 = wv.y; w2 = wv.z; w3 = wv.w;
+            }
+            pos += 4;
             e += 2;
           } else {
             const uint32_t* c = reinterpret_cast<const uint32_t*>(e);
@@ -178,7 +209,7 @@ static Meta make_meta(int mode, int nblk, double density, unsigned seed) {
             memcpy(&wb[t], &wv, 4);
             c[t] = uint32_t(4 * k + 256 * (b & 1));
           }
-          if (mode == 0) {
+          if (mode == 0 || mode == 4 || mode == 5) {
             for (int t = 0; t < 4; ++t) { w.push_back(lb | c[t]); w.push_back(wb[t]); }
           } else if (mode == 1 || mode == 3) {
             for (int t = 0; t < 4; ++t) w.push_back(lb | c[t]);
@@ -217,7 +248,7 @@ static void run(const char* name, int chunks, int nblk = 8) {
   CK(cudaMalloc(&out, sizeof(float) * sms * 1024));
   CK(cudaMalloc(&cyc, sizeof(long long) * sms * 32));
   auto kern = meta_kernel<MODE, SYNC>;
-  const size_t smem = m.words.size() * sizeof(uint4);
+  const size_t smem = m.words.size() * sizeof(uint4) + (MODE >= 4 ? 256 : 0);  // MODE 4/5 windows read up to 31 entries past a stream
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   cudaFuncAttributes fa;
   CK(cudaFuncGetAttributes(&fa, kern));
@@ -252,6 +283,8 @@ int main(int argc, char** argv) {
     run<0>("MODE 0 LDS.128 {c,w,c,w} /2 (product)", chunks);
     run<1>("MODE 1 LDS.128 {c0..c3} /4, const w", chunks);
     run<2>("MODE 2 LDS.128 {w0..w3} + LDS.64 16-bit cols /4", chunks);
+    run<4>("MODE 4 lane-distributed LDS.64 /32, REDUX col + w", chunks);
+    run<5>("MODE 5 REDUX col, LDS.128 {w0..w3} /4", chunks);
     run<0, 0>("MODE 0, 12 distinct blocks, no sync", chunks, 12);
     run<0, 1>("MODE 0, 12 distinct blocks, barrier every chunk", chunks, 12);
     run<0, 2>("MODE 0, 12 distinct blocks, barrier every 2 chunks", chunks, 12);
