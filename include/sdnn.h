@@ -78,8 +78,8 @@ typedef struct {
                                kernel 4: 1..10 = about that many rows per warp (more row blocks of
                                the fixed 24 × 10-slot geometry; 0 = 10).  Auto handles keep a
                                second TMEM plan with ~25 % more row blocks and take it per call
-                               where its grid fills the waves better (not serialized: a
-                               deserialized handle uses the 10-row plan)                         */
+                               where its grid fills the waves better (serialized with the
+                               handle, blob role 4)                                              */
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
                                multiple of 8                                                        */
@@ -218,8 +218,8 @@ SDNN_API sdnn_status sdnn_conv2d(sdnn_handle h, const float* X, int32_t B, int32
                                  int32_t FY, int32_t FX, int32_t pad, int32_t stride, const float* bias, int32_t act,
                                  float* Y, void* stream);
 
-/* sdnn_serialize / sdnn_deserialize: the prepared handle (every plan it keeps — row, TMEM, narrow —
- * with its execution-ordered metadata) as a self-contained blob, so another process skips
+/* sdnn_serialize / sdnn_deserialize: the prepared handle (every plan it keeps — row, both TMEM plans,
+ * narrow — with its execution-ordered metadata) as a self-contained blob, so another process skips
  * Algorithm 1 and the packing (the paper's reusable preparation stage).
  *   sdnn_serialize(h, NULL, &size) stores the blob size; sdnn_serialize(h, buf, &size) writes it to
  *   the HOST buffer (SDNN_ERR_INVALID_ARGUMENT if *size is too small; *size = bytes written).

@@ -89,7 +89,7 @@ struct sdnn_handle_s {
   // the call fits its fast path and fills at least one wave of CTAs (tmem_worth)
   sdnn_handle_s* alt = nullptr;
   // auto handles: the same TMEM plan with ~25 % more row blocks (fewer rows per warp) — taken per call
-  // when its grid fills the GPU's waves better (tmem_pick); not serialized (rebuilt plans use alt)
+  // when its grid fills the GPU's waves better (tmem_pick); blob role 4
   sdnn_handle_s* alt2 = nullptr;
   // auto handles: a row plan with more, smaller row blocks, for row-plan calls whose grid on the
   // main row plan is under one wave (small N: one or two N tiles)
@@ -3218,7 +3218,7 @@ sdnn_status sdnn_get_info(sdnn_handle h, sdnn_info* info) {
 // Algorithm 1 and the packing.  Blob: "SDNNPLAN", u32 version, u32 plan count, then per plan a u32
 // role (0 main, 1 TMEM, 2 narrow, 3 narrow4) and its fields in a fixed order (little-endian, sizes as u64).
 namespace {
-constexpr uint32_t kBlobVersion = 1;
+constexpr uint32_t kBlobVersion = 2;  // 2: role 4 = the second TMEM plan
 struct BlobW {
   std::vector<uint8_t> b;
   template <class T> void s(const T& v) {
@@ -3268,8 +3268,11 @@ sdnn_status plan_with_meta(const sdnn_handle_s* h, Plan& out) {
 // Structural checks of a deserialized plan before it is uploaded and launched.
 bool plan_sane(const Plan& p, uint32_t role) {
   if (p.M < 1 || p.K < 1 || p.kernel < 1 || p.kernel > 6 || p.kernel == 3) return false;
-  // plan kind per role: 0 main (row / group / TMEM), 1 TMEM alternative, 2-3 narrow row plans
-  if ((role == 1 && p.kernel != 4 && p.kernel != 5 && p.kernel != 6) || (role >= 2 && p.kernel != 1)) return false;
+  // plan kind per role: 0 main (row / group / TMEM), 1 TMEM alternative, 2-3 narrow row plans, 4 the
+  // second TMEM plan of an auto handle (TMEM-R only: tmem_pick compares it with role 1)
+  if ((role == 1 && p.kernel != 4 && p.kernel != 5 && p.kernel != 6) || ((role == 2 || role == 3) && p.kernel != 1) ||
+      (role == 4 && p.kernel != 4))
+    return false;
   if (p.perm.size() != size_t(p.M) || p.num_row_blocks < 1 || p.num_chunks < 1 || p.k_chunk < 1) return false;
   if (p.num_chunks != (p.K + p.k_chunk - 1) / p.k_chunk) return false;
   // panel geometry the kernels are compiled for
@@ -3368,7 +3371,7 @@ extern "C" {
 
 sdnn_status sdnn_serialize(sdnn_handle h, void* buf, size_t* size) {
   if (!h || !size) return fail(SDNN_ERR_INVALID_ARGUMENT, "NULL handle or size");
-  const sdnn_handle_s* parts[4] = {h, h->alt, h->narrow, h->narrow4};
+  const sdnn_handle_s* parts[5] = {h, h->alt, h->narrow, h->narrow4, h->alt ? h->alt2 : nullptr};
   for (const sdnn_handle_s* q : parts)
     if (q && q->plan.kernel == 3)
       return fail(SDNN_ERR_UNSUPPORTED, "codegen plans are JIT-compiled from the CSR and are not serialized");
@@ -3379,8 +3382,10 @@ sdnn_status sdnn_serialize(sdnn_handle h, void* buf, size_t* size) {
     const char magic[8] = {'S', 'D', 'N', 'N', 'P', 'L', 'A', 'N'};
     w.b.insert(w.b.end(), magic, magic + 8);
     w.s(kBlobVersion);
-    w.s(uint32_t((h->alt ? 1 : 0) + (h->narrow ? 1 : 0) + (h->narrow4 ? 1 : 0) + 1));
-    for (uint32_t role = 0; role < 4; ++role) {
+    uint32_t count = 0;
+    for (const sdnn_handle_s* q : parts) count += q ? 1 : 0;
+    w.s(count);
+    for (uint32_t role = 0; role < 5; ++role) {
       if (!parts[role]) continue;
       Plan pl;
       st = plan_with_meta(parts[role], pl);
@@ -3414,9 +3419,9 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
   uint32_t ver = 0, count = 0;
   r.s(ver);
   r.s(count);
-  if (!r.ok || ver != kBlobVersion) return fail(SDNN_ERR_UNSUPPORTED, "blob version " + std::to_string(ver) + " != 1");
-  if (count < 1 || count > 4) return fail(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan count)");
-  sdnn_handle parts[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (!r.ok || ver != kBlobVersion) return fail(SDNN_ERR_UNSUPPORTED, "blob version " + std::to_string(ver) + " != " + std::to_string(kBlobVersion));
+  if (count < 1 || count > 5) return fail(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan count)");
+  sdnn_handle parts[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   auto cleanup = [&](sdnn_status s, const std::string& m) {
     for (auto& q : parts)
       if (q) sdnn_destroy(q);
@@ -3424,11 +3429,13 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
   };
   try {
     for (uint32_t i = 0; i < count; ++i) {
-      uint32_t role = 4;
+      uint32_t role = 5;
       r.s(role);
       Plan pl;
       plan_fields(r, pl);
-      if (!r.ok || role > 3 || parts[role] || (role == 3 && !parts[2]) || !plan_sane(pl, role) || (role == 0) != (i == 0))
+      if (!r.ok || role > 4 || parts[role] || (role == 3 && !parts[2]) || (role == 4 && !parts[1]) ||
+          !plan_sane(pl, role) || (role == 0) != (i == 0) ||
+          (role == 4 && (pl.M != parts[1]->plan.M || pl.K != parts[1]->plan.K || parts[1]->plan.kernel != 4)))
         return cleanup(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (plan " + std::to_string(i) + ")");
       sdnn_status st = prepare_one(nullptr, nullptr, nullptr, pl.M, pl.K, nullptr, &parts[role], nullptr, &pl);
       if (st != SDNN_OK) {
@@ -3441,6 +3448,7 @@ sdnn_status sdnn_deserialize(const void* buf, size_t size, sdnn_handle* out) {
   }
   if (r.off != size) return cleanup(SDNN_ERR_INVALID_ARGUMENT, "corrupt blob (trailing bytes)");
   parts[0]->alt = parts[1];
+  parts[0]->alt2 = parts[4];
   parts[0]->narrow = parts[2];
   parts[0]->narrow4 = parts[3];
   *out = parts[0];

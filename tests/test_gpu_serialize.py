@@ -45,7 +45,7 @@ def test_corrupt_blobs_rejected(sdnn):
     p = synth.config_problem("c1")
     blob = sdnn.Handle.from_problem(p).serialize()
     for bad in (b"", blob[:7], b"XXXXXXXX" + blob[8:], blob[:len(blob) // 2], blob + b"\0",
-                blob[:8] + (2).to_bytes(4, "little") + blob[12:]):
+                blob[:8] + (99).to_bytes(4, "little") + blob[12:]):
         with pytest.raises(sdnn.SdnnError):
             sdnn.Handle.deserialize(bad)
 
@@ -126,3 +126,28 @@ def test_corrupt_fields_rejected(sdnn):
             sdnn.Handle.deserialize(b)
         assert e.value.status == 1, i  # SDNN_ERR_INVALID_ARGUMENT
     sdnn.Handle.deserialize(blob).close()  # the unmodified blob still loads
+
+
+def test_second_tmem_plan_round_trip(sdnn):
+    """An auto handle's second TMEM plan (more row blocks, picked per call by wave fill) travels in the
+    blob as role 4, so the deserialized handle holds the same plans, and a role-4 plan without its
+    role-1 partner, of another shape or of another kernel is rejected."""
+    p = synth.config_problem("c2_3072x768")  # tmem_pick takes the second plan at N = 1024 (DESIGN §6)
+    h = sdnn.Handle.from_problem(p)
+    blob = h.serialize()
+    idx = _index(blob)
+    nplans = len({k[0] for k in idx})
+    roles = {int(np.frombuffer(blob, "u4", 1, idx[(i, "role")][0])[0]): i for i in range(nplans)}
+    assert 1 in roles and 4 in roles
+    rb = lambda i: int(np.frombuffer(blob, "i4", 1, idx[(i, "num_row_blocks")][0])[0])
+    assert rb(roles[4]) > rb(roles[1])
+    h2 = sdnn.Handle.deserialize(blob)
+    assert h2.serialize() == blob  # every plan, the second TMEM plan included, came back
+    X = torch.from_numpy(p.x()).cuda()
+    b = torch.from_numpy(p.bias).cuda()
+    assert h2.kernel_for(p.N, X.data_ptr()) == h.kernel_for(p.N, X.data_ptr()) == 4
+    np.testing.assert_array_equal(h2.spmm(X, b, act=1).cpu().numpy(), h.spmm(X, b, act=1).cpu().numpy())
+    for bad in (_patch(blob, idx, roles[4], "kernel", 1), _patch(blob, idx, roles[4], "M", p.M - 1),
+                _patch(blob, idx, roles[4], "role", 1), _patch(blob, idx, roles[1], "role", 4)):
+        with pytest.raises(sdnn.SdnnError):
+            sdnn.Handle.deserialize(bad)
