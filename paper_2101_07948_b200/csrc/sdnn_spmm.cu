@@ -2070,8 +2070,14 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
     const char* e = getenv("SDNN_TMEM_PERSIST");
     return e ? atoi(e) : -1;
   }();
+  // Even chunk counts only (forced or not): a chunk's TMEM half is packed into the metadata as the parity
+  // of its index within the K range, while the persistent pipeline alternates halves over the CTA's
+  // whole chunk stream — with an odd count every second item would read the other half (found by
+  // tools/fuzz.py: K = 2, 64, 192, 300, 448 over >= 4 items per SM gave wrong Y from the CTA's second
+  // item on; tests/test_gpu_parity.py::test_short_k_many_items).
   const bool persist_auto = nblocks >= 4 * int64_t(h->sms) && pl.num_chunks <= 8;
-  const bool persist = rep && !prs && !multi && (persist_env > 0 || (persist_env < 0 && persist_auto));
+  const bool persist = rep && !prs && !multi && pl.num_chunks % 2 == 0 &&
+                       (persist_env > 0 || (persist_env < 0 && persist_auto));
   if (persist) {
     const unsigned pg = unsigned(std::min<int64_t>(nblocks, h->sms));
     if (h->tmem_runs_only)

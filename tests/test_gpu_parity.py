@@ -458,6 +458,35 @@ if given is not None:
         check(sdnn, oracle_mod, p, X=X, act=int(seed % 2), kernel=kernel)
 
 
+@pytest.mark.parametrize("K", [2, 64, 65, 128, 192, 256, 300, 448, 512])
+@pytest.mark.parametrize("kernel,mask", [("auto", "uniform"), ("tmem", "blocks4")])
+def test_short_k_many_items(sdnn, oracle_mod, K, kernel, mask):
+    """Short K ranges (1-8 chunks of 64, odd and even counts) over >= 4 (row block, N tile) items per SM:
+    the calls the launch rules may run on persistent TMEM-R CTAs.  Regression: with an odd chunk count
+    the persistent pipeline's alternating TMEM halves disagreed with the half packed into the metadata
+    from a CTA's second item on (found by tools/fuzz.py); odd counts now launch one CTA per item."""
+    M, N = 2274, 7808  # 10 row blocks x 61 N tiles = 610 items > 4 x 148 SMs
+    rng = np.random.default_rng(1000 + K)
+    if mask == "blocks4":
+        m = np.repeat(rng.random((M, (K + 3) // 4)) < 0.15, 4, axis=1)[:, :K]
+    else:
+        m = rng.random((M, K)) < 0.1
+    rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum(m.sum(1))
+    ci = np.nonzero(m)[1].astype(np.int32)
+    v = (0.05 * rng.standard_normal(ci.size)).astype(np.float32)
+    v[v == 0] = 0.01
+    b = (0.1 * rng.standard_normal(M)).astype(np.float32)
+    p = synth.Problem("shortk", M, K, N, 0, "x", rp, ci, v, b, 1, K)
+    X = rng.standard_normal((K, N)).astype(np.float32)
+    _, Y, h = check(sdnn, oracle_mod, p, X=X, kernel=kernel)
+    assert h.kernel_for(N) == 4
+    # permuted output (the chained-layer form) through the same launch
+    hp = sdnn.Handle.from_problem(p, kernel=kernel, permuted_output=True)
+    perm = hp.permutation()
+    Yp = hp.spmm(torch.from_numpy(X).cuda(), torch.from_numpy(np.ascontiguousarray(b[perm])).cuda(), act=1).cpu().numpy()
+    np.testing.assert_array_equal(Yp, Y[perm])
+
+
 if given is not None:
     @settings(max_examples=10, deadline=None, suppress_health_check=list(HealthCheck))
     @given(M=st.integers(16, 1500), K=st.integers(1024, 4096), n4=st.integers(1, 50), dens=st.sampled_from([0.02, 0.1, 0.2]),
