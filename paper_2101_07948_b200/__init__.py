@@ -234,7 +234,15 @@ class Handle:
         if OC >= 64 and not opts.get("panel_rows") and not opts.get("cta_panels"):
             opts["cta_panels"] = 8
         opts.setdefault("split_rows", False)
-        return cls(row_ptr, col_idx, vals, OC, IC * fyx, **opts)
+        try:
+            return cls(row_ptr, col_idx, vals, OC, IC * fyx, **opts)
+        except SdnnError as e:
+            # a whole-channel chunk that does not fit the stage ring (e.g. 3×5 filters: 120 columns): the
+            # library's own chunk choice instead
+            if e.status != 3 or not opts.get("k_chunk") or opts["k_chunk"] != kc:
+                raise
+            opts["k_chunk"] = 0
+            return cls(row_ptr, col_idx, vals, OC, IC * fyx, **opts)
 
     def conv2d_tune(self, X, FY: int = 3, FX: int = 3, pad: int = 1, stride: int = 1, stream=None) -> dict:
         """sdnn_conv2d_tune for X's geometry: {"pixels": 2 | 4 | 0 (rules) | -2 (explicit form: virtual

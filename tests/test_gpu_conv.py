@@ -40,7 +40,8 @@ def test_conv_suite_parity(sdnn, OC, IC, HW, B, sp):
     run(sdnn, synth.make_conv_problem(f"cs{OC}_{IC}_{HW}", OC, IC, HW, HW, B, sp))
 
 
-@pytest.mark.parametrize("FY,FX,pad,stride", [(3, 3, 0, 1), (3, 3, 1, 2), (5, 5, 2, 1), (1, 1, 0, 1), (1, 3, 0, 1)])
+@pytest.mark.parametrize("FY,FX,pad,stride", [(3, 3, 0, 1), (3, 3, 1, 2), (5, 5, 2, 1), (1, 1, 0, 1), (1, 3, 0, 1),
+                                                 (3, 5, 2, 2)])  # 3×5: a whole-channel chunk (120) does not fit → the library's own chunks
 def test_conv_shapes(sdnn, FY, FX, pad, stride):
     run(sdnn, synth.make_conv_problem(f"sh{FY}{FX}{pad}{stride}", 48, 24, 13, 11, 2, 0.85, FY=FY, FX=FX, pad=pad,
                                       stride=stride))

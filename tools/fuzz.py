@@ -53,6 +53,7 @@ def main() -> int:
     ap.add_argument("--max-n", type=int, default=8192)
     ap.add_argument("--max-gflop", type=float, default=12.0)
     ap.add_argument("--big", action="store_true", help="M, K in [400, max-dim], N a multiple of 4 in [512, max-n]")
+    ap.add_argument("--wide-n", action="store_true", help="short K (1-12 chunks), many N tiles: persistent / wave-fill rules")
     args = ap.parse_args()
 
     import torch
@@ -73,6 +74,10 @@ def main() -> int:
         if args.big:
             M, K = int(rng.integers(400, args.max_dim + 1)), int(rng.integers(400, args.max_dim + 1))
             N = int(rng.integers(128, args.max_n // 4 + 1)) * 4 if rng.random() < 0.5 else 128 * int(rng.integers(4, args.max_n // 128 + 1))
+        if args.wide_n:
+            M = int(rng.integers(100, args.max_dim + 1))
+            K = int(np.clip(64 * int(rng.integers(1, 13)) + int(rng.choice([0, 0, -1, 1, -30])), 1, None))
+            N = 128 * int(rng.integers(8, max(9, args.max_n // 128 + 1))) + int(rng.choice([0, 0, 0, 4, 64, 1]))
         dens = float(rng.choice([0.0, 0.005, 0.02, 0.05, 0.1, 0.2, 0.5, 1.0], p=[.03, .1, .15, .2, .25, .15, .09, .03]))
         while 2.0 * dens * M * K * N > args.max_gflop * 1e9 and N > 128:
             N //= 2
