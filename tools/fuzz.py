@@ -91,8 +91,13 @@ def main() -> int:
         use_bias, act = bool(rng.random() < 0.8), int(rng.random() < 0.7)
         b = (0.1 * rng.standard_normal(M)).astype(np.float32) if use_bias else None
         X = rng.standard_normal((K, N)).astype(np.float32)
-        kernel = str(rng.choice(["auto", "auto", "auto", "auto", "row", "tmem", "tmemp", "tmem8"]))
+        kernel = str(rng.choice(["auto", "auto", "auto", "auto", "row", "tmem", "tmemp", "tmem8", "group"]))
         opts = dict(kernel=kernel, permute=bool(rng.random() < 0.9))
+        if kernel == "group":
+            opts["group_sb"] = int(rng.choice([0, 1, 2, 4]))
+        if kernel == "row" and rng.random() < 0.5:
+            opts.update(panel_rows=int(rng.choice([4, 8])), cta_panels=int(rng.choice([1, 2, 4, 8, 16])),
+                        k_chunk=int(rng.choice([0, 8, 32, 64, 128])))
         if rng.random() < 0.15:
             opts["split_k"] = False
         if rng.random() < 0.15:
