@@ -82,7 +82,10 @@ typedef struct {
                                handle, blob role 4)                                              */
   int32_t cta_panels;       /* panels (warps) per CTA row block: 0 = auto, else 1..16                */
   int32_t k_chunk;          /* reduction-dimension tile (split-K tiling): 0 = auto, else 8..128,
-                               multiple of 8                                                        */
+                               multiple of 8.  An explicit chunk must fit two pipeline stages (its X
+                               tile at the widest N tile, 1 KB per K row, plus its largest metadata
+                               block) in 220 KB of shared memory — about 104 at most; beyond that
+                               sdnn_prepare returns SDNN_ERR_UNSUPPORTED                            */
   int32_t group_sb;         /* group kernel sub-block rows: 0 = auto (cost model), 1, 2 or 4         */
   uint32_t flags;           /* SDNN_FLAG_NO_ROW_SPLIT | SDNN_FLAG_PERMUTED_OUTPUT | SDNN_FLAG_NO_SPLIT_K */
 } sdnn_perm_opts;

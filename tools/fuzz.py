@@ -97,7 +97,7 @@ def main() -> int:
             opts["group_sb"] = int(rng.choice([0, 1, 2, 4]))
         if kernel == "row" and rng.random() < 0.5:
             opts.update(panel_rows=int(rng.choice([4, 8])), cta_panels=int(rng.choice([1, 2, 4, 8, 16])),
-                        k_chunk=int(rng.choice([0, 8, 32, 64, 128])))
+                        k_chunk=int(rng.choice([0, 8, 32, 64, 96])))
         if rng.random() < 0.15:
             opts["split_k"] = False
         if rng.random() < 0.15:
