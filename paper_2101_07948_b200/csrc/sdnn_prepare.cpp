@@ -49,16 +49,22 @@ sdnn_status validate_csr(const int32_t* csr_ptr, const int32_t* col_idx, int32_t
 // Algorithm 1.  line 4: the first row is the one with most nonzeros; line 8: each next
 // row maximises |nnz(B[i-1]) ∩ nnz(A[x])| over the remaining rows.  Ties → lowest original index
 // (readings C2/C3).  Inverted index: per step, every row sharing a column with the previous row gets
-// +1 per shared column, then one argmax scan over the remaining rows — O(Σ_c colnnz(c)^2 + M^2).
+// +1 per shared column.  Two ways to take the argmax, chosen per step by the number T of list entries
+// the previous row's columns hold (both give the argmax scan's order, row for row):
+//  * T ≥ M/2 (dense patterns, c5): plain increment / reset loops and one scan over the remaining rows;
+//  * T < M/2 (tall sparse matrices): only the touched rows can have a positive overlap, so the argmax
+//    runs over them (lowest index among equals) and, when no remaining row is touched, the answer is the
+//    lowest remaining index (a moving pointer) — no M² term: 100 000 rows of ~4 nonzeros take 5 s
+//    instead of 33 s.
+// Placed rows leave the column lists when a list is walked in the second mode, and everywhere each time
+// the number of remaining rows has halved (O(nnz·log M) in total).
 void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32_t K, int32_t* order) {
   std::vector<int32_t> col_ptr(K + 1, 0), col_rows(csr_ptr[M]);
   for (int32_t p = 0; p < csr_ptr[M]; ++p) col_ptr[col_idx[p] + 1]++;
   for (int32_t c = 0; c < K; ++c) col_ptr[c + 1] += col_ptr[c];
-  {
-    std::vector<int32_t> fill(col_ptr.begin(), col_ptr.end() - 1);
-    for (int32_t m = 0; m < M; ++m)
-      for (int32_t p = csr_ptr[m]; p < csr_ptr[m + 1]; ++p) col_rows[fill[col_idx[p]]++] = m;
-  }
+  std::vector<int32_t> col_end(col_ptr.begin(), col_ptr.end() - 1);  // live end of each column's list
+  for (int32_t m = 0; m < M; ++m)
+    for (int32_t p = csr_ptr[m]; p < csr_ptr[m + 1]; ++p) col_rows[col_end[col_idx[p]]++] = m;
   std::vector<uint8_t> rem(M, 1);
   std::vector<int32_t> cnt(M, 0);
   int32_t row = 0;
@@ -66,18 +72,56 @@ void algorithm1(const int32_t* csr_ptr, const int32_t* col_idx, int32_t M, int32
     if (csr_ptr[x + 1] - csr_ptr[x] > csr_ptr[row + 1] - csr_ptr[row]) row = x;
   order[0] = row;
   rem[row] = 0;
+  int32_t lo = 0;              // lowest remaining row index
+  int32_t next_compact = M / 2;  // remaining rows at which every list is compacted next
   for (int32_t i = 1; i < M; ++i) {
     const int32_t prev = order[i - 1];
-    for (int32_t p = csr_ptr[prev]; p < csr_ptr[prev + 1]; ++p) {
-      const int32_t c = col_idx[p];
-      for (int32_t q = col_ptr[c]; q < col_ptr[c + 1]; ++q) cnt[col_rows[q]]++;
+    if (M - i <= next_compact && next_compact > 0) {
+      for (int32_t c = 0; c < K; ++c) {
+        int32_t w = col_ptr[c];
+        for (int32_t q = col_ptr[c]; q < col_end[c]; ++q)
+          if (rem[col_rows[q]]) col_rows[w++] = col_rows[q];
+        col_end[c] = w;
+      }
+      next_compact /= 2;
     }
+    while (!rem[lo]) ++lo;
+    int64_t T = 0;
+    for (int32_t p = csr_ptr[prev]; p < csr_ptr[prev + 1]; ++p) T += col_end[col_idx[p]] - col_ptr[col_idx[p]];
     int32_t best = -1, arg = -1;
-    for (int32_t x = 0; x < M; ++x)
-      if (rem[x] && cnt[x] > best) { best = cnt[x]; arg = x; }
-    for (int32_t p = csr_ptr[prev]; p < csr_ptr[prev + 1]; ++p) {
-      const int32_t c = col_idx[p];
-      for (int32_t q = col_ptr[c]; q < col_ptr[c + 1]; ++q) cnt[col_rows[q]] = 0;
+    if (2 * T >= M) {
+      for (int32_t p = csr_ptr[prev]; p < csr_ptr[prev + 1]; ++p) {
+        const int32_t c = col_idx[p];
+        for (int32_t q = col_ptr[c]; q < col_end[c]; ++q) cnt[col_rows[q]]++;
+      }
+      for (int32_t x = lo; x < M; ++x)
+        if (rem[x] && cnt[x] > best) { best = cnt[x]; arg = x; }
+      for (int32_t p = csr_ptr[prev]; p < csr_ptr[prev + 1]; ++p) {
+        const int32_t c = col_idx[p];
+        for (int32_t q = col_ptr[c]; q < col_end[c]; ++q) cnt[col_rows[q]] = 0;
+      }
+    } else {
+      for (int32_t p = csr_ptr[prev]; p < csr_ptr[prev + 1]; ++p) {
+        const int32_t c = col_idx[p];
+        int32_t w = col_ptr[c];
+        for (int32_t q = col_ptr[c]; q < col_end[c]; ++q) {
+          const int32_t r = col_rows[q];
+          if (!rem[r]) continue;  // placed since this list was last compacted: drop it
+          col_rows[w++] = r;
+          cnt[r]++;
+        }
+        col_end[c] = w;
+      }
+      best = 0;
+      for (int32_t p = csr_ptr[prev]; p < csr_ptr[prev + 1]; ++p) {
+        const int32_t c = col_idx[p];
+        for (int32_t q = col_ptr[c]; q < col_end[c]; ++q) {
+          const int32_t r = col_rows[q], n = cnt[r];  // 0 on a row's later visits: never a candidate
+          if (n > best || (n == best && n > 0 && r < arg)) { best = n; arg = r; }
+          cnt[r] = 0;
+        }
+      }
+      if (arg < 0) arg = lo;  // no remaining row shares a column with the previous one
     }
     order[i] = arg;
     rem[arg] = 0;
