@@ -2216,6 +2216,7 @@ static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const Y
 // 96 µs, 768×3072 N = 2048 95 → 67 µs, 512×4096 N = 2048 91 → 48 µs; 768×3072 / 512×4096 at N = 128
 // (4 / 3 row blocks) stay on the row plan's split-K (22.2 / 19.9 → 14.7 / 13.0 µs).
 // SDNN_TMEM_SPLIT_K=0 disables it.
+static sdnn_handle_s* narrow_pick(const sdnn_handle_s* h, int64_t N);
 static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo) {
   const sdnn_handle_s* a = h->alt;
   if (!a || h->plan.no_split_k || !h->ws_pool) return 0;
@@ -2231,12 +2232,21 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   const int64_t grid = int64_t(ap.num_row_blocks) * ((N + TN - 1) / TN);
   if (10 * grid >= 9 * int64_t(h->sms) || ap.num_chunks < 16) return 0;
   const bool dense = 5 * ap.nnz >= int64_t(ap.M) * ap.K;
-  if (N < 2 * TN && ap.num_chunks < (dense ? 32 : 48)) return 0;
+  // The row plan this call would otherwise take cannot split K when it has split rows (heavy rows of a
+  // log-normal pattern: their pieces are summed inside the CTA) — its one CTA per row block then walks
+  // the whole K range.  There the TMEM split wins from 32 chunks and from 16 split CTAs on (c2 768×3072
+  // at N = 128, the BERT FFN down projection at 128 tokens: row plan 42.1 µs, 8 TMEM slices of 4 row
+  // blocks 20.6 µs; 537×3333 and 1068×2578 log-normal at N = 128: 32 → 18 µs, 34 → 21 µs;
+  // profiles/r02_s4_tune_gap.log).
+  const sdnn_handle_s* rp = narrow_pick(h, N);
+  const bool row_cannot_split = !(rp ? rp : h)->plan.split_row.empty();
+  if (N < 2 * TN && ap.num_chunks < (dense || row_cannot_split ? 32 : 48)) return 0;
   const int64_t pairs = (ap.num_chunks + 1) / 2;
   // at most one CTA per SM in total: a second partial wave of split CTAs doubles the time (768×3072,
   // N = 1024: 5 slices of 32 CTAs = 160 CTAs, 55 µs against 39 µs at 4 slices)
   const int64_t ks = std::min<int64_t>({8, pairs / 2, int64_t(h->sms) / grid});
-  if (ks < 2 || 3 * grid * ks < h->sms) return 0;
+  if (ks < 2) return 0;
+  if (3 * grid * ks < h->sms && !(row_cannot_split && ks >= 4 && grid * ks >= 16)) return 0;
   return int(ks);
 }
 static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
