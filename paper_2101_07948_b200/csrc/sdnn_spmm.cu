@@ -2234,9 +2234,10 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   const bool dense = 5 * ap.nnz >= int64_t(ap.M) * ap.K;
   // The row plan this call would otherwise take cannot split K when it has split rows (heavy rows of a
   // log-normal pattern: their pieces are summed inside the CTA) — its one CTA per row block then walks
-  // the whole K range.  There the TMEM split wins from 32 chunks and from 16 split CTAs on (c2 768×3072
+  // the whole K range.  There the TMEM split wins from 32 chunks and from 8 split CTAs on (c2 768×3072
   // at N = 128, the BERT FFN down projection at 128 tokens: row plan 42.1 µs, 8 TMEM slices of 4 row
-  // blocks 20.6 µs; 537×3333 and 1068×2578 log-normal at N = 128: 32 → 18 µs, 34 → 21 µs;
+  // blocks 20.6 µs; 537×3333 and 1068×2578 log-normal at N = 128: 32 → 18 µs, 34 → 21 µs; one row block,
+  // 70-97 × 2655: 30-39 → 16-18 µs;
   // profiles/r02_s4_tune_gap.log).
   const sdnn_handle_s* rp = narrow_pick(h, N);
   const bool row_cannot_split = !(rp ? rp : h)->plan.split_row.empty();
@@ -2246,7 +2247,7 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   // N = 1024: 5 slices of 32 CTAs = 160 CTAs, 55 µs against 39 µs at 4 slices)
   const int64_t ks = std::min<int64_t>({8, pairs / 2, int64_t(h->sms) / grid});
   if (ks < 2) return 0;
-  if (3 * grid * ks < h->sms && !(row_cannot_split && ks >= 4 && grid * ks >= 16)) return 0;
+  if (3 * grid * ks < h->sms && !(row_cannot_split && ks >= 4 && grid * ks >= 8)) return 0;
   return int(ks);
 }
 static bool narrow_worth(const sdnn_handle_s* h, int64_t N) {
