@@ -2230,7 +2230,11 @@ static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, con
   const Plan& ap = a->plan;
   const int64_t TN = tmem_tn(ap.kernel);
   const int64_t grid = int64_t(ap.num_row_blocks) * ((N + TN - 1) / TN);
-  if (10 * grid >= 9 * int64_t(h->sms) || ap.num_chunks < 16) return 0;
+  // K ranges of 8-15 chunks split too (in two: ≥ 2 chunk pairs per slice) once the call is large enough
+  // for the second kernel not to matter (≥ 1e8 multiply-adds): 1059×578 80 % at N = 1152 37.8 → 27 µs,
+  // c2 3072×768 at N = 512 27.8 → 24.7 µs (tools/tune_gap.py, profiles/r02_s4_tune_gap.log)
+  const int min_chunks = double(ap.nnz) * double(N) >= 1e8 ? 8 : 16;
+  if (10 * grid >= 9 * int64_t(h->sms) || ap.num_chunks < min_chunks) return 0;
   const bool dense = 5 * ap.nnz >= int64_t(ap.M) * ap.K;
   // The row plan this call would otherwise take cannot split K when it has split rows (heavy rows of a
   // log-normal pattern: their pieces are summed inside the CTA) — its one CTA per row block then walks
