@@ -2209,12 +2209,14 @@ static int splitk_for(const sdnn_handle_s* h, int64_t N, const float* X, const Y
 }
 // TMEM plan with split-K: a call on the TMEM fast path whose grid is under 0.9 of a wave runs over
 // KS ≤ 8 slices of K (cut at even chunks, ≥ 2 chunk pairs each), KS = ⌊SMs / grid⌋, then the
-// slice-ordered reduction — when K has ≥ 16 chunks (shorter ranges: the unsplit kernel or the row
-// plans), at a single N tile only for long K (≥ 48 chunks; ≥ 32 with ≥ 20 % nonzeros), and when the
-// split grid reaches a third of a wave.  Re-derived for the TMEM-R kernel from sdnn_tune over the
+// slice-ordered reduction — when K has ≥ 16 chunks (≥ 8 for calls of ≥ 1e8 multiply-adds; shorter
+// ranges: the unsplit kernel or the row plans), at a single N tile only for long K (≥ 48 chunks; ≥ 32
+// with ≥ 20 % nonzeros or when the row plan has split rows and so cannot split K itself), and when the
+// split grid reaches a third of a wave (8 CTAs in that last case).  Re-derived for the TMEM-R kernel from sdnn_tune over the
 // BASELINE configs and the round-1 shape grid (profiles/r02_tune_rules*.log): 4096² N = 512 146 →
 // 96 µs, 768×3072 N = 2048 95 → 67 µs, 512×4096 N = 2048 91 → 48 µs; 768×3072 / 512×4096 at N = 128
-// (4 / 3 row blocks) stay on the row plan's split-K (22.2 / 19.9 → 14.7 / 13.0 µs).
+// (4 / 3 row blocks) stayed on the row plan's split-K (22.2 / 19.9 → 14.7 / 13.0 µs) until plans with
+// split rows stopped splitting K (session 4: see row_cannot_split below).
 // SDNN_TMEM_SPLIT_K=0 disables it.
 static sdnn_handle_s* narrow_pick(const sdnn_handle_s* h, int64_t N);
 static int tmem_split_for(const sdnn_handle_s* h, const float* X, int64_t N, const YOut& yo) {
