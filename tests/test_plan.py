@@ -219,6 +219,26 @@ def test_c_alg1_equals_bruteforce_random(oracle_mod, seed):
     assert order == oracle_mod.alg1_bruteforce([set(np.flatnonzero(mask[i]).tolist()) for i in range(M)])
 
 
+@pytest.mark.parametrize("M,K,per_row,seed", [(3000, 50, 3, 0), (5000, 8, 1, 1), (2000, 400, 2, 2), (4000, 64, 0.3, 3),
+                                              (1500, 1500, 40, 4), (2500, 30, 6, 5)])
+def test_c_alg1_tall_sparse_equals_oracle(oracle_mod, M, K, per_row, seed):
+    """Algorithm 1's two argmax modes (rows touched by the previous row when they are few, a plain scan
+    otherwise) and its list compaction give the oracle's order on tall sparse matrices, where steps switch
+    between the modes — with duplicate rows (ties: lowest index), empty rows and runs of rows that share
+    no column with their predecessor (the lowest-remaining-index pointer)."""
+    rng = np.random.default_rng(seed)
+    counts = np.minimum(K, rng.poisson(per_row, size=M))
+    counts[rng.integers(0, M, M // 10)] = 0                     # empty rows
+    cols = [np.sort(rng.choice(K, size=int(n), replace=False)) for n in counts]
+    for dst, src in zip(rng.integers(0, M, M // 8), rng.integers(0, M, M // 8)):  # duplicates → ties
+        cols[dst] = cols[src]
+    rp = np.zeros(M + 1, np.int32); rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = (np.concatenate(cols) if rp[-1] else np.zeros(0)).astype(np.int32)
+    order = sdnn.permutation(rp, ci, M, K)
+    assert sorted(order.tolist()) == list(range(M))
+    np.testing.assert_array_equal(order, oracle_mod.alg1(rp, ci, M, K))
+
+
 @pytest.mark.parametrize("key,opts", [
     ("c1", {}), ("c1", dict(permute=False)), ("c2_768x3072", {}), ("c3_128x64", dict(panel_rows=8, cta_panels=3)),
     ("c4_512x2048_s80", dict(k_chunk=8)), ("c3_256x128", dict(k_chunk=96, cta_panels=1)),
