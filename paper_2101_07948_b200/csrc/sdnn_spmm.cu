@@ -2073,7 +2073,7 @@ static sdnn_status launch_tmem(sdnn_handle_s* h, const float* X, int64_t N, cons
   // Even chunk counts only (forced or not): a chunk's TMEM half is packed into the metadata as the parity
   // of its index within the K range, while the persistent pipeline alternates halves over the CTA's
   // whole chunk stream — with an odd count every second item would read the other half (found by
-  // tools/fuzz.py: K = 2, 64, 192, 300, 448 over >= 4 items per SM gave wrong Y from the CTA's second
+  // tests/stress/fuzz.py: K = 2, 64, 192, 300, 448 over >= 4 items per SM gave wrong Y from the CTA's second
   // item on; tests/test_gpu_parity.py::test_short_k_many_items).
   const bool persist_auto = nblocks >= 4 * int64_t(h->sms) && pl.num_chunks <= 8;
   const bool persist = rep && !prs && !multi && pl.num_chunks % 2 == 0 &&

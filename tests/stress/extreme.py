@@ -3,7 +3,7 @@ use): very tall / very wide W, one row / one column, K beyond 16-bit columns, M 
 kernels' gridDim.y, N = 1, N beyond 2^20, a fully dense and an almost empty W, Y beyond 2^31 elements
 (sampled columns).  One line per case; exit code 1 on any failure.
 
-  python tools/extreme.py > gpurun_out/extreme.log
+  python tests/stress/extreme.py > gpurun_out/extreme.log
 """
 from __future__ import annotations
 
@@ -12,7 +12,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import oracle  # noqa: E402  (the checker; this tool is test infrastructure)
 

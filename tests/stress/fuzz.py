@@ -3,7 +3,7 @@ test in tests/test_gpu_parity.py: M, K up to 5000, N up to 8192, heavy-tailed ro
 per-call rules can reach — TMEM-R / second TMEM plan / persistent / split-K / row / narrow / narrow4 /
 V = 2 — with guard zones around Y, repeat-run determinism, sdnn_tune and a serialize round trip).
 
-  python tools/fuzz.py --n 300 --seed 1 > gpurun_out/fuzz.log
+  python tests/stress/fuzz.py --n 300 --seed 1 > gpurun_out/fuzz.log
 Prints one line per case and a summary; exit code 1 if any case failed.
 """
 from __future__ import annotations
@@ -15,7 +15,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402  (the checker; this tool is test infrastructure)

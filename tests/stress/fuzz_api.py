@@ -1,10 +1,10 @@
-"""Randomised stress of the other entry points against the oracle on a GPU (companion of tools/fuzz.py):
+"""Randomised stress of the other entry points against the oracle on a GPU (companion of tests/stress/fuzz.py):
 sdnn_conv2d (random geometry: 1x1..5x5, stride 1-2, pad 0-2, ragged images, with / without
 sdnn_conv2d_tune), sdnn_spmm_host (random block sizes), Chain (2-3 layers with the permutation carried
 across layers) and sdnn_spmm_multi (several destinations, leading dimension > N, column offset; guard
 columns checked).
 
-  python tools/fuzz_api.py --n 200 --seed 1 > gpurun_out/fuzz_api.log
+  python tests/stress/fuzz_api.py --n 200 --seed 1 > gpurun_out/fuzz_api.log
 """
 from __future__ import annotations
 
@@ -15,7 +15,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402  (the checker; this tool is test infrastructure)

@@ -3,7 +3,7 @@ call sdnn_spmm / sdnn_spmm_host with different N (row plan, split-K workspace, T
 persistent) in a loop; every result must be bitwise the single-threaded one (ctypes drops the GIL, so
 the calls really overlap).
 
-  python tools/fuzz_threads.py --threads 4 --iters 60 > gpurun_out/fuzz_threads.log
+  python tests/stress/fuzz_threads.py --threads 4 --iters 60 > gpurun_out/fuzz_threads.log
 """
 from __future__ import annotations
 
@@ -14,7 +14,7 @@ import threading
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import sdnn_synth as synth  # noqa: E402
 

@@ -464,7 +464,7 @@ def test_short_k_many_items(sdnn, oracle_mod, K, kernel, mask):
     """Short K ranges (1-8 chunks of 64, odd and even counts) over >= 4 (row block, N tile) items per SM:
     the calls the launch rules may run on persistent TMEM-R CTAs.  Regression: with an odd chunk count
     the persistent pipeline's alternating TMEM halves disagreed with the half packed into the metadata
-    from a CTA's second item on (found by tools/fuzz.py); odd counts now launch one CTA per item."""
+    from a CTA's second item on (found by tests/stress/fuzz.py); odd counts now launch one CTA per item."""
     M, N = 2274, 7808  # 10 row blocks x 61 N tiles = 610 items > 4 x 148 SMs
     rng = np.random.default_rng(1000 + K)
     if mask == "blocks4":
